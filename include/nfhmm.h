@@ -1,0 +1,147 @@
+/*
+ * nfhmm.h -- C-ABI of libnfhmm: B200-native (sm_100a) variational inference for the Bayesian
+ * non-negative factorial HMM of Mysore & Sahani, "Variational Inference in Non-negative Factorial
+ * Hidden Markov Models for Efficient Audio Source Separation", ICML 2012 (arXiv 1206.6468).
+ *
+ * Citation keys: "P:n" = line n of PAPER.md (the paper text), "S:n" = line n of SPEC.md,
+ * "DESIGN Rn" = reading n in DESIGN.md section "Readings of the paper".
+ *
+ * What one call of nfhmm_vb_iterate computes, per mixture and per sweep ("We iterate over
+ * Eqs. 6, 7, 8, and the forward-backward algorithm for each source"; order z -> alpha -> phi -> FB,
+ * DESIGN R6):
+ *   Eq. 7  z_{t,l,k} = beta_l(k) exp(psi(alpha_{t,k}) - psi(sum_k alpha_{t,k})) / V_hat_{t,l},
+ *                  V_hat_{t,l} = sum_k beta_l(k) exp(psi(alpha_{t,k}) - psi(sum_k alpha_{t,k}))
+ *                  (z is never materialised: only V / V_hat is needed);
+ *   Eq. 6  alpha_{t,k} = sum_l V_lt z_{t,l,k} + gamma sum_{s,n} d_{t,n}^{(s)} B_snk + 1;
+ *   Eq. 8  phi_{t,n}^{(s)} = sum_k B_snk (psi(alpha_{t,k}) - psi(sum_k alpha_{t,k}));
+ *   forward-backward per source on log-likelihood gamma * phi (DESIGN R1) -> d;
+ *   the variational bound L (closed form DESIGN R8) per sweep, FP64.
+ * nfhmm_separate computes Section 4: V_src^(s) = v_t sum_{k in s} beta_l(k) E[theta_tk],
+ * E[theta] = alpha / sum alpha (DESIGN R9), and V*^(s) = V V_src^(s) / sum_s' V_src^(s').
+ *
+ * Dimensions: F frequency bins (l), T frames (t), S sources (s), N states per source (n), K elements
+ * per state dictionary; Kt = S*N*K global elements, ordered k = (s*N + n)*K + j, so
+ * B_snk = 1 iff floor(k / K) == s*N + n (sources do not share elements).
+ *
+ * Pointers: every array argument may be a HOST pointer (pageable or pinned) or a DEVICE pointer on
+ * the handle's device; the library tells them apart with cudaPointerGetAttributes and copies with
+ * cudaMemcpy*Async on the handle's stream.  All arrays are dense row-major FP32 (FP64 where stated).
+ * Ownership: inputs are borrowed for the duration of the call only (copied into the workspace);
+ * outputs go to caller-allocated buffers; the handle owns nothing the caller passed in.
+ * Threading: a handle is single-threaded; handles on different devices are independent.
+ * Errors: every function returns an NFHMM_* status; nothing aborts or throws across the ABI; the
+ * detail of the last failure is in nfhmm_last_error().  Device-side conditions (zero support,
+ * non-finite values) are sticky flags read once per nfhmm_vb_iterate / nfhmm_sync.
+ */
+#ifndef NFHMM_H
+#define NFHMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NFHMM_OK 0
+#define NFHMM_EINVAL (-1)        /* bad dimension, NULL where required, negative/non-finite input,
+                                    dictionary column / transition row / prior not normalised (1e-4) */
+#define NFHMM_ESTATE (-2)        /* call order violated: create -> [workspace] -> model -> observations
+                                    -> iterate -> posteriors / separate */
+#define NFHMM_ECUDA (-3)         /* CUDA runtime error; text in nfhmm_last_error */
+#define NFHMM_ENOMEM (-4)        /* workspace too small / allocation failed */
+#define NFHMM_EZEROSUPPORT (-5)  /* some V_lt > 0 with V_hat_lt = 0 */
+#define NFHMM_ENUMERIC (-6)      /* non-finite alpha, phi or log Z */
+
+typedef struct nfhmm nfhmm_t;     /* opaque, library-owned */
+
+typedef struct {
+    int64_t n_mix;      /* independent mixtures (same model) on this handle; default 1           */
+    double gamma;       /* Dirichlet concentration gamma >= 0 ("we took gamma = 1"); default 1 */
+    int32_t device;     /* CUDA ordinal; default 0                                              */
+    int32_t max_iters;  /* capacity of the per-mixture free-energy trace; default 1024            */
+    int32_t free_energy;/* 1 = assemble L every sweep (default), 0 = skip the FP64 bound terms      */
+    int32_t reserved;
+    void *stream;       /* cudaStream_t to launch on (e.g. torch.cuda.current_stream().cuda_stream);
+                           NULL = the legacy default stream                                      */
+} nfhmm_options;
+
+/* Fill *opt with the defaults above. */
+void nfhmm_default_options(nfhmm_options *opt);
+
+/* Create a handle for n_mix mixtures of F x T counts with S sources of N states x K elements.
+ * opt may be NULL (defaults).  Validates dims (all >= 1, Kt and padded sizes fit in int32 rows).
+ * *out receives the handle; on error *out = NULL. */
+int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nfhmm_options *opt,
+                 nfhmm_t **out);
+
+/* Device bytes the handle needs (all state, 256-B aligned sub-buffers). */
+int nfhmm_workspace_size(const nfhmm_t *h, size_t *bytes);
+
+/* Hand the handle a caller-owned device buffer of >= nfhmm_workspace_size bytes (e.g. a torch
+ * uint8 tensor).  dptr = NULL, bytes = 0 asks the library to cudaMalloc (and free in destroy).
+ * The hot path never allocates.  Must precede set_model. */
+int nfhmm_set_workspace(nfhmm_t *h, void *dptr, size_t bytes);
+
+/* Source models: dict [S][N][K][F] = beta_l(k) at dict[k*F + l], each column >= 0
+ * summing to 1 (+-1e-4); trans [S][N][N] row-stochastic, trans[s][i][j] = P(D_t = j | D_{t-1} = i)
+ * (= rho^(s) transposed, DESIGN R4); prior [S][N] = pi^(s), sums to 1 (+-1e-4).
+ * Shared by all mixtures of the handle. */
+int nfhmm_set_model(nfhmm_t *h, const float *dict, const float *trans, const float *prior);
+
+/* Observed spectrogram counts V [n_mix][T][F] (V_lt at V[(m*T + t)*F + l]), >= 0 and
+ * finite.  Implies nfhmm_reset. */
+int nfhmm_set_observations(nfhmm_t *h, const float *V);
+
+/* Initial state (DESIGN R5): alpha = 1 + gamma/N, d = 1/N, then the z-step of that state.  Clears
+ * the free-energy trace and the iteration counter. */
+int nfhmm_reset(nfhmm_t *h);
+
+/* Run n_iters sweeps (each: Eq. 6 alpha-step from the current z, Eq. 8, forward-backward per source,
+ * then the Eq. 7 z-step of the new alpha, which also gives L of the sweep), then synchronise the
+ * stream and check the device error flags.  Sweeps accumulate across calls (resume). */
+int nfhmm_vb_iterate(nfhmm_t *h, int32_t n_iters);
+
+/* Same, without the final synchronisation / flag check (enqueue only).  Follow with nfhmm_sync. */
+int nfhmm_vb_iterate_async(nfhmm_t *h, int32_t n_iters);
+
+/* Synchronise the handle's stream and return the sticky device error status. */
+int nfhmm_sync(nfhmm_t *h);
+
+/* Copy out the current posteriors (any output may be NULL):
+ *   d_hat       [n_mix][S][T][N]  q(D_t^(s) = n)
+ *   alpha_hat   [n_mix][T][Kt]    Dirichlet parameters of q(theta_t) (Eq. 6)
+ *   V_hat       [n_mix][T][F]     sum_k beta_l(k) exp(E log theta_tk) for the current alpha (Eq. 7
+ *                                 normaliser, DESIGN R7)
+ *   free_energy [n_mix][max_iters] FP64 bound L_i, i = 1..iters_done (row stride max_iters)
+ *   iters_done  number of sweeps since the last reset
+ * Synchronises. */
+int nfhmm_posteriors(nfhmm_t *h, float *d_hat, float *alpha_hat, float *V_hat, double *free_energy,
+                     int32_t *iters_done);
+
+/* Section 4 separation from the current alpha: V_star [n_mix][S][T][F] (required),
+ * V_src [n_mix][S][T][F] (nullable, the unmasked V_hat^(s)).  Synchronises. */
+int nfhmm_separate(nfhmm_t *h, float *V_star, float *V_src);
+
+/* Free the handle (and the workspace if the library allocated it). NULL is a no-op. */
+int nfhmm_destroy(nfhmm_t *h);
+
+/* Static text for a status code. */
+const char *nfhmm_strerror(int status);
+
+/* Detail of the last failure on h (empty string if none). */
+const char *nfhmm_last_error(const nfhmm_t *h);
+
+/* Number of kernels this handle has launched since creation (evidence for bench gpu_launches). */
+int nfhmm_kernel_launches(const nfhmm_t *h, int64_t *count);
+
+/* Tile configuration chosen for the handle: padded F (BN of the reconstruction GEMM multiple) and
+ * padded Kt (BN of the back-projection GEMM multiple).  Informational. */
+int nfhmm_layout(const nfhmm_t *h, int64_t *F_pad, int64_t *Kt_pad, int32_t *bn_recon,
+                 int32_t *bn_backproj);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NFHMM_H */

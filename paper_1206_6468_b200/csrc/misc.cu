@@ -1,0 +1,161 @@
+// misc.cu -- small kernels around the VB sweep: (g) the FP64 bound reduction, Section 4's ratio mask
+// (part of (f)), initial state, observation statistics, the dictionary transpose.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "nfhmm_internal.cuh"
+
+namespace nfk {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// (g) L_i[m] = sum_t (sum_tiles data_part[t] + hdir[t]) + sum_s log Z[m][s] + T c_prior   (DESIGN R8)
+// One CTA per mixture, fixed-order FP64 reduction: bitwise independent of how mixtures are sharded.
+__global__ void __launch_bounds__(256) elbo_kernel(ElboArgs p) {
+    __shared__ double scratch[8];
+    const int m = blockIdx.x;
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
+        const size_t f = (size_t)m * p.T + t;
+        double v = p.hdir[f];
+        for (int c = 0; c < p.n_tiles; ++c) v += p.data_part[f * p.n_tiles + c];
+        acc += v;
+    }
+    acc = warp_sum_d(acc);
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += scratch[w];
+        for (int k = 0; k < p.S; ++k) s += p.logZ[(size_t)m * p.S + k];
+        s += p.c_prior_T;
+        p.fe[(size_t)m * p.max_iters + p.iter] = s;
+    }
+}
+
+__global__ void init_state_kernel(int frames, int ld, int Kt, float a0, float th0, float *alpha, float *theta) {
+    const size_t n = (size_t)frames * ld;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % ld);
+        alpha[i] = k < Kt ? a0 : 0.f;
+        theta[i] = k < Kt ? th0 : 0.f;
+    }
+}
+
+__global__ void fill_kernel(float *p, long long n, float v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void transpose_kernel(const float *__restrict__ src, int rows, int cols, int lds, float *__restrict__ dst,
+                                 int ldd) {
+    __shared__ float tile[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < rows && c < cols) ? src[(size_t)r * lds + c] : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, r = r0 + threadIdx.x;
+        if (c < cols && r < rows) dst[(size_t)c * ldd + r] = tile[threadIdx.x][i];
+    }
+}
+
+// v_t = sum_l V_lt (FP64 accumulation) and input checks (V >= 0, finite) -- one warp per frame.
+__global__ void obs_stats_kernel(const float *__restrict__ V, int frames, int F, int ld, float *vt, unsigned *flags) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= frames) return;
+    double s = 0.0;
+    unsigned bad = 0;
+    for (int l = lane; l < F; l += 32) {
+        const float v = V[(size_t)w * ld + l];
+        if (!(v >= 0.f) || !isfinite(v)) bad = FLAG_BAD_INPUT;
+        s += (double)v;
+    }
+    s = warp_sum_d(s);
+    if (lane == 0) vt[w] = (float)s;
+    if (bad) atomicOr(flags, bad);
+}
+
+// scale_t = v_t / alpha_0 (posterior mean E[theta] = alpha / alpha_0, DESIGN R9; v_t from S:408).
+__global__ void sep_scale_kernel(const float *__restrict__ alpha, int frames, int Kt, int ld, const float *vt, float *scale) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= frames) return;
+    double s = 0.0;
+    for (int k = lane; k < Kt; k += 32) s += (double)alpha[(size_t)w * ld + k];
+    s = warp_sum_d(s);
+    if (lane == 0) scale[w] = (float)((double)vt[w] / s);
+}
+
+// P:203  V*^(s) = V V_src^(s) / sum_s' V_src^(s');  1/S where the denominator is 0.
+__global__ void wiener_kernel(const float *__restrict__ V, int ldv, const float *vsrc, float *vstar, int M, int S,
+                              int T, int F) {
+    const size_t n = (size_t)M * T * F;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int l = (int)(i % F);
+        const size_t mt = i / F;
+        const int t = (int)(mt % T), m = (int)(mt / T);
+        const float v = V[mt * ldv + l];
+        float den = 0.f;
+        for (int s = 0; s < S; ++s) den += vsrc[((size_t)(m * S + s) * T + t) * F + l];
+        for (int s = 0; s < S; ++s) {
+            const size_t o = ((size_t)(m * S + s) * T + t) * F + l;
+            vstar[o] = den > 0.f ? v * (vsrc[o] / den) : v / (float)S;
+        }
+    }
+}
+
+int grid_for(size_t n, int block) {
+    size_t g = (n + block - 1) / block;
+    if (g > 148 * 32) g = 148 * 32;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+}  // namespace
+
+cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st) {
+    elbo_kernel<<<a.M, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_state(int frames, int ld, int Kt, float alpha0, float theta0, float *alpha, float *theta,
+                              float *d_hat, long long d_count, float d0, cudaStream_t st) {
+    init_state_kernel<<<grid_for((size_t)frames * ld, 256), 256, 0, st>>>(frames, ld, Kt, alpha0, theta0, alpha, theta);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fill_kernel<<<grid_for((size_t)d_count, 256), 256, 0, st>>>(d_hat, d_count, d0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const float *src, int rows, int cols, int ld_src, float *dst, int ld_dst, cudaStream_t st) {
+    dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+    transpose_kernel<<<grid, block, 0, st>>>(src, rows, cols, ld_src, dst, ld_dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_obs_stats(const float *V, int frames, int F, int ld, float *vt, unsigned *flags, cudaStream_t st) {
+    obs_stats_kernel<<<(frames * 32 + 255) / 256, 256, 0, st>>>(V, frames, F, ld, vt, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sep_scale(const float *alpha, int frames, int Kt, int ld, const float *vt, float *scale,
+                             cudaStream_t st) {
+    sep_scale_kernel<<<(frames * 32 + 255) / 256, 256, 0, st>>>(alpha, frames, Kt, ld, vt, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wiener(const float *V, int ldv, const float *vsrc, float *vstar, int M, int S, int T, int F,
+                          cudaStream_t st) {
+    wiener_kernel<<<grid_for((size_t)M * T * F, 256), 256, 0, st>>>(V, ldv, vsrc, vstar, M, S, T, F);
+    return cudaGetLastError();
+}
+
+}  // namespace nfk

@@ -1,0 +1,556 @@
+// nfhmm_abi.cu -- host runtime behind the C-ABI of include/nfhmm.h: handle, workspace carving, argument
+// validation, the per-sweep launch sequence and the copies in/out.  Every step of the path runs in the
+// kernels of gemm_simt.cu, dirichlet.cu, fb.cu and misc.cu; there is no CPU fallback.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "nfhmm_internal.cuh"
+
+using namespace nfk;
+
+struct nfhmm {
+    int64_t F = 0, T = 0, M = 0, frames = 0;
+    int S = 0, N = 0, K = 0, Kt = 0;
+    int Fa = 0, Kb = 0, bn_a = 0, bn_b = 0, nt_a = 0;
+    double gamma = 1.0;
+    int device = 0, max_iters = 1024, free_energy = 1;
+    cudaStream_t st = nullptr;
+
+    void *ws = nullptr;
+    size_t ws_bytes = 0;
+    bool ws_owned = false;
+
+    float *betaT = nullptr, *beta = nullptr, *trans = nullptr, *prior = nullptr;
+    float *V = nullptr, *R = nullptr, *theta = nullptr, *alpha = nullptr;
+    float *dhat = nullptr, *ec = nullptr, *fwd = nullptr, *cinv = nullptr;
+    float *vt = nullptr, *scale = nullptr, *vsrc = nullptr;
+    double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
+    unsigned *flags = nullptr;
+
+    bool have_model = false, have_obs = false, R_valid = false;
+    int iters_done = 0;
+    int64_t launches = 0;
+    double c_prior_T = 0.0;
+    std::string err;
+};
+
+namespace {
+
+const int kReconBN[] = {40, 64, 88, 104, 128};
+const int kBackBN[] = {24, 64, 80, 120, 128, 160};
+
+int pick_bn(int64_t n, const int *c, int nc) {
+    int best = -1;
+    int64_t best_pad = INT64_MAX;
+    for (int i = 0; i < nc; ++i) {
+        const int64_t pad = (n + c[i] - 1) / c[i] * c[i];
+        if (pad < best_pad || (pad == best_pad && c[i] > best)) {
+            best_pad = pad;
+            best = c[i];
+        }
+    }
+    return best;
+}
+
+int fail(nfhmm_t *h, int code, const char *fmt, ...) {
+    if (h) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        h->err = buf;
+    }
+    return code;
+}
+
+#define CU(h, call)                                                                            \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) return fail(h, NFHMM_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define LAUNCH(h, call)         \
+    do {                        \
+        CU(h, call);            \
+        (h)->launches++;        \
+    } while (0)
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+size_t al(size_t b) { return (b + 255) & ~size_t(255); }
+
+// Carve (or just size) the workspace.  Order is fixed; sizes in bytes.
+size_t carve(nfhmm_t *h, char *base) {
+    const size_t fr = (size_t)h->frames, Fa = h->Fa, Kb = h->Kb;
+    const size_t chainTN = (size_t)h->M * h->S * h->T * h->N, chainT = (size_t)h->M * h->S * h->T;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        char *p = base ? base + o : nullptr;
+        o += al(bytes);
+        return p;
+    };
+    char *p;
+    p = take(Kb * Fa * 4);                       h->betaT = (float *)p;
+    p = take(Fa * Kb * 4);                       h->beta = (float *)p;
+    p = take((size_t)h->S * h->N * h->N * 4);    h->trans = (float *)p;
+    p = take((size_t)h->S * h->N * 4);           h->prior = (float *)p;
+    p = take(fr * Fa * 4);                       h->V = (float *)p;
+    p = take(fr * Fa * 4);                       h->R = (float *)p;
+    p = take(fr * Kb * 4);                       h->theta = (float *)p;
+    p = take(fr * Kb * 4);                       h->alpha = (float *)p;
+    p = take(chainTN * 4);                       h->dhat = (float *)p;
+    p = take(chainTN * 4);                       h->ec = (float *)p;
+    p = take(chainTN * 4);                       h->fwd = (float *)p;
+    p = take(chainT * 4);                        h->cinv = (float *)p;
+    p = take(chainT * 8);                        h->eoff = (double *)p;
+    p = take((size_t)h->M * h->S * 8);           h->logZ = (double *)p;
+    p = take(fr * h->nt_a * 8);                  h->data_part = (double *)p;
+    p = take(fr * 8);                            h->hdir = (double *)p;
+    p = take((size_t)h->M * h->max_iters * 8);   h->fe = (double *)p;
+    p = take(fr * 4);                            h->vt = (float *)p;
+    p = take(fr * 4);                            h->scale = (float *)p;
+    p = take((size_t)h->M * h->S * h->T * h->F * 4); h->vsrc = (float *)p;
+    p = take(256);                               h->flags = (unsigned *)p;
+    return o;
+}
+
+// Bytes the workspace needs (sized on a copy so the live handle's pointers are untouched).
+size_t ws_need(const nfhmm_t *h) {
+    nfhmm tmp = *h;
+    return carve(&tmp, nullptr);
+}
+
+int check_flags(nfhmm_t *h) {
+    unsigned f = 0;
+    CU(h, cudaMemcpyAsync(&f, h->flags, sizeof f, cudaMemcpyDeviceToHost, h->st));
+    CU(h, cudaStreamSynchronize(h->st));
+    if (f & FLAG_BAD_INPUT) return fail(h, NFHMM_EINVAL, "observations contain negative or non-finite values");
+    if (f & FLAG_ZERO_SUPPORT) return fail(h, NFHMM_EZEROSUPPORT, "V > 0 where V_hat = 0 (zero support, S:278)");
+    if (f & FLAG_NONFINITE) return fail(h, NFHMM_ENUMERIC, "non-finite alpha, phi or log Z");
+    return NFHMM_OK;
+}
+
+int recon_ratio(nfhmm_t *h) {
+    ReconArgs a{};
+    a.M = (int)h->frames;
+    a.k_begin = 0;
+    a.k_end = h->Kt;
+    a.A = h->theta;
+    a.lda = h->Kb;
+    a.B = h->betaT;
+    a.ldb = h->Fa;
+    a.F = (int)h->F;
+    a.V = h->V;
+    a.ldv = h->Fa;
+    a.R = h->R;
+    a.data_part = h->data_part;
+    a.n_tiles = h->nt_a;
+    a.flags = h->flags;
+    LAUNCH(h, launch_recon(h->bn_a, a, h->st));
+    return NFHMM_OK;
+}
+
+int sweep(nfhmm_t *h) {
+    if (!h->R_valid) {
+        int r = recon_ratio(h);
+        if (r) return r;
+        h->R_valid = true;
+    }
+    // (b) n = theta .* (R beta): the Eq. 6 data term  sum_l V_lt z_{t,l,k}
+    BackprojArgs b{};
+    b.M = (int)h->frames;
+    b.Kpad = h->Fa;
+    b.A = h->R;
+    b.lda = h->Fa;
+    b.B = h->beta;
+    b.ldb = h->Kb;
+    b.theta = h->theta;
+    b.n_out = h->alpha;
+    LAUNCH(h, launch_backproj(h->bn_b, b, h->st));
+    // (c)+(d) Eq. 6, digamma/exp, Eq. 8
+    DirichletArgs d{};
+    d.frames = (int)h->frames;
+    d.T = (int)h->T;
+    d.S = h->S;
+    d.N = h->N;
+    d.K = h->K;
+    d.Kt = h->Kt;
+    d.ld = h->Kb;
+    d.gamma = (float)h->gamma;
+    d.n_in = h->alpha;
+    d.alpha = h->alpha;
+    d.theta = h->theta;
+    d.d_hat = h->dhat;
+    d.ec = h->ec;
+    d.eoff = h->eoff;
+    d.hdir = h->free_energy ? h->hdir : nullptr;
+    d.flags = h->flags;
+    LAUNCH(h, launch_dirichlet(d, h->st));
+    // (e) forward-backward per source
+    FBArgs f{};
+    f.M = (int)h->M;
+    f.S = h->S;
+    f.T = (int)h->T;
+    f.N = h->N;
+    f.ec = h->ec;
+    f.eoff = h->eoff;
+    f.trans = h->trans;
+    f.prior = h->prior;
+    f.d_hat = h->dhat;
+    f.fwd = h->fwd;
+    f.cinv = h->cinv;
+    f.logZ = h->logZ;
+    f.flags = h->flags;
+    LAUNCH(h, launch_fb(f, h->st));
+    // (a) z-step of the new alpha: R for the next sweep and the data term of L_i
+    int r = recon_ratio(h);
+    if (r) return r;
+    // (g) L_i
+    if (h->free_energy && h->iters_done < h->max_iters) {
+        ElboArgs e{};
+        e.M = (int)h->M;
+        e.T = (int)h->T;
+        e.n_tiles = h->nt_a;
+        e.S = h->S;
+        e.iter = h->iters_done;
+        e.max_iters = h->max_iters;
+        e.c_prior_T = h->c_prior_T;
+        e.data_part = h->data_part;
+        e.hdir = h->hdir;
+        e.logZ = h->logZ;
+        e.fe = h->fe;
+        LAUNCH(h, launch_elbo(e, h->st));
+    }
+    h->iters_done++;
+    return NFHMM_OK;
+}
+
+int enter(nfhmm_t *h) {
+    if (!h) return NFHMM_EINVAL;
+    h->err.clear();
+    CU(h, cudaSetDevice(h->device));
+    return NFHMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void nfhmm_default_options(nfhmm_options *o) {
+    if (!o) return;
+    memset(o, 0, sizeof *o);
+    o->n_mix = 1;
+    o->gamma = 1.0;
+    o->device = 0;
+    o->max_iters = 1024;
+    o->free_energy = 1;
+    o->stream = nullptr;
+}
+
+int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nfhmm_options *opt, nfhmm_t **out) {
+    if (!out) return NFHMM_EINVAL;
+    *out = nullptr;
+    nfhmm_options o;
+    nfhmm_default_options(&o);
+    if (opt) o = *opt;
+    if (F < 1 || T < 1 || S < 1 || N < 1 || K < 1 || o.n_mix < 1 || !(o.gamma >= 0.0) || !isfinite(o.gamma) ||
+        o.max_iters < 1)
+        return NFHMM_EINVAL;
+    if (N > 128) return NFHMM_EINVAL;  // forward-backward keeps <= 4 states per lane
+    const int64_t Kt = (int64_t)S * N * K;
+    const int64_t frames = o.n_mix * T;
+    if (Kt > (1 << 24) || F > (1 << 24) || frames > (int64_t)1 << 30) return NFHMM_EINVAL;
+    nfhmm_t *h = new (std::nothrow) nfhmm;
+    if (!h) return NFHMM_ENOMEM;
+    h->F = F;
+    h->T = T;
+    h->S = S;
+    h->N = N;
+    h->K = K;
+    h->Kt = (int)Kt;
+    h->M = o.n_mix;
+    h->frames = frames;
+    h->gamma = o.gamma;
+    h->device = o.device;
+    h->max_iters = o.max_iters;
+    h->free_energy = o.free_energy ? 1 : 0;
+    h->st = (cudaStream_t)o.stream;
+    h->bn_a = pick_bn(F, kReconBN, sizeof kReconBN / sizeof *kReconBN);
+    h->bn_b = pick_bn(Kt, kBackBN, sizeof kBackBN / sizeof *kBackBN);
+    h->Fa = (int)((F + h->bn_a - 1) / h->bn_a * h->bn_a);
+    h->Kb = (int)((Kt + h->bn_b - 1) / h->bn_b * h->bn_b);
+    h->nt_a = h->Fa / h->bn_a;
+    // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)
+    h->c_prior_T = (double)T * (lgamma((double)Kt + o.gamma * S * K) - (double)S * K * lgamma(1.0 + o.gamma));
+    // no CUDA call here: dims/layout/workspace queries work without a device; the first call that
+    // touches the device (set_workspace) selects it.
+    *out = h;
+    return NFHMM_OK;
+}
+
+int nfhmm_workspace_size(const nfhmm_t *h, size_t *bytes) {
+    if (!h || !bytes) return NFHMM_EINVAL;
+    *bytes = ws_need(h);
+    return NFHMM_OK;
+}
+
+int nfhmm_set_workspace(nfhmm_t *h, void *dptr, size_t bytes) {
+    int r = enter(h);
+    if (r) return r;
+    const size_t need = ws_need(h);
+    if (h->ws_owned && h->ws) {
+        cudaFree(h->ws);
+        h->ws = nullptr;
+        h->ws_owned = false;
+    }
+    if (!dptr) {
+        CU(h, cudaMalloc(&h->ws, need));
+        h->ws_owned = true;
+        h->ws_bytes = need;
+    } else {
+        if (bytes < need) return fail(h, NFHMM_ENOMEM, "workspace %zu < required %zu bytes", bytes, need);
+        if (((uintptr_t)dptr & 255) != 0) return fail(h, NFHMM_EINVAL, "workspace must be 256-byte aligned");
+        if (!is_device_ptr(dptr)) return fail(h, NFHMM_EINVAL, "workspace must be device memory");
+        h->ws = dptr;
+        h->ws_bytes = bytes;
+    }
+    carve(h, (char *)h->ws);
+    // zero everything once: all padding (bins >= F, elements >= Kt) stays zero for the handle's life
+    CU(h, cudaMemsetAsync(h->ws, 0, need, h->st));
+    h->have_model = h->have_obs = h->R_valid = false;
+    h->iters_done = 0;
+    return NFHMM_OK;
+}
+
+int nfhmm_set_model(nfhmm_t *h, const float *dict, const float *trans, const float *prior) {
+    int r = enter(h);
+    if (r) return r;
+    if (!h->ws) return fail(h, NFHMM_ESTATE, "set_workspace must precede set_model");
+    if (!dict || !trans || !prior) return fail(h, NFHMM_EINVAL, "NULL model array");
+    const size_t nd = (size_t)h->Kt * h->F, nt = (size_t)h->S * h->N * h->N, np = (size_t)h->S * h->N;
+    std::vector<float> hd(nd), ht(nt), hp(np);
+    CU(h, cudaMemcpy(hd.data(), dict, nd * 4, cudaMemcpyDefault));
+    CU(h, cudaMemcpy(ht.data(), trans, nt * 4, cudaMemcpyDefault));
+    CU(h, cudaMemcpy(hp.data(), prior, np * 4, cudaMemcpyDefault));
+    for (int k = 0; k < h->Kt; ++k) {
+        double s = 0.0;
+        for (int64_t l = 0; l < h->F; ++l) {
+            const float v = hd[(size_t)k * h->F + l];
+            if (!(v >= 0.f) || !isfinite(v)) return fail(h, NFHMM_EINVAL, "dictionary element %d has a negative/non-finite entry", k);
+            s += v;
+        }
+        if (fabs(s - 1.0) > 1e-4) return fail(h, NFHMM_EINVAL, "dictionary element %d sums to %.8g, not 1", k, s);
+    }
+    for (int s = 0; s < h->S; ++s) {
+        for (int i = 0; i < h->N; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < h->N; ++j) {
+                const float v = ht[((size_t)s * h->N + i) * h->N + j];
+                if (!(v >= 0.f) || !isfinite(v)) return fail(h, NFHMM_EINVAL, "transition (%d,%d,%d) invalid", s, i, j);
+                acc += v;
+            }
+            if (fabs(acc - 1.0) > 1e-4) return fail(h, NFHMM_EINVAL, "transition row (%d,%d) sums to %.8g", s, i, acc);
+        }
+        double acc = 0.0;
+        for (int i = 0; i < h->N; ++i) {
+            const float v = hp[(size_t)s * h->N + i];
+            if (!(v >= 0.f) || !isfinite(v)) return fail(h, NFHMM_EINVAL, "prior (%d,%d) invalid", s, i);
+            acc += v;
+        }
+        if (fabs(acc - 1.0) > 1e-4) return fail(h, NFHMM_EINVAL, "prior of source %d sums to %.8g", s, acc);
+    }
+    // betaT [Kb][Fa] (rows k, padded with zeros), beta [Fa][Kb] its transpose
+    CU(h, cudaMemsetAsync(h->betaT, 0, (size_t)h->Kb * h->Fa * 4, h->st));
+    CU(h, cudaMemsetAsync(h->beta, 0, (size_t)h->Fa * h->Kb * 4, h->st));
+    CU(h, cudaMemcpy2DAsync(h->betaT, (size_t)h->Fa * 4, hd.data(), (size_t)h->F * 4, (size_t)h->F * 4, h->Kt,
+                            cudaMemcpyHostToDevice, h->st));
+    LAUNCH(h, launch_transpose(h->betaT, h->Kt, (int)h->F, h->Fa, h->beta, h->Kb, h->st));
+    CU(h, cudaMemcpyAsync(h->trans, ht.data(), nt * 4, cudaMemcpyHostToDevice, h->st));
+    CU(h, cudaMemcpyAsync(h->prior, hp.data(), np * 4, cudaMemcpyHostToDevice, h->st));
+    CU(h, cudaStreamSynchronize(h->st));   // host vectors go out of scope
+    h->have_model = true;
+    h->R_valid = false;
+    return NFHMM_OK;
+}
+
+int nfhmm_reset(nfhmm_t *h) {
+    int r = enter(h);
+    if (r) return r;
+    if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "set_model and set_observations must precede reset");
+    // DESIGN R5: alpha = 1 + gamma/N, d = 1/N; theta = exp(psi(alpha) - psi(Kt alpha)) (uniform)
+    const double a0 = 1.0 + h->gamma / h->N;
+    auto dg = [](double x) {
+        double res = 0.0;
+        while (x < 10.0) { res -= 1.0 / x; x += 1.0; }
+        const double f = 1.0 / (x * x);
+        return res + log(x) - 0.5 / x - f * (1.0 / 12 - f * (1.0 / 120 - f / 252));
+    };
+    const float th0 = (float)exp(dg(a0) - dg(a0 * h->Kt));
+    LAUNCH(h, launch_init_state((int)h->frames, h->Kb, h->Kt, (float)a0, th0, h->alpha, h->theta, h->dhat,
+                                (long long)h->M * h->S * h->T * h->N, (float)(1.0 / h->N), h->st));
+    CU(h, cudaMemsetAsync(h->fe, 0, (size_t)h->M * h->max_iters * 8, h->st));
+    h->R_valid = false;
+    r = recon_ratio(h);
+    if (r) return r;
+    h->R_valid = true;
+    h->iters_done = 0;
+    return NFHMM_OK;
+}
+
+int nfhmm_set_observations(nfhmm_t *h, const float *V) {
+    int r = enter(h);
+    if (r) return r;
+    if (!h->have_model) return fail(h, NFHMM_ESTATE, "set_model must precede set_observations");
+    if (!V) return fail(h, NFHMM_EINVAL, "NULL observations");
+    CU(h, cudaMemsetAsync(h->flags, 0, sizeof(unsigned), h->st));   // new data: clear sticky flags
+    CU(h, cudaMemcpy2DAsync(h->V, (size_t)h->Fa * 4, V, (size_t)h->F * 4, (size_t)h->F * 4, (size_t)h->frames,
+                            cudaMemcpyDefault, h->st));
+    LAUNCH(h, launch_obs_stats(h->V, (int)h->frames, (int)h->F, h->Fa, h->vt, h->flags, h->st));
+    h->have_obs = true;
+    return nfhmm_reset(h);
+}
+
+int nfhmm_vb_iterate_async(nfhmm_t *h, int32_t n_iters) {
+    int r = enter(h);
+    if (r) return r;
+    if (n_iters < 0) return fail(h, NFHMM_EINVAL, "n_iters < 0");
+    if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
+    for (int i = 0; i < n_iters; ++i) {
+        r = sweep(h);
+        if (r) return r;
+    }
+    return NFHMM_OK;
+}
+
+int nfhmm_sync(nfhmm_t *h) {
+    int r = enter(h);
+    if (r) return r;
+    return check_flags(h);
+}
+
+int nfhmm_vb_iterate(nfhmm_t *h, int32_t n_iters) {
+    int r = nfhmm_vb_iterate_async(h, n_iters);
+    if (r) return r;
+    return check_flags(h);
+}
+
+int nfhmm_posteriors(nfhmm_t *h, float *d_hat, float *alpha_hat, float *V_hat, double *free_energy,
+                     int32_t *iters_done) {
+    int r = enter(h);
+    if (r) return r;
+    if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
+    const size_t chainTN = (size_t)h->M * h->S * h->T * h->N;
+    if (d_hat) CU(h, cudaMemcpyAsync(d_hat, h->dhat, chainTN * 4, cudaMemcpyDefault, h->st));
+    if (alpha_hat)
+        CU(h, cudaMemcpy2DAsync(alpha_hat, (size_t)h->Kt * 4, h->alpha, (size_t)h->Kb * 4, (size_t)h->Kt * 4,
+                                (size_t)h->frames, cudaMemcpyDefault, h->st));
+    if (V_hat) {
+        const bool dev = is_device_ptr(V_hat);
+        ReconArgs a{};
+        a.M = (int)h->frames;
+        a.k_begin = 0;
+        a.k_end = h->Kt;
+        a.A = h->theta;
+        a.lda = h->Kb;
+        a.B = h->betaT;
+        a.ldb = h->Fa;
+        a.F = (int)h->F;
+        a.Vhat = dev ? V_hat : h->vsrc;
+        a.n_tiles = h->nt_a;
+        a.flags = h->flags;
+        LAUNCH(h, launch_recon(h->bn_a, a, h->st));
+        if (!dev) CU(h, cudaMemcpyAsync(V_hat, h->vsrc, (size_t)h->frames * h->F * 4, cudaMemcpyDeviceToHost, h->st));
+    }
+    if (free_energy)
+        CU(h, cudaMemcpyAsync(free_energy, h->fe, (size_t)h->M * h->max_iters * 8, cudaMemcpyDefault, h->st));
+    if (iters_done) *iters_done = h->iters_done;
+    return check_flags(h);
+}
+
+int nfhmm_separate(nfhmm_t *h, float *V_star, float *V_src) {
+    int r = enter(h);
+    if (r) return r;
+    if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
+    if (!V_star) return fail(h, NFHMM_EINVAL, "V_star is required");
+    LAUNCH(h, launch_sep_scale(h->alpha, (int)h->frames, h->Kt, h->Kb, h->vt, h->scale, h->st));
+    const int NK = h->N * h->K;
+    for (int s = 0; s < h->S; ++s) {
+        ReconArgs a{};
+        a.M = (int)h->frames;
+        a.k_begin = s * NK;
+        a.k_end = (s + 1) * NK;
+        a.A = h->alpha;
+        a.lda = h->Kb;
+        a.B = h->betaT;
+        a.ldb = h->Fa;
+        a.F = (int)h->F;
+        a.n_tiles = h->nt_a;
+        a.row_scale = h->scale;
+        a.out_src = h->vsrc;
+        a.T = (int)h->T;
+        a.S = h->S;
+        a.s = s;
+        a.flags = h->flags;
+        LAUNCH(h, launch_recon(h->bn_a, a, h->st));
+    }
+    const size_t n = (size_t)h->M * h->S * h->T * h->F;
+    if (V_src) CU(h, cudaMemcpyAsync(V_src, h->vsrc, n * 4, cudaMemcpyDefault, h->st));
+    const bool dev = is_device_ptr(V_star);
+    LAUNCH(h, launch_wiener(h->V, h->Fa, h->vsrc, dev ? V_star : h->vsrc, (int)h->M, h->S, (int)h->T, (int)h->F, h->st));
+    if (!dev) CU(h, cudaMemcpyAsync(V_star, h->vsrc, n * 4, cudaMemcpyDeviceToHost, h->st));
+    return check_flags(h);
+}
+
+int nfhmm_destroy(nfhmm_t *h) {
+    if (!h) return NFHMM_OK;
+    cudaSetDevice(h->device);
+    if (h->ws_owned && h->ws) cudaFree(h->ws);
+    delete h;
+    return NFHMM_OK;
+}
+
+const char *nfhmm_strerror(int s) {
+    switch (s) {
+        case NFHMM_OK: return "ok";
+        case NFHMM_EINVAL: return "invalid argument";
+        case NFHMM_ESTATE: return "call order violated";
+        case NFHMM_ECUDA: return "CUDA error";
+        case NFHMM_ENOMEM: return "out of memory / workspace too small";
+        case NFHMM_EZEROSUPPORT: return "zero support: V > 0 where V_hat = 0";
+        case NFHMM_ENUMERIC: return "non-finite value in alpha, phi or log Z";
+        default: return "unknown status";
+    }
+}
+
+const char *nfhmm_last_error(const nfhmm_t *h) { return h ? h->err.c_str() : ""; }
+
+int nfhmm_kernel_launches(const nfhmm_t *h, int64_t *count) {
+    if (!h || !count) return NFHMM_EINVAL;
+    *count = h->launches;
+    return NFHMM_OK;
+}
+
+int nfhmm_layout(const nfhmm_t *h, int64_t *F_pad, int64_t *Kt_pad, int32_t *bn_recon, int32_t *bn_backproj) {
+    if (!h) return NFHMM_EINVAL;
+    if (F_pad) *F_pad = h->Fa;
+    if (Kt_pad) *Kt_pad = h->Kb;
+    if (bn_recon) *bn_recon = h->bn_a;
+    if (bn_backproj) *bn_backproj = h->bn_b;
+    return NFHMM_OK;
+}
+
+}  // extern "C"

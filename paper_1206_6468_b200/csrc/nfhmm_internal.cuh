@@ -1,0 +1,112 @@
+// nfhmm_internal.cuh -- shared declarations of libnfhmm's device kernels and host runtime.
+// Product path: no code here is shared with oracle/ (task rule: the two share nothing).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/nfhmm.h"
+
+namespace nfk {
+
+// Device error flags (sticky, OR-ed by kernels, read once per sync).
+enum : unsigned { FLAG_ZERO_SUPPORT = 1u, FLAG_NONFINITE = 2u, FLAG_BAD_INPUT = 4u };
+
+// Reconstruction-GEMM modes (kernel (a) and the Section 4 reconstruction of kernel (f)).
+enum ReconMode : int {
+    RECON_RATIO = 0,     // R = V / V_hat, sum V log V_hat partials, optional V_hat store   (Eq. 7)
+    RECON_STORE = 1,     // store V_hat only (posteriors)
+    RECON_SEPARATE = 2,  // V_src^(s) = (v_t / alpha_0) * sum_{k in s} beta alpha
+};
+
+struct ReconArgs {
+    int M;                    // rows (frames) of the GEMM
+    int k_begin, k_end;       // contraction range over global elements k
+    const float *A;           // [M][lda] theta (RATIO/STORE) or alpha (SEPARATE)
+    int lda;
+    const float *B;           // betaT [Kpad][ldb]
+    int ldb;
+    int F;                    // true number of bins
+    const float *V;           // [M][ldv] counts (padded with zeros to ldv)
+    int ldv;
+    float *R;                 // [M][ldv] ratio out (RATIO)
+    float *Vhat;              // optional [..][F] V_hat out (RATIO/STORE), row-major ld = F
+    double *data_part;        // [M][n_tiles] FP64 sum_l V log V_hat per (row, column tile) (RATIO)
+    int n_tiles;
+    const float *row_scale;   // SEPARATE: per-row v_t / alpha_0
+    float *out_src;           // SEPARATE: V_src base for this source
+    int T, S, s;              // SEPARATE: address ((m*S + s)*T + t)*F + l
+    unsigned *flags;
+};
+
+struct BackprojArgs {
+    int M;
+    int Kpad;                 // contraction length (padded bins, multiple of 8)
+    const float *A;           // R [M][lda]
+    int lda;
+    const float *B;           // beta [Kpad][ldb]
+    int ldb;
+    const float *theta;       // [M][ldb]
+    float *n_out;             // [M][ldb]  n = theta .* (R beta)   (data term of Eq. 6)
+};
+
+// Launchers (return cudaError_t of the launch).
+cudaError_t launch_recon(int bn, const ReconArgs &a, cudaStream_t st);
+cudaError_t launch_backproj(int bn, const BackprojArgs &a, cudaStream_t st);
+
+struct DirichletArgs {
+    int frames, T, S, N, K, Kt, ld;   // ld = padded row length of n/alpha/theta
+    float gamma;
+    const float *n_in;        // [frames][ld]  data term of Eq. 6 (sum_l V z)
+    float *alpha;             // [frames][ld]  out: alpha (may alias n_in)
+    float *theta;             // [frames][ld]  out: exp(psi(alpha) - psi(alpha_0))
+    const float *d_hat;       // [M][S][T][N]  previous q(D) marginals
+    float *ec;                // [M][S][T][N]  out: centred log-emission gamma*(phi - max_n phi)
+    double *eoff;             // [M][S][T]     out: gamma * max_n phi (FP64)
+    double *hdir;             // [frames]      out: Dirichlet entropy terms of the bound (or NULL)
+    unsigned *flags;
+};
+cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st);
+
+struct FBArgs {
+    int M, S, T, N;
+    const float *ec;          // [M][S][T][N]
+    const double *eoff;       // [M][S][T]
+    const float *trans;       // [S][N][N]
+    const float *prior;       // [S][N]
+    float *d_hat;             // [M][S][T][N] out
+    float *fwd;               // [M][S][T][N] scratch: normalised forward messages
+    float *cinv;              // [M][S][T]    scratch: 1 / c_t
+    double *logZ;             // [M][S] out
+    unsigned *flags;
+};
+cudaError_t launch_fb(const FBArgs &a, cudaStream_t st);
+
+struct ElboArgs {
+    int M, T, n_tiles, S, iter, max_iters;
+    double c_prior_T;         // T * (lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma))
+    const double *data_part;  // [M*T][n_tiles]
+    const double *hdir;       // [M*T]
+    const double *logZ;       // [M][S]
+    double *fe;               // [M][max_iters]
+};
+cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st);
+
+// Initial state (DESIGN R5): alpha = 1 + gamma/N, theta = exp(psi(a) - psi(Kt a)), d = 1/N.
+cudaError_t launch_init_state(int frames, int ld, int Kt, float alpha0, float theta0, float *alpha,
+                              float *theta, float *d_hat, long long d_count, float d0,
+                              cudaStream_t st);
+// betaT [rows][ldT] -> beta [ldT][ldb] transpose (rows = Kt, cols = F)
+cudaError_t launch_transpose(const float *src, int rows, int cols, int ld_src, float *dst, int ld_dst,
+                             cudaStream_t st);
+// Observation checks + per-frame row sums v_t (FP32 exact for integer counts; FP64 accumulate).
+cudaError_t launch_obs_stats(const float *V, int frames, int F, int ld, float *vt, unsigned *flags,
+                             cudaStream_t st);
+// Per-row scale v_t / alpha_0 for separation.
+cudaError_t launch_sep_scale(const float *alpha, int frames, int Kt, int ld, const float *vt, float *scale,
+                             cudaStream_t st);
+// V*^(s) = V V_src^(s) / sum_s' V_src^(s'), V_src layout [M][S][T][F]; writes V_star.
+cudaError_t launch_wiener(const float *V, int ldv, const float *vsrc, float *vstar, int M, int S, int T,
+                          int F, cudaStream_t st);
+
+}  // namespace nfk

@@ -1,0 +1,264 @@
+"""Thin Python binding of libnfhmm's C-ABI (include/nfhmm.h): argument marshalling only.
+
+Every step of the VB path runs in the library's sm_100a kernels.  There is no CPU fallback: if
+libnfhmm.so is missing this module raises at import, and every call that fails on the device raises
+NFHMMError with the library's status and message.
+
+PyTorch is used for plumbing only: device memory (the workspace and any output tensors), the CUDA
+stream handed to the library, and torch.distributed for multi-GPU sharding (bench.py).
+
+The module-level functions carry the C names (nfhmm_create, nfhmm_set_model, ...); the NFHMM class
+wraps a handle for convenience.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libnfhmm.so")
+
+NFHMM_OK, NFHMM_EINVAL, NFHMM_ESTATE, NFHMM_ECUDA = 0, -1, -2, -3
+NFHMM_ENOMEM, NFHMM_EZEROSUPPORT, NFHMM_ENUMERIC = -4, -5, -6
+
+
+class NFHMMError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"libnfhmm status {status}: {msg}")
+        self.status = status
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("n_mix", ctypes.c_int64), ("gamma", ctypes.c_double), ("device", ctypes.c_int32),
+                ("max_iters", ctypes.c_int32), ("free_energy", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("stream", ctypes.c_void_p)]
+
+
+# symbol -> (restype, argtypes); mirrors include/nfhmm.h exactly (tests check the two agree)
+_P, _I32, _I64, _D, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
+SIGNATURES = {
+    "nfhmm_default_options": (None, [ctypes.POINTER(Options)]),
+    "nfhmm_create": (ctypes.c_int, [_I64, _I64, _I32, _I32, _I32, ctypes.POINTER(Options), ctypes.POINTER(_P)]),
+    "nfhmm_workspace_size": (ctypes.c_int, [_P, ctypes.POINTER(_SZ)]),
+    "nfhmm_set_workspace": (ctypes.c_int, [_P, _P, _SZ]),
+    "nfhmm_set_model": (ctypes.c_int, [_P, _P, _P, _P]),
+    "nfhmm_set_observations": (ctypes.c_int, [_P, _P]),
+    "nfhmm_reset": (ctypes.c_int, [_P]),
+    "nfhmm_vb_iterate": (ctypes.c_int, [_P, _I32]),
+    "nfhmm_vb_iterate_async": (ctypes.c_int, [_P, _I32]),
+    "nfhmm_sync": (ctypes.c_int, [_P]),
+    "nfhmm_posteriors": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.POINTER(_I32)]),
+    "nfhmm_separate": (ctypes.c_int, [_P, _P, _P]),
+    "nfhmm_destroy": (ctypes.c_int, [_P]),
+    "nfhmm_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "nfhmm_last_error": (ctypes.c_char_p, [_P]),
+    "nfhmm_kernel_launches": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+    "nfhmm_layout": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32),
+                                    ctypes.POINTER(_I32)]),
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+
+
+def library():
+    return _lib
+
+
+def _ptr(x):
+    """Raw address of a numpy array / torch tensor (host or device); None -> NULL."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"], "arrays must be C-contiguous"
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        assert x.is_contiguous(), "tensors must be contiguous"
+        return x.data_ptr()
+    if isinstance(x, int):
+        return x
+    raise TypeError(f"unsupported array type {type(x)}")
+
+
+def _check(h, status):
+    if status != NFHMM_OK:
+        msg = _lib.nfhmm_last_error(h).decode() if h else ""
+        raise NFHMMError(status, msg or _lib.nfhmm_strerror(status).decode())
+
+
+# ---- C-named thin wrappers ------------------------------------------------------------------
+def nfhmm_default_options():
+    o = Options()
+    _lib.nfhmm_default_options(ctypes.byref(o))
+    return o
+
+
+def nfhmm_create(F, T, S, N, K, opt=None):
+    h = ctypes.c_void_p()
+    st = _lib.nfhmm_create(F, T, S, N, K, ctypes.byref(opt) if opt is not None else None, ctypes.byref(h))
+    if st != NFHMM_OK:
+        raise NFHMMError(st, _lib.nfhmm_strerror(st).decode())
+    return h
+
+
+def nfhmm_workspace_size(h):
+    n = ctypes.c_size_t()
+    _check(h, _lib.nfhmm_workspace_size(h, ctypes.byref(n)))
+    return n.value
+
+
+def nfhmm_set_workspace(h, dptr, nbytes):
+    _check(h, _lib.nfhmm_set_workspace(h, dptr, nbytes))
+
+
+def nfhmm_set_model(h, dict_, trans, prior):
+    _check(h, _lib.nfhmm_set_model(h, _ptr(dict_), _ptr(trans), _ptr(prior)))
+
+
+def nfhmm_set_observations(h, V):
+    _check(h, _lib.nfhmm_set_observations(h, _ptr(V)))
+
+
+def nfhmm_reset(h):
+    _check(h, _lib.nfhmm_reset(h))
+
+
+def nfhmm_vb_iterate(h, n_iters):
+    _check(h, _lib.nfhmm_vb_iterate(h, n_iters))
+
+
+def nfhmm_vb_iterate_async(h, n_iters):
+    _check(h, _lib.nfhmm_vb_iterate_async(h, n_iters))
+
+
+def nfhmm_sync(h):
+    _check(h, _lib.nfhmm_sync(h))
+
+
+def nfhmm_posteriors(h, d_hat=None, alpha_hat=None, V_hat=None, free_energy=None):
+    it = ctypes.c_int32()
+    _check(h, _lib.nfhmm_posteriors(h, _ptr(d_hat), _ptr(alpha_hat), _ptr(V_hat), _ptr(free_energy), ctypes.byref(it)))
+    return it.value
+
+
+def nfhmm_separate(h, V_star, V_src=None):
+    _check(h, _lib.nfhmm_separate(h, _ptr(V_star), _ptr(V_src)))
+
+
+def nfhmm_destroy(h):
+    _lib.nfhmm_destroy(h)
+
+
+def nfhmm_kernel_launches(h):
+    n = ctypes.c_int64()
+    _check(h, _lib.nfhmm_kernel_launches(h, ctypes.byref(n)))
+    return n.value
+
+
+def nfhmm_layout(h):
+    fp, kp, br, bb = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+    _check(h, _lib.nfhmm_layout(h, ctypes.byref(fp), ctypes.byref(kp), ctypes.byref(br), ctypes.byref(bb)))
+    return dict(F_pad=fp.value, Kt_pad=kp.value, bn_recon=br.value, bn_backproj=bb.value)
+
+
+# ---- convenience handle -----------------------------------------------------------------------
+class NFHMM:
+    """One libnfhmm handle: n_mix mixtures of F x T counts, S sources x N states x K elements.
+
+    Inputs/outputs may be numpy arrays (host) or torch tensors (host or CUDA).  The workspace is a
+    torch uint8 CUDA tensor owned by this object."""
+
+    def __init__(self, F, T, S, N, K, n_mix=1, gamma=1.0, device=0, max_iters=1024, free_energy=True,
+                 stream=None):
+        import torch
+        self.F, self.T, self.S, self.N, self.K, self.n_mix = F, T, S, N, K, n_mix
+        self.Kt = S * N * K
+        self.max_iters = max_iters
+        self.device = device
+        opt = nfhmm_default_options()
+        opt.n_mix, opt.gamma, opt.device = n_mix, gamma, device
+        opt.max_iters, opt.free_energy = max_iters, 1 if free_energy else 0
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        opt.stream = stream.cuda_stream
+        self.h = nfhmm_create(F, T, S, N, K, opt)
+        nbytes = nfhmm_workspace_size(self.h)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+        nfhmm_set_workspace(self.h, self.workspace.data_ptr(), nbytes)
+
+    def close(self):
+        if getattr(self, "h", None):
+            nfhmm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_model(self, dict_, trans, prior):
+        nfhmm_set_model(self.h, dict_, trans, prior)
+
+    def set_observations(self, V):
+        nfhmm_set_observations(self.h, V)
+
+    def reset(self):
+        nfhmm_reset(self.h)
+
+    def vb_iterate(self, n):
+        nfhmm_vb_iterate(self.h, n)
+
+    def vb_iterate_async(self, n):
+        nfhmm_vb_iterate_async(self.h, n)
+
+    def sync(self):
+        nfhmm_sync(self.h)
+
+    def kernel_launches(self):
+        return nfhmm_kernel_launches(self.h)
+
+    def layout(self):
+        return nfhmm_layout(self.h)
+
+    def posteriors(self, d_hat=True, alpha_hat=True, V_hat=True, free_energy=True):
+        """Returns host numpy arrays: d_hat [M][S][T][N], alpha_hat [M][T][Kt], V_hat [M][T][F],
+        free_energy [M][iters_done] (FP64), iters_done."""
+        M, S, T, N, F, Kt = self.n_mix, self.S, self.T, self.N, self.F, self.Kt
+        d = np.empty((M, S, T, N), np.float32) if d_hat else None
+        a = np.empty((M, T, Kt), np.float32) if alpha_hat else None
+        v = np.empty((M, T, F), np.float32) if V_hat else None
+        fe = np.empty((M, self.max_iters), np.float64) if free_energy else None
+        it = nfhmm_posteriors(self.h, d, a, v, fe)
+        out = dict(iters_done=it)
+        if d is not None:
+            out["d_hat"] = d
+        if a is not None:
+            out["alpha_hat"] = a
+        if v is not None:
+            out["V_hat"] = v
+        if fe is not None:
+            out["free_energy"] = fe[:, :min(it, self.max_iters)]
+        return out
+
+    def separate(self, V_src=False):
+        M, S, T, F = self.n_mix, self.S, self.T, self.F
+        vst = np.empty((M, S, T, F), np.float32)
+        vs = np.empty((M, S, T, F), np.float32) if V_src else None
+        nfhmm_separate(self.h, vst, vs)
+        return (vst, vs) if V_src else vst

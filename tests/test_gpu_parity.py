@@ -1,0 +1,150 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the FP64 oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  after 1 sweep:             d_hat, V_hat (and alpha_hat) rel-L2 <= 1e-5
+  after the config's sweeps: V_star rel-L2 <= 1e-3, free energy rel <= 1e-5 (every sweep)
+  every sweep (GPU):         free energy non-decreasing within 1e-6 |L|
+Sizes span several 128-frame tiles with a ragged tail; configs 1-4 are run at reduced T / M here and
+at full size in test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+
+from tests.gpu_common import make_inputs, rel_l2, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL1 = 1e-5
+TOL_VSTAR = 1e-3
+TOL_L = 1e-5
+
+
+def check_parity(cfg, model, V, iters, gamma=1.0, mixtures=None, tol1=TOL1):
+    g1 = run_gpu(cfg, model, V, 1, gamma=gamma, separate=False)
+    gn = run_gpu(cfg, model, V, iters, gamma=gamma)
+    for m in (mixtures if mixtures is not None else range(V.shape[0])):
+        o1 = run_oracle(cfg, model, V[m], 1, gamma=gamma, separate=False)
+        assert rel_l2(g1["d_hat"][m], o1["d_hat"]) <= tol1
+        assert rel_l2(g1["V_hat"][m], o1["V_hat"]) <= tol1
+        assert rel_l2(g1["alpha_hat"][m], o1["alpha"]) <= tol1
+        assert abs(g1["free_energy"][m, 0] - o1["free_energy"][0]) <= TOL_L * abs(o1["free_energy"][0])
+        on = run_oracle(cfg, model, V[m], iters, gamma=gamma)
+        assert rel_l2(gn["V_star"][m], on["V_star"]) <= TOL_VSTAR
+        assert rel_l2(gn["V_src"][m], on["V_src"]) <= TOL_VSTAR
+        fe_g, fe_o = gn["free_energy"][m], on["free_energy"]
+        assert fe_g.shape == fe_o.shape
+        assert np.all(np.abs(fe_g - fe_o) <= TOL_L * np.abs(fe_o)), np.max(np.abs(fe_g - fe_o) / np.abs(fe_o))
+        assert np.all(np.diff(fe_g) >= -1e-6 * np.abs(fe_g[1:]))
+    return g1, gn
+
+
+def test_cfg0_tiny_full():
+    cfg, model, V = make_inputs(0)
+    g1, gn = check_parity(cfg, model, V, cfg.iters)
+    assert gn["iters_done"] == cfg.iters
+
+
+def test_cfg1_reduced_T200():
+    cfg, model, V = make_inputs(1, T=200)
+    check_parity(cfg, model, V, 30)
+
+
+def test_cfg2_three_sources_reduced():
+    cfg, model, V = make_inputs(2, T=150)
+    check_parity(cfg, model, V, 20)
+
+
+def test_cfg3_batched_reduced_multi_mixture():
+    cfg, model, V = make_inputs(3, T=300, M=3)
+    check_parity(cfg, model, V, 15)
+
+
+def test_cfg4_large_reduced():
+    cfg, model, V = make_inputs(4, T=40, M=2)
+    check_parity(cfg, model, V, 4, mixtures=[1])
+
+
+@pytest.mark.parametrize("gamma", [0.0, 2.5])
+def test_gamma_values(gamma):
+    cfg, model, V = make_inputs(0, T=70)
+    check_parity(cfg, model, V, 10, gamma=gamma)
+
+
+@pytest.mark.parametrize("shape", [dict(S=1, N=3, K=2, F=17, T=1), dict(S=1, N=1, K=1, F=5, T=9),
+                                   dict(S=2, N=1, K=5, F=64, T=129), dict(S=2, N=33, K=1, F=40, T=31),
+                                   dict(S=3, N=2, K=3, F=9, T=257)])
+def test_edge_shapes(shape):
+    cfg, model, V = make_inputs(0, counts=500, **shape)
+    check_parity(cfg, model, V, 6)
+
+
+def test_empty_frames_and_sharding_invariance():
+    """Frames with V = 0 are legal (alpha = prior pseudo-counts); per-mixture results are bitwise the
+    same whether a mixture runs alone or batched with others (the multi-GPU sharding invariant)."""
+    cfg, model, V = make_inputs(3, T=150, M=3, counts=2000)
+    V[1, 10:20] = 0.0
+    batched = run_gpu(cfg, model, V, 5)
+    for m in range(3):
+        single = run_gpu(cfg, model, V[m:m + 1], 5)
+        for key in ("d_hat", "alpha_hat", "V_hat", "free_energy", "V_star", "V_src"):
+            np.testing.assert_array_equal(batched[key][m], single[key][0], err_msg=key)
+    o = run_oracle(cfg, model, V[1], 5)
+    assert rel_l2(batched["V_star"][1], o["V_star"]) <= TOL_VSTAR
+    np.testing.assert_allclose(batched["V_star"][1].sum(0), V[1], rtol=1e-5, atol=1e-3)
+
+
+def test_resume_equals_single_call_and_device_io():
+    cfg, model, V = make_inputs(0)
+    a = run_gpu(cfg, model, V, 7)
+    b = run_gpu(cfg, model, V, 7, split=[3, 1, 3])
+    c = run_gpu(cfg, model, V, 7, device_io=True)
+    for key in ("d_hat", "alpha_hat", "V_hat", "free_energy", "V_star"):
+        np.testing.assert_array_equal(a[key], b[key], err_msg=key)
+        np.testing.assert_array_equal(a[key], c[key], err_msg=key)
+
+
+def test_invariants_on_gpu_outputs():
+    cfg, model, V = make_inputs(1, T=257)
+    g = run_gpu(cfg, model, V, 10)
+    np.testing.assert_allclose(g["d_hat"].sum(-1), 1.0, atol=2e-6)
+    assert (g["alpha_hat"] >= 1.0).all()
+    Kt = cfg.Kt
+    np.testing.assert_allclose(g["alpha_hat"].sum(-1), V.sum(-1) + Kt + cfg.S * cfg.K, rtol=2e-6)
+    np.testing.assert_allclose(g["V_star"].sum(1), V, rtol=1e-5, atol=1e-3)
+    np.testing.assert_allclose(g["V_src"].sum((1, 3)), V.sum(-1), rtol=1e-5)
+
+
+def test_errors_are_explicit():
+    import torch
+    from paper_1206_6468_b200.nfhmm import NFHMM, NFHMMError, NFHMM_EINVAL, NFHMM_ESTATE, NFHMM_EZEROSUPPORT
+    cfg, model, V = make_inputs(0)
+    h = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K)
+    with pytest.raises(NFHMMError) as e:
+        h.vb_iterate(1)
+    assert e.value.status == NFHMM_ESTATE
+    bad = model.beta.copy()
+    bad[0, 0, 0, 0] += 0.5
+    with pytest.raises(NFHMMError) as e:
+        h.set_model(bad, model.trans, model.prior)
+    assert e.value.status == NFHMM_EINVAL
+    h.set_model(model.beta, model.trans, model.prior)
+    Vn = V.copy()
+    Vn[0, 3, 4] = -1.0
+    with pytest.raises(NFHMMError) as e:
+        h.set_observations(Vn)
+        h.vb_iterate(1)
+    assert e.value.status == NFHMM_EINVAL
+    # zero support: a bin no dictionary element covers, with counts in it
+    zb = model.beta.copy()
+    zb[..., 0] = 0.0
+    zb /= zb.sum(-1, keepdims=True)
+    h2 = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K)
+    h2.set_model(zb, model.trans, model.prior)
+    Vz = V.copy()
+    Vz[0, :, 0] = 3.0
+    with pytest.raises(NFHMMError) as e:
+        h2.set_observations(Vz)
+        h2.vb_iterate(1)
+    assert e.value.status == NFHMM_EZEROSUPPORT
+    h.close()
+    h2.close()
