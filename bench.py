@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the VB inference hot path (BASELINE.json metric: frame-iterations/s).
+
+One "step" = one full inference job on this rank's shard of the workload: nfhmm_reset (initial state
++ z-step), `iters` VB sweeps (all of SURVEY §8(a) rows a-e, g, h) and nfhmm_separate (row f), with
+the inputs already resident in HBM.  frame-iterations per step = mixtures * T * iters.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+N > 1: launched by torch.distributed.run, one rank per GPU; the config's mixtures are sharded across
+ranks (mixture m on rank m * N // M ... contiguous blocks), no collective on the data path; timings are
+all-reduced with MAX (NCCL) after the timed region.  Prints ONE JSON line on rank 0.
+
+--impl reference: the CPU oracle (oracle/, FP64, single-threaded per process) on the host cores,
+timed as it stands on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1206_6468_b200 import synth  # noqa: E402
+
+METRIC = "frame-iterations/sec (S=2,N=40,K=10,F=513) at 1/2/4/8 B200; % FP32/HBM roofline"
+UNIT = "frame-iterations/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--iters", type=int, default=None, help="VB sweeps per step (default: the config's)")
+    ap.add_argument("--mixtures", type=int, default=None, help="override total mixtures (default: config)")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds for the oracle sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(M, world, rank):
+    lo = rank * M // world
+    hi = (rank + 1) * M // world
+    return list(range(lo, hi))
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names[1:], parts[5:9]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline leg and --impl reference)
+# ------------------------------------------------------------------------------------------------
+def _oracle_job(args):
+    cfg, model, V, iters = args
+    from oracle import oracle
+    t0 = time.perf_counter()
+    oracle.vb_run(model.beta, model.trans, model.prior, V, cfg.dims, iters)
+    return time.perf_counter() - t0
+
+
+def oracle_sample(cfg, model, V0, target_s, procs=1):
+    """Time the oracle as it stands on a bounded sample: `procs` independent single-threaded processes,
+    each running `iters` sweeps of one mixture truncated to T_s frames.  Returns (value, cores, sample)."""
+    from oracle import oracle
+    oracle.build()
+    T_s = min(cfg.T, 250)
+    sub = synth.Config(**{**cfg.__dict__, "T": T_s})
+    Vs = np.ascontiguousarray(V0[:T_s])
+    t1 = _oracle_job((sub, model, Vs, 1))                       # calibrate one sweep
+    iters = max(1, min(50, int(target_s / max(t1, 1e-3))))
+    if procs <= 1:
+        dt = _oracle_job((sub, model, Vs, iters))
+        wall = dt
+    else:
+        from concurrent.futures import ProcessPoolExecutor
+        with ProcessPoolExecutor(max_workers=procs) as ex:
+            t0 = time.perf_counter()
+            list(ex.map(_oracle_job, [(sub, model, Vs, iters)] * procs))
+            wall = time.perf_counter() - t0
+    value = procs * T_s * iters / wall
+    sample = (f"{procs} process(es) x 1 mixture x T={T_s} frames x {iters} sweeps of cfg{cfg_id(cfg)} "
+              f"(S={cfg.S},N={cfg.N},K={cfg.K},F={cfg.F}); {wall:.1f} s wall")
+    return value, procs, sample
+
+
+def cfg_id(cfg):
+    for k, v in synth.CONFIGS.items():
+        if v.name == cfg.name:
+            return k
+    return "?"
+
+
+# ------------------------------------------------------------------------------------------------
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = synth.config(args.config)
+    if args.mixtures:
+        cfg = synth.Config(**{**cfg.__dict__, "M": args.mixtures})
+    iters = args.iters or cfg.iters
+    seed = synth.seed_of(args.config)
+    model = synth.make_model(cfg, seed)
+    procs = max(1, min(os.cpu_count() or 1, 16))
+    # one step = every process runs its sample once; the sample is sized so all steps fit in minutes
+    per_step_s = max(2.0, min(20.0, 240.0 / max(1, args.steps + args.warmup)))
+    Vs = [synth.make_mixture(cfg, model, seed, m).V for m in range(min(procs, cfg.M))]
+    from concurrent.futures import ProcessPoolExecutor
+    from oracle import oracle
+    oracle.build()
+    T_s = min(cfg.T, 250)
+    sub = synth.Config(**{**cfg.__dict__, "T": T_s})
+    t1 = _oracle_job((sub, model, np.ascontiguousarray(Vs[0][:T_s]), 1))
+    sweeps = max(1, int(per_step_s / max(t1, 1e-3)))
+    jobs = [(sub, model, np.ascontiguousarray(Vs[i % len(Vs)][:T_s]), sweeps) for i in range(procs)]
+    times = []
+    with ProcessPoolExecutor(max_workers=procs) as ex:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            list(ex.map(_oracle_job, jobs))
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+    ms = 1000.0 * (max(times) if times else float("nan"))
+    value = procs * T_s * sweeps / (ms / 1000.0)
+    sample = f"{procs} processes x 1 mixture x T={T_s} frames x {sweeps} sweeps per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg{args.config}-{cfg.name}", "S": cfg.S, "N": cfg.N, "K": cfg.K, "F": cfg.F,
+                   "T": cfg.T, "mixtures": cfg.M, "iters": iters},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    from paper_1206_6468_b200.nfhmm import NFHMM, KERNEL_CLASSES
+
+    cfg = synth.config(args.config)
+    if args.mixtures:
+        cfg = synth.Config(**{**cfg.__dict__, "M": args.mixtures})
+    iters = args.iters or cfg.iters
+    seed = synth.seed_of(args.config)
+    model = synth.make_model(cfg, seed)
+    mine = shard(cfg.M, world, rank)
+    M = len(mine)
+    t_gen = time.perf_counter()
+    V = synth.make_batch(cfg, model, seed, mine)           # [M][T][F] float32, this rank's shard only
+    t_gen = time.perf_counter() - t_gen
+
+    stream = torch.cuda.current_stream(dev)
+    h = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, device=dev, max_iters=max(iters, 1), stream=stream)
+    h.set_model(model.beta, model.trans, model.prior)
+    Vd = torch.from_numpy(V).to(f"cuda:{dev}")
+    h.set_observations(Vd)
+    vstar_d = torch.empty((M, cfg.S, cfg.T, cfg.F), dtype=torch.float32, device=f"cuda:{dev}")
+
+    def step():
+        h.reset()
+        h.vb_iterate_async(iters)
+        h.separate_into(vstar_d)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(dev)
+    clocks.start()
+    l0 = h.kernel_launches()
+    h.profile_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    prof = h.profile_read()
+    h.profile_enable(False)
+    launches = h.kernel_launches() - l0 - 0  # profile bookkeeping launches nothing
+    clk = clocks.stop()
+    elapsed = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        dist.barrier()
+    ms_per_step = elapsed / args.steps
+    frame_iters = cfg.M * cfg.T * iters                     # whole job, all ranks
+    value = frame_iters / (ms_per_step / 1000.0)
+
+    # ---- e2e: public API with host buffers, copies inside the timed region -------------------
+    e2e = None
+    if not args.no_e2e:
+        Vh = torch.from_numpy(V).pin_memory()
+        out_h = torch.empty((M, cfg.S, cfg.T, cfg.F), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            h.set_observations(Vh)
+            h.vb_iterate_async(iters)
+            h.separate_into(out_h)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        el = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": frame_iters / (el / args.steps / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(Vh.numel() * 4) * world, "d2h_bytes_per_step": int(out_h.numel() * 4) * world,
+               "ms_per_step": el / args.steps}
+
+    # ---- roofline of the dominant kernel ------------------------------------------------------
+    peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # TFLOP/s, FFMA pipe (DESIGN "Rooflines")
+    hbm_peak = float(peaks.get("hbm_gbs", 6539.2))
+    dom = max(("recon", "backproj", "dirichlet", "fb"), key=lambda k: prof[k][0])
+    ms_k, n_k = prof[dom]
+    frames_local = M * cfg.T
+    if dom in ("recon", "backproj"):
+        flops = 2.0 * frames_local * cfg.F * cfg.Kt       # algorithmic FLOPs per launch (true F, Kt)
+        achieved = flops / (ms_k / n_k / 1000.0) / 1e12
+        roof = {"kernel": dom, "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "peak_note": f"FP32 FFMA 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz"}
+    else:
+        if dom == "dirichlet":
+            byts = frames_local * (3 * cfg.Kt * 4 + cfg.S * cfg.N * 4 * 2 + cfg.S * 8 + 8)
+        else:
+            byts = M * cfg.S * cfg.T * (cfg.N * 4 * 4 + 4 * 2 + 8)
+        achieved = byts / (ms_k / n_k / 1000.0) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        tr = json.load(open(tpath)).get(f"cfg{args.config}", {}).get(dom)
+        if tr:
+            traffic = tr.get("dram_bytes_per_launch")
+    roof["traffic"] = traffic
+    kernels = {k: {"ms_per_step": prof[k][0] / args.steps, "launches_per_step": prof[k][1] / args.steps}
+               for k in KERNEL_CLASSES if prof[k][1]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        val, cores, sample = oracle_sample(cfg, model, V[0], args.cpu_seconds, procs=1)
+        cpu = {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"cfg{args.config}-{cfg.name}", "S": cfg.S, "N": cfg.N, "K": cfg.K, "F": cfg.F,
+                       "T": cfg.T, "mixtures": cfg.M, "iters": iters, "parallelism": f"mixture-shard x{world}",
+                       "l2": "no flush: per-step inputs/state exceed L2 (V %.2f GB, theta %.2f GB per GPU)" % (
+                           M * cfg.T * h.layout()["F_pad"] * 4 / 1e9, M * cfg.T * h.layout()["Kt_pad"] * 4 / 1e9),
+                       "step": "reset + iters sweeps + separate, inputs resident in HBM"},
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": launches, "gen_seconds": round(t_gen, 2),
+        }
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -140,6 +140,22 @@ int nfhmm_kernel_launches(const nfhmm_t *h, int64_t *count);
 int nfhmm_layout(const nfhmm_t *h, int64_t *F_pad, int64_t *Kt_pad, int32_t *bn_recon,
                  int32_t *bn_backproj);
 
+/* Per-kernel-class device timing: when enabled, every launch on the handle's stream is bracketed by
+ * CUDA events (no host synchronisation).  Classes: */
+#define NFHMM_K_RECON 0      /* (a) reconstruction GEMM + ratio epilogue (z-step, Eq. 7)          */
+#define NFHMM_K_BACKPROJ 1   /* (b) back-projection GEMM (Eq. 6 data term)                          */
+#define NFHMM_K_DIRICHLET 2  /* (c)+(d) Eq. 6 update, digamma/exp, Eq. 8                             */
+#define NFHMM_K_FB 3         /* (e) forward-backward                                                 */
+#define NFHMM_K_ELBO 4       /* (g) bound reduction                                                  */
+#define NFHMM_K_SEPARATE 5   /* (f) Section 4 reconstruction GEMMs + ratio mask                      */
+#define NFHMM_K_OTHER 6      /* initial state, observation statistics, dictionary transpose          */
+#define NFHMM_NUM_KERNEL_CLASSES 7
+/* on != 0 starts recording (and clears previous records); on = 0 stops. */
+int nfhmm_profile_enable(nfhmm_t *h, int on);
+/* Synchronise and return, per class, the summed device milliseconds and launch counts recorded since
+ * the last enable.  Both arrays have NFHMM_NUM_KERNEL_CLASSES entries; either may be NULL. */
+int nfhmm_profile_read(nfhmm_t *h, double *ms, int64_t *launches);
+
 #ifdef __cplusplus
 }
 #endif

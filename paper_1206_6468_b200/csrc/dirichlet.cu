@@ -1,14 +1,16 @@
-// dirichlet.cu -- kernels (c) and (d) of the VB sweep, fused: one CTA per frame.
+// dirichlet.cu -- kernels (c) and (d) of the VB sweep, fused: one warp per frame, no block barriers.
 //
-//   (c) Eq. 6:  alpha_k = n_k + gamma * d^{(s(k))}_{t, n(k)} + 1, alpha_0 = sum_k alpha_k (FP64),
+//   (c) Eq. 6:  alpha_k = n_k + gamma * d^{(s(k))}_{t, n(k)} + 1,  alpha_0 = sum_k alpha_k (FP64),
 //       Eq. 7 weights: theta_k = exp(psi(alpha_k) - psi(alpha_0));
-//   (d) Eq. 8:  phi_n^{(s)} = sum_{j<K} psi(alpha_{(sN+n)K+j}) - K psi(alpha_0), emitted to the
-//       forward-backward as gamma * phi (DESIGN R1), centred per (s, t): ec = gamma (phi - max_n phi),
-//       eoff = gamma max_n phi in FP64 (the FB is shift-invariant per frame);
+//   (d) Eq. 8:  phi_n^{(s)} = sum_{j<K} psi(alpha_{(sN+n)K+j}) - K psi(alpha_0), handed to the
+//       forward-backward as gamma * phi (DESIGN R1), centred per (s, t): ec = gamma (phi - max_n phi) in
+//       FP32 and eoff = gamma max_n phi in FP64 (the FB is shift-invariant per frame);
 //   bound term (DESIGN R8): H_t = sum_k [lnG(alpha_k) - (alpha_k - 1) psi(alpha_k)]
-//                                 - lnG(alpha_0) + (alpha_0 - Kt) psi(alpha_0)   (FP64 accumulation).
-// HBM-bound: reads n (Kt floats) + d (S N), writes alpha, theta (2 Kt) + phi (S N) per frame,
-// 128-bit vectorised and coalesced; the per-block sums of Eq. 8 read psi back from shared memory.
+//                                 - lnG(alpha_0) + (alpha_0 - Kt) psi(alpha_0)      (FP64 accumulation).
+// HBM-bound: per frame it reads n (Kt floats) + d (S N) and writes alpha, theta (2 Kt) + phi (S N).
+// Pass 1 streams the row with 128-bit loads for alpha_0; pass 2 re-reads it (L1/L2-resident) in chunks
+// of 32 (s, n) blocks staged through shared memory, so that each lane owns whole blocks (the Eq. 8
+// segment sums need no cross-lane reduction) while global loads and stores stay coalesced float4.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -18,17 +20,38 @@ namespace nfk {
 
 namespace {
 
-// psi(x) for x >= 1 (alpha >= 1 by Eq. 6).  Recurrence to x >= 6, then the asymptotic series to
-// x^-10 (truncation < 1e-11 at x = 6); IEEE FP32, no fast-math (DESIGN R14).
-__device__ __forceinline__ float digammaf_pos(float x) {
-    float r = 0.f;
-    while (x < 6.f) {
-        r -= 1.f / x;
-        x += 1.f;
+constexpr int WPB = 8;   // frames (warps) per CTA
+
+// psi(x) and lnGamma(x) for x >= 1 (alpha >= 1 by Eq. 6), IEEE FP32 without fast-math (DESIGN R14).
+// x < 6 is shifted by 5 with psi(x) = psi(x+5) - sum_{i<5} 1/(x+i), the five reciprocals folded into
+// one quotient, and lnGamma(x) = lnGamma(x+5) - ln prod_{i<5}(x+i); then the asymptotic series
+// psi(y) = ln y - 1/(2y) - 1/(12y^2) + 1/(120y^4) - 1/(252y^6) + 1/(240y^8)   (trunc. < 2e-9 at y = 6)
+// lnG(y) = (y - 1/2) ln y - y + ln(2 pi)/2 + 1/(12y) - 1/(360y^3) + 1/(1260y^5)  (trunc. < 2e-8 at y = 6)
+struct PsiLg {
+    float psi, lng;
+};
+__device__ __forceinline__ PsiLg psi_lngamma(float x, bool want_lng) {
+    float rs = 0.f, lprod = 0.f;
+    if (x < 6.f) {
+        const float a0 = x, a1 = x + 1.f, a2 = x + 2.f, a3 = x + 3.f, a4 = x + 4.f;
+        const float p01 = a0 * a1, p23 = a2 * a3;
+        const float num4 = (a0 + a1) * p23 + (a2 + a3) * p01;
+        const float den4 = p01 * p23;
+        const float den = den4 * a4;
+        rs = (num4 * a4 + den4) / den;      // sum_{i<5} 1/(x+i)
+        if (want_lng) lprod = logf(den);
+        x += 5.f;
     }
-    const float f = 1.f / (x * x);
-    const float t = f * (-1.f / 12.f + f * (1.f / 120.f + f * (-1.f / 252.f + f * (1.f / 240.f + f * (-1.f / 132.f)))));
-    return r + logf(x) - 0.5f / x + t;
+    const float r = 1.f / x;
+    const float f = r * r;
+    const float ly = logf(x);
+    const float ser = f * (-1.f / 12.f + f * (1.f / 120.f + f * (-1.f / 252.f + f * (1.f / 240.f))));
+    PsiLg o;
+    o.psi = ly - 0.5f * r + ser - rs;
+    o.lng = 0.f;
+    if (want_lng)
+        o.lng = (x - 0.5f) * ly - x + 0.91893853320467274f + r * (1.f / 12.f + f * (-1.f / 360.f + f * (1.f / 1260.f))) - lprod;
+    return o;
 }
 
 __device__ double digamma_d(double x) {
@@ -43,13 +66,12 @@ __device__ double digamma_d(double x) {
     return r + log(x) - 0.5 / x + t;
 }
 
-// g(a) = lnGamma(a) - (a - 1) psi(a): FP32 for a < 64 (no catastrophic cancellation there), FP64
-// Stirling form for large a, where lnGamma and (a-1)psi are both ~a ln a and cancel to ~ -a.
-__device__ __forceinline__ double gterm(float a, float psi_a) {
-    if (a < 64.f) return (double)(lgammaf(a) - (a - 1.f) * psi_a);
+// g(a) = lnGamma(a) - (a - 1) psi(a).  FP32 below 64 (no catastrophic cancellation there); above, the
+// FP64 Stirling form (lnGamma and (a-1) psi are both ~ a ln a and cancel to ~ -a):
+// g(x) = ln(x)/2 - x + ln(2 pi)/2 + 1/2 - 1/(3x) - 1/(12x^2) - 1/(90x^3) + 1/(120x^4) + 1/(1260x^5) + ...
+__device__ __forceinline__ double gterm(float a, const PsiLg &pl) {
+    if (a < 64.f) return (double)(pl.lng - (a - 1.f) * pl.psi);
     const double x = a, ix = 1.0 / x, ix2 = ix * ix;
-    // lnG(x) - (x-1) psi(x) = 0.5 ln x - x + 0.5 ln(2 pi) + 0.5 - 1/(3x) - 1/(12x^2) - 1/(90x^3) + 1/(120 x^4) ...
-    // (derived from the Stirling series of lnGamma and the asymptotic series of psi; terms to x^-5)
     const double series = -ix / 3.0 - ix2 / 12.0 - ix2 * ix / 90.0 + ix2 * ix2 / 120.0 + ix2 * ix2 * ix / 1260.0;
     return 0.5 * log(x) - x + 0.91893853320467274178 + 0.5 + series;
 }
@@ -59,115 +81,112 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-
-// Block-wide FP64 sum with a fixed reduction tree (deterministic).  All threads get the result.
-__device__ double block_sum_d(double v, double *scratch) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    v = warp_sum_d(v);
-    __syncthreads();
-    if (lane == 0) scratch[w] = v;
-    __syncthreads();
-    double s = 0.0;
-    for (int i = 0; i < nw; ++i) s += scratch[i];
-    return s;
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
 }
 
-__global__ void __launch_bounds__(128) dirichlet_kernel(DirichletArgs p) {
+__global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // layout: row [ld] floats (alpha, then psi) | dsm [S*N] floats | sps [S*N] doubles | mx [S] doubles | scratch [4]
-    float *row = reinterpret_cast<float *>(smem_raw);
-    const int SN = p.S * p.N;
-    float *dsm = row + p.ld;
-    double *sps = reinterpret_cast<double *>(reinterpret_cast<uintptr_t>(dsm + SN + 1) & ~uintptr_t(7));
-    double *mx = sps + SN;
-    double *scratch = mx + p.S;
-    __shared__ double s_psi0;
+    const int SN = p.S * p.N, K = p.K, CK = 32 * K;   // CK = elements per chunk of 32 blocks
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // per warp: sps [SN] doubles | dsm [SN] floats | ca [CK] floats | ct [CK] floats (16-B aligned pieces)
+    const size_t sps_b = ((size_t)SN * 8 + 15) & ~size_t(15), dsm_b = ((size_t)SN * 4 + 15) & ~size_t(15);
+    const size_t per_warp = sps_b + dsm_b + 2 * (((size_t)CK * 4 + 15) & ~size_t(15));   // multiple of 16
+    unsigned char *base = smem_raw + warp * per_warp;
+    double *sps = reinterpret_cast<double *>(base);
+    float *dsm = reinterpret_cast<float *>(base + sps_b);
+    float *ca = reinterpret_cast<float *>(base + sps_b + dsm_b);
+    float *ct = ca + ((CK + 3) & ~3);
 
-    const int f = blockIdx.x;
+    const int f = blockIdx.x * WPB + warp;
+    if (f >= p.frames) return;
     const int m = f / p.T, t = f - m * p.T;
-    const int tid = threadIdx.x;
-    const int nv = p.ld >> 2;
+    const float gamma = p.gamma;
 
-    for (int b = tid; b < SN; b += blockDim.x) {
-        const int s = b / p.N, n = b - s * p.N;
-        dsm[b] = p.d_hat[((size_t)(m * p.S + s) * p.T + t) * p.N + n];
-    }
-    __syncthreads();
-
-    // Eq. 6: alpha_k = n_k + gamma d_{s(k), n(k)} + 1, kept in shared memory; alpha_0 in FP64.
-    const float4 *nin = reinterpret_cast<const float4 *>(p.n_in + (size_t)f * p.ld);
-    double a0p = 0.0;
-    for (int q = tid; q < nv; q += blockDim.x) {
-        const float4 v = nin[q];
-        const float vv[4] = {v.x, v.y, v.z, v.w};
-        float a[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int k = 4 * q + j;
-            a[j] = k < p.Kt ? vv[j] + p.gamma * dsm[k / p.K] + 1.f : 0.f;
-            a0p += (double)a[j];
+    // d of the previous sweep for this frame (one coalesced row of N per source)
+    double dsum = 0.0;
+    for (int s = 0; s < p.S; ++s) {
+        const float *src = p.d_hat + ((size_t)(m * p.S + s) * p.T + t) * p.N;
+        for (int n = lane; n < p.N; n += 32) {
+            const float v = src[n];
+            dsm[s * p.N + n] = v;
+            dsum += (double)v;
         }
-        *reinterpret_cast<float4 *>(row + 4 * q) = make_float4(a[0], a[1], a[2], a[3]);
     }
-    const double a0 = block_sum_d(a0p, scratch);
-    if (tid == 0) s_psi0 = digamma_d(a0);
-    __syncthreads();
-    const double psi0 = s_psi0;
+    // pass 1: alpha_0 = sum_k n_k + Kt + gamma K sum_{s,n} d   (FP64)
+    const float4 *nin = reinterpret_cast<const float4 *>(p.n_in + (size_t)f * p.ld);
+    const int nv = p.ld >> 2;
+    double nsum = 0.0;
+    for (int q = lane; q < nv; q += 32) {
+        const float4 v = nin[q];
+        nsum += ((double)v.x + (double)v.y) + ((double)v.z + (double)v.w);
+    }
+    const double a0 = warp_sum_d(nsum) + (double)p.Kt + (double)gamma * (double)K * warp_sum_d(dsum);
+    const double psi0 = digamma_d(a0);
     const float psi0f = (float)psi0;
+    __syncwarp();
 
-    // Eq. 7 weights theta = exp(psi(alpha) - psi(alpha_0)); psi kept for Eq. 8; bound terms.
+    // pass 2: chunks of 32 blocks; lane b owns block (c*32 + b)
     float4 *aout = reinterpret_cast<float4 *>(p.alpha + (size_t)f * p.ld);
     float4 *tout = reinterpret_cast<float4 *>(p.theta + (size_t)f * p.ld);
+    const bool want_h = p.hdir != nullptr;
     double hp = 0.0;
     unsigned bad = 0;
-    for (int q = tid; q < nv; q += blockDim.x) {
-        const float4 a4 = *reinterpret_cast<const float4 *>(row + 4 * q);
-        const float a[4] = {a4.x, a4.y, a4.z, a4.w};
-        float ps[4], th[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int k = 4 * q + j;
-            if (k < p.Kt) {
-                ps[j] = digammaf_pos(a[j]);
-                th[j] = expf(ps[j] - psi0f);
-                if (p.hdir) hp += gterm(a[j], ps[j]);
-                if (!isfinite(a[j]) || !isfinite(th[j])) bad |= FLAG_NONFINITE;
-            } else {
-                ps[j] = 0.f;
-                th[j] = 0.f;
+    for (int c0 = 0; c0 < p.Kt; c0 += CK) {
+        const int cend = min(c0 + CK, p.Kt);
+        const int q0 = c0 >> 2, q1 = (cend + 3) >> 2;      // float4 range covering the chunk
+        for (int q = q0 + lane; q < q1; q += 32) reinterpret_cast<float4 *>(ca)[q - q0] = nin[q];
+        __syncwarp();
+        const int b = (c0 / K) + lane;                        // global block index
+        if (b < SN) {
+            const float dv = gamma * dsm[b] + 1.f;
+            float *pa = ca + lane * K, *pt = ct + lane * K;
+            double sp = 0.0;
+            for (int j = 0; j < K; ++j) {
+                const float a = pa[j] + dv;
+                const PsiLg pl = psi_lngamma(a, want_h);
+                const float th = expf(pl.psi - psi0f);
+                pa[j] = a;
+                pt[j] = th;
+                sp += (double)pl.psi;
+                if (want_h) hp += gterm(a, pl);
+                if (!isfinite(a) || !isfinite(th)) bad |= FLAG_NONFINITE;
             }
+            sps[b] = sp;
         }
-        aout[q] = a4;
-        tout[q] = make_float4(th[0], th[1], th[2], th[3]);
-        *reinterpret_cast<float4 *>(row + 4 * q) = make_float4(ps[0], ps[1], ps[2], ps[3]);
+        __syncwarp();
+        for (int q = q0 + lane; q < q1; q += 32) {
+            float4 av = reinterpret_cast<const float4 *>(ca)[q - q0];
+            float4 tv = reinterpret_cast<const float4 *>(ct)[q - q0];
+            const int k = 4 * q;
+            if (k + 0 >= p.Kt) av.x = tv.x = 0.f;
+            if (k + 1 >= p.Kt) av.y = tv.y = 0.f;
+            if (k + 2 >= p.Kt) av.z = tv.z = 0.f;
+            if (k + 3 >= p.Kt) av.w = tv.w = 0.f;
+            aout[q] = av;
+            tout[q] = tv;
+        }
+        __syncwarp();
     }
-    __syncthreads();
 
-    // Eq. 8 block sums (FP64) of psi over the K elements of each (s, n) block.
-    for (int b = tid; b < SN; b += blockDim.x) {
-        double acc = 0.0;
-        const float *pp = row + b * p.K;
-        for (int j = 0; j < p.K; ++j) acc += (double)pp[j];
-        sps[b] = acc;
+    // Eq. 8: centre per source and emit
+    for (int s = 0; s < p.S; ++s) {
+        double mx = -INFINITY;
+        for (int n = lane; n < p.N; n += 32) mx = fmax(mx, sps[s * p.N + n]);
+        mx = warp_max_d(mx);
+        float *dst = p.ec + ((size_t)(m * p.S + s) * p.T + t) * p.N;
+        for (int n = lane; n < p.N; n += 32) dst[n] = (float)((double)gamma * (sps[s * p.N + n] - mx));
+        if (lane == 0) {
+            const double off = (double)gamma * (mx - (double)K * psi0);
+            p.eoff[(size_t)(m * p.S + s) * p.T + t] = off;
+            if (!isfinite(off)) bad |= FLAG_NONFINITE;
+        }
     }
-    __syncthreads();
-    if (tid < p.S) {
-        double mm = -INFINITY;
-        for (int n = 0; n < p.N; ++n) mm = fmax(mm, sps[tid * p.N + n]);
-        mx[tid] = mm;
-        const size_t o = (size_t)(m * p.S + tid) * p.T + t;
-        const double off = (double)p.gamma * (mm - (double)p.K * psi0);
-        p.eoff[o] = off;
-        if (!isfinite(off)) bad |= FLAG_NONFINITE;
-    }
-    __syncthreads();
-    for (int b = tid; b < SN; b += blockDim.x) {
-        const int s = b / p.N, n = b - s * p.N;
-        p.ec[((size_t)(m * p.S + s) * p.T + t) * p.N + n] = (float)((double)p.gamma * (sps[b] - mx[s]));
-    }
-    if (p.hdir) {
-        const double h = block_sum_d(hp, scratch);
-        if (tid == 0) p.hdir[f] = h - lgamma(a0) + (a0 - (double)p.Kt) * psi0;
+    if (want_h) {
+        const double h = warp_sum_d(hp);
+        if (lane == 0) p.hdir[f] = h - lgamma(a0) + (a0 - (double)p.Kt) * psi0;
     }
     if (bad) atomicOr(p.flags, bad);
 }
@@ -175,15 +194,17 @@ __global__ void __launch_bounds__(128) dirichlet_kernel(DirichletArgs p) {
 }  // namespace
 
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
-    const int SN = a.S * a.N;
-    size_t smem = (size_t)a.ld * 4 + (size_t)SN * 4 + 16 + (size_t)SN * 8 + (size_t)a.S * 8 + 4 * 8;
-    smem = (smem + 15) & ~size_t(15);
-    static bool attr_set = false;
-    if (smem > 48 * 1024 && !attr_set) {
-        cudaFuncSetAttribute(dirichlet_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr_set = true;
+    const int SN = a.S * a.N, CK = 32 * a.K;
+    const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15)) +
+                            2 * (((size_t)CK * 4 + 15) & ~size_t(15));
+    const size_t smem = per_warp * WPB;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && attr < smem) {
+        cudaError_t e = cudaFuncSetAttribute(dirichlet_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
     }
-    dirichlet_kernel<<<a.frames, 128, smem, st>>>(a);
+    dirichlet_kernel<<<(a.frames + WPB - 1) / WPB, WPB * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 

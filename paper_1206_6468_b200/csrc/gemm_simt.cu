@@ -188,12 +188,12 @@ __global__ void __launch_bounds__(Cfg<NTC>::NT, Cfg<NTC>::MINB) recon_kernel(Rec
         }
         if (bad) atomicOr(p.flags, bad);
         __syncthreads();
-        if (tid < BM) {
-            const int r = m0 + tid;
+        for (int rl = tid; rl < BM; rl += Cfg<NTC>::NT) {   // NT may be < BM for narrow tiles
+            const int r = m0 + rl;
             if (r < p.M) {
                 double s = 0.0;
 #pragma unroll 4
-                for (int c = 0; c < NTC; ++c) s += red[tid][c];
+                for (int c = 0; c < NTC; ++c) s += red[rl][c];
                 p.data_part[(size_t)r * p.n_tiles + ntile] = s;
             }
         }

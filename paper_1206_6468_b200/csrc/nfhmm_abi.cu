@@ -38,6 +38,12 @@ struct nfhmm {
     int64_t launches = 0;
     double c_prior_T = 0.0;
     std::string err;
+    // per-kernel-class profiling (events bracketing each launch)
+    bool prof = false;
+    struct Rec { int cls; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    size_t pool_used = 0;
 };
 
 namespace {
@@ -76,10 +82,29 @@ int fail(nfhmm_t *h, int code, const char *fmt, ...) {
         if (e_ != cudaSuccess) return fail(h, NFHMM_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
     } while (0)
 
-#define LAUNCH(h, call)         \
-    do {                        \
-        CU(h, call);            \
-        (h)->launches++;        \
+cudaEvent_t prof_event(nfhmm_t *h) {
+    if (h->pool_used == h->pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        h->pool.push_back(e);
+    }
+    return h->pool[h->pool_used++];
+}
+
+#define LAUNCH(h, cls, call)                                                   \
+    do {                                                                       \
+        cudaEvent_t ea_ = nullptr, eb_ = nullptr;                              \
+        if ((h)->prof) {                                                       \
+            ea_ = prof_event(h);                                               \
+            eb_ = prof_event(h);                                               \
+            if (ea_) cudaEventRecord(ea_, (h)->st);                            \
+        }                                                                      \
+        CU(h, call);                                                           \
+        (h)->launches++;                                                       \
+        if (ea_ && eb_) {                                                      \
+            cudaEventRecord(eb_, (h)->st);                                     \
+            (h)->recs.push_back({cls, ea_, eb_});                              \
+        }                                                                      \
     } while (0)
 
 bool is_device_ptr(const void *p) {
@@ -160,7 +185,7 @@ int recon_ratio(nfhmm_t *h) {
     a.data_part = h->data_part;
     a.n_tiles = h->nt_a;
     a.flags = h->flags;
-    LAUNCH(h, launch_recon(h->bn_a, a, h->st));
+    LAUNCH(h, NFHMM_K_RECON, launch_recon(h->bn_a, a, h->st));
     return NFHMM_OK;
 }
 
@@ -180,7 +205,7 @@ int sweep(nfhmm_t *h) {
     b.ldb = h->Kb;
     b.theta = h->theta;
     b.n_out = h->alpha;
-    LAUNCH(h, launch_backproj(h->bn_b, b, h->st));
+    LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj(h->bn_b, b, h->st));
     // (c)+(d) Eq. 6, digamma/exp, Eq. 8
     DirichletArgs d{};
     d.frames = (int)h->frames;
@@ -199,7 +224,7 @@ int sweep(nfhmm_t *h) {
     d.eoff = h->eoff;
     d.hdir = h->free_energy ? h->hdir : nullptr;
     d.flags = h->flags;
-    LAUNCH(h, launch_dirichlet(d, h->st));
+    LAUNCH(h, NFHMM_K_DIRICHLET, launch_dirichlet(d, h->st));
     // (e) forward-backward per source
     FBArgs f{};
     f.M = (int)h->M;
@@ -215,7 +240,7 @@ int sweep(nfhmm_t *h) {
     f.cinv = h->cinv;
     f.logZ = h->logZ;
     f.flags = h->flags;
-    LAUNCH(h, launch_fb(f, h->st));
+    LAUNCH(h, NFHMM_K_FB, launch_fb(f, h->st));
     // (a) z-step of the new alpha: R for the next sweep and the data term of L_i
     int r = recon_ratio(h);
     if (r) return r;
@@ -233,7 +258,7 @@ int sweep(nfhmm_t *h) {
         e.hdir = h->hdir;
         e.logZ = h->logZ;
         e.fe = h->fe;
-        LAUNCH(h, launch_elbo(e, h->st));
+        LAUNCH(h, NFHMM_K_ELBO, launch_elbo(e, h->st));
     }
     h->iters_done++;
     return NFHMM_OK;
@@ -378,7 +403,7 @@ int nfhmm_set_model(nfhmm_t *h, const float *dict, const float *trans, const flo
     CU(h, cudaMemsetAsync(h->beta, 0, (size_t)h->Fa * h->Kb * 4, h->st));
     CU(h, cudaMemcpy2DAsync(h->betaT, (size_t)h->Fa * 4, hd.data(), (size_t)h->F * 4, (size_t)h->F * 4, h->Kt,
                             cudaMemcpyHostToDevice, h->st));
-    LAUNCH(h, launch_transpose(h->betaT, h->Kt, (int)h->F, h->Fa, h->beta, h->Kb, h->st));
+    LAUNCH(h, NFHMM_K_OTHER, launch_transpose(h->betaT, h->Kt, (int)h->F, h->Fa, h->beta, h->Kb, h->st));
     CU(h, cudaMemcpyAsync(h->trans, ht.data(), nt * 4, cudaMemcpyHostToDevice, h->st));
     CU(h, cudaMemcpyAsync(h->prior, hp.data(), np * 4, cudaMemcpyHostToDevice, h->st));
     CU(h, cudaStreamSynchronize(h->st));   // host vectors go out of scope
@@ -400,7 +425,7 @@ int nfhmm_reset(nfhmm_t *h) {
         return res + log(x) - 0.5 / x - f * (1.0 / 12 - f * (1.0 / 120 - f / 252));
     };
     const float th0 = (float)exp(dg(a0) - dg(a0 * h->Kt));
-    LAUNCH(h, launch_init_state((int)h->frames, h->Kb, h->Kt, (float)a0, th0, h->alpha, h->theta, h->dhat,
+    LAUNCH(h, NFHMM_K_OTHER, launch_init_state((int)h->frames, h->Kb, h->Kt, (float)a0, th0, h->alpha, h->theta, h->dhat,
                                 (long long)h->M * h->S * h->T * h->N, (float)(1.0 / h->N), h->st));
     CU(h, cudaMemsetAsync(h->fe, 0, (size_t)h->M * h->max_iters * 8, h->st));
     h->R_valid = false;
@@ -419,7 +444,7 @@ int nfhmm_set_observations(nfhmm_t *h, const float *V) {
     CU(h, cudaMemsetAsync(h->flags, 0, sizeof(unsigned), h->st));   // new data: clear sticky flags
     CU(h, cudaMemcpy2DAsync(h->V, (size_t)h->Fa * 4, V, (size_t)h->F * 4, (size_t)h->F * 4, (size_t)h->frames,
                             cudaMemcpyDefault, h->st));
-    LAUNCH(h, launch_obs_stats(h->V, (int)h->frames, (int)h->F, h->Fa, h->vt, h->flags, h->st));
+    LAUNCH(h, NFHMM_K_OTHER, launch_obs_stats(h->V, (int)h->frames, (int)h->F, h->Fa, h->vt, h->flags, h->st));
     h->have_obs = true;
     return nfhmm_reset(h);
 }
@@ -472,7 +497,7 @@ int nfhmm_posteriors(nfhmm_t *h, float *d_hat, float *alpha_hat, float *V_hat, d
         a.Vhat = dev ? V_hat : h->vsrc;
         a.n_tiles = h->nt_a;
         a.flags = h->flags;
-        LAUNCH(h, launch_recon(h->bn_a, a, h->st));
+        LAUNCH(h, NFHMM_K_OTHER, launch_recon(h->bn_a, a, h->st));
         if (!dev) CU(h, cudaMemcpyAsync(V_hat, h->vsrc, (size_t)h->frames * h->F * 4, cudaMemcpyDeviceToHost, h->st));
     }
     if (free_energy)
@@ -486,7 +511,7 @@ int nfhmm_separate(nfhmm_t *h, float *V_star, float *V_src) {
     if (r) return r;
     if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
     if (!V_star) return fail(h, NFHMM_EINVAL, "V_star is required");
-    LAUNCH(h, launch_sep_scale(h->alpha, (int)h->frames, h->Kt, h->Kb, h->vt, h->scale, h->st));
+    LAUNCH(h, NFHMM_K_SEPARATE, launch_sep_scale(h->alpha, (int)h->frames, h->Kt, h->Kb, h->vt, h->scale, h->st));
     const int NK = h->N * h->K;
     for (int s = 0; s < h->S; ++s) {
         ReconArgs a{};
@@ -505,19 +530,49 @@ int nfhmm_separate(nfhmm_t *h, float *V_star, float *V_src) {
         a.S = h->S;
         a.s = s;
         a.flags = h->flags;
-        LAUNCH(h, launch_recon(h->bn_a, a, h->st));
+        LAUNCH(h, NFHMM_K_SEPARATE, launch_recon(h->bn_a, a, h->st));
     }
     const size_t n = (size_t)h->M * h->S * h->T * h->F;
     if (V_src) CU(h, cudaMemcpyAsync(V_src, h->vsrc, n * 4, cudaMemcpyDefault, h->st));
     const bool dev = is_device_ptr(V_star);
-    LAUNCH(h, launch_wiener(h->V, h->Fa, h->vsrc, dev ? V_star : h->vsrc, (int)h->M, h->S, (int)h->T, (int)h->F, h->st));
+    LAUNCH(h, NFHMM_K_SEPARATE, launch_wiener(h->V, h->Fa, h->vsrc, dev ? V_star : h->vsrc, (int)h->M, h->S, (int)h->T, (int)h->F, h->st));
     if (!dev) CU(h, cudaMemcpyAsync(V_star, h->vsrc, n * 4, cudaMemcpyDeviceToHost, h->st));
     return check_flags(h);
+}
+
+int nfhmm_profile_enable(nfhmm_t *h, int on) {
+    int r = enter(h);
+    if (r) return r;
+    CU(h, cudaStreamSynchronize(h->st));
+    h->recs.clear();
+    h->pool_used = 0;
+    h->prof = on != 0;
+    return NFHMM_OK;
+}
+
+int nfhmm_profile_read(nfhmm_t *h, double *ms, int64_t *launches) {
+    int r = enter(h);
+    if (r) return r;
+    CU(h, cudaStreamSynchronize(h->st));
+    double acc[NFHMM_NUM_KERNEL_CLASSES] = {0};
+    int64_t cnt[NFHMM_NUM_KERNEL_CLASSES] = {0};
+    for (const auto &rec : h->recs) {
+        float t = 0.f;
+        CU(h, cudaEventElapsedTime(&t, rec.a, rec.b));
+        acc[rec.cls] += t;
+        cnt[rec.cls] += 1;
+    }
+    for (int i = 0; i < NFHMM_NUM_KERNEL_CLASSES; ++i) {
+        if (ms) ms[i] = acc[i];
+        if (launches) launches[i] = cnt[i];
+    }
+    return NFHMM_OK;
 }
 
 int nfhmm_destroy(nfhmm_t *h) {
     if (!h) return NFHMM_OK;
     cudaSetDevice(h->device);
+    for (cudaEvent_t e : h->pool) cudaEventDestroy(e);
     if (h->ws_owned && h->ws) cudaFree(h->ws);
     delete h;
     return NFHMM_OK;

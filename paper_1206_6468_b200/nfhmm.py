@@ -55,6 +55,8 @@ SIGNATURES = {
     "nfhmm_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "nfhmm_last_error": (ctypes.c_char_p, [_P]),
     "nfhmm_kernel_launches": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+    "nfhmm_profile_enable": (ctypes.c_int, [_P, ctypes.c_int]),
+    "nfhmm_profile_read": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
     "nfhmm_layout": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32),
                                     ctypes.POINTER(_I32)]),
 }
@@ -175,6 +177,22 @@ def nfhmm_layout(h):
     return dict(F_pad=fp.value, Kt_pad=kp.value, bn_recon=br.value, bn_backproj=bb.value)
 
 
+KERNEL_CLASSES = ("recon", "backproj", "dirichlet", "fb", "elbo", "separate", "other")
+
+
+def nfhmm_profile_enable(h, on=True):
+    _check(h, _lib.nfhmm_profile_enable(h, 1 if on else 0))
+
+
+def nfhmm_profile_read(h):
+    """{class: (device ms, launches)} accumulated since the last enable (synchronises)."""
+    n = len(KERNEL_CLASSES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int64 * n)()
+    _check(h, _lib.nfhmm_profile_read(h, ms, cnt))
+    return {k: (ms[i], cnt[i]) for i, k in enumerate(KERNEL_CLASSES)}
+
+
 # ---- convenience handle -----------------------------------------------------------------------
 class NFHMM:
     """One libnfhmm handle: n_mix mixtures of F x T counts, S sources x N states x K elements.
@@ -236,6 +254,12 @@ class NFHMM:
     def layout(self):
         return nfhmm_layout(self.h)
 
+    def profile_enable(self, on=True):
+        nfhmm_profile_enable(self.h, on)
+
+    def profile_read(self):
+        return nfhmm_profile_read(self.h)
+
     def posteriors(self, d_hat=True, alpha_hat=True, V_hat=True, free_energy=True):
         """Returns host numpy arrays: d_hat [M][S][T][N], alpha_hat [M][T][Kt], V_hat [M][T][F],
         free_energy [M][iters_done] (FP64), iters_done."""
@@ -255,6 +279,10 @@ class NFHMM:
         if fe is not None:
             out["free_energy"] = fe[:, :min(it, self.max_iters)]
         return out
+
+    def separate_into(self, V_star, V_src=None):
+        """Separation into caller buffers (torch CUDA tensors, pinned host tensors or numpy arrays)."""
+        nfhmm_separate(self.h, V_star, V_src)
 
     def separate(self, V_src=False):
         M, S, T, F = self.n_mix, self.S, self.T, self.F
