@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--iters", type=int, default=None, help="VB sweeps per step (default: the config's)")
     ap.add_argument("--mixtures", type=int, default=None, help="override total mixtures (default: config)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--math", choices=["tc", "simt"], default="tc",
+                    help="contraction engine: tcgen05 3xTF32 (default) or FP32 FFMA")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds for the oracle sample")
@@ -236,7 +238,8 @@ def run_ours(args):
     t_gen = time.perf_counter() - t_gen
 
     stream = torch.cuda.current_stream(dev)
-    h = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, device=dev, max_iters=max(iters, 1), stream=stream)
+    h = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, device=dev, max_iters=max(iters, 1), stream=stream,
+              math=args.math)
     h.set_model(model.beta, model.trans, model.prior)
     Vd = torch.from_numpy(V).to(f"cuda:{dev}")
     h.set_observations(Vd)

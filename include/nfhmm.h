@@ -55,13 +55,17 @@ extern "C" {
 
 typedef struct nfhmm nfhmm_t;     /* opaque, library-owned */
 
+#define NFHMM_MATH_TC 0          /* 3xTF32 split on tcgen05: a_lo b_hi + a_hi b_lo + a_hi b_hi, FP32 accumulate */
+#define NFHMM_MATH_SIMT 1        /* FP32 FFMA register tiles */
+
 typedef struct {
     int64_t n_mix;      /* independent mixtures (same model) on this handle; default 1           */
     double gamma;       /* Dirichlet concentration gamma >= 0 ("we took gamma = 1"); default 1 */
     int32_t device;     /* CUDA ordinal; default 0                                              */
     int32_t max_iters;  /* capacity of the per-mixture free-energy trace; default 1024            */
     int32_t free_energy;/* 1 = assemble L every sweep (default), 0 = skip the FP64 bound terms      */
-    int32_t reserved;
+    int32_t math;       /* contraction engine for (a)/(b): NFHMM_MATH_TC (default) = tcgen05 3xTF32
+                           tensor cores; NFHMM_MATH_SIMT = FP32 FFMA tiles                        */
     void *stream;       /* cudaStream_t to launch on (e.g. torch.cuda.current_stream().cuda_stream);
                            NULL = the legacy default stream                                      */
 } nfhmm_options;

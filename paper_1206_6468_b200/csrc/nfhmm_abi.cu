@@ -18,6 +18,7 @@ struct nfhmm {
     int64_t F = 0, T = 0, M = 0, frames = 0;
     int S = 0, N = 0, K = 0, Kt = 0;
     int Fa = 0, Kb = 0, bn_a = 0, bn_b = 0, nt_a = 0;
+    int math = NFHMM_MATH_TC, bn_tc_a = 0, bn_tc_b = 0, nt_tc_a = 0;
     double gamma = 1.0;
     int device = 0, max_iters = 1024, free_energy = 1;
     cudaStream_t st = nullptr;
@@ -143,7 +144,7 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take(chainT * 4);                        h->cinv = (float *)p;
     p = take(chainT * 8);                        h->eoff = (double *)p;
     p = take((size_t)h->M * h->S * 8);           h->logZ = (double *)p;
-    p = take(fr * h->nt_a * 8);                  h->data_part = (double *)p;
+    p = take(fr * (size_t)(h->nt_a > h->nt_tc_a ? h->nt_a : h->nt_tc_a) * 8); h->data_part = (double *)p;
     p = take(fr * 8);                            h->hdir = (double *)p;
     p = take((size_t)h->M * h->max_iters * 8);   h->fe = (double *)p;
     p = take(fr * 4);                            h->vt = (float *)p;
@@ -169,6 +170,24 @@ int check_flags(nfhmm_t *h) {
     return NFHMM_OK;
 }
 
+// (a) / (f) reconstruction GEMM on the selected engine: sets the operand layout the engine expects.
+int run_recon(nfhmm_t *h, int cls, ReconArgs a) {
+    if (h->math == NFHMM_MATH_TC) {
+        a.B = h->beta;      // [F_pad][Kt_pad], K-major rows
+        a.ldb = h->Kb;
+        a.n_tiles = h->nt_tc_a;
+        LAUNCH(h, cls, launch_recon_tc(h->bn_tc_a, a, h->st));
+    } else {
+        a.B = h->betaT;     // [Kt_pad][F_pad]
+        a.ldb = h->Fa;
+        a.n_tiles = h->nt_a;
+        LAUNCH(h, cls, launch_recon(h->bn_a, a, h->st));
+    }
+    return NFHMM_OK;
+}
+
+int data_tiles(const nfhmm_t *h) { return h->math == NFHMM_MATH_TC ? h->nt_tc_a : h->nt_a; }
+
 int recon_ratio(nfhmm_t *h) {
     ReconArgs a{};
     a.M = (int)h->frames;
@@ -183,10 +202,8 @@ int recon_ratio(nfhmm_t *h) {
     a.ldv = h->Fa;
     a.R = h->R;
     a.data_part = h->data_part;
-    a.n_tiles = h->nt_a;
     a.flags = h->flags;
-    LAUNCH(h, NFHMM_K_RECON, launch_recon(h->bn_a, a, h->st));
-    return NFHMM_OK;
+    return run_recon(h, NFHMM_K_RECON, a);
 }
 
 int sweep(nfhmm_t *h) {
@@ -205,7 +222,12 @@ int sweep(nfhmm_t *h) {
     b.ldb = h->Kb;
     b.theta = h->theta;
     b.n_out = h->alpha;
-    LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj(h->bn_b, b, h->st));
+    if (h->math == NFHMM_MATH_TC) {
+        b.B = h->betaT;     // [Kt_pad][F_pad], K-major rows
+        LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj_tc(h->bn_tc_b, h->Kt, b, h->st));
+    } else {
+        LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj(h->bn_b, b, h->st));
+    }
     // (c)+(d) Eq. 6, digamma/exp, Eq. 8
     DirichletArgs d{};
     d.frames = (int)h->frames;
@@ -249,7 +271,7 @@ int sweep(nfhmm_t *h) {
         ElboArgs e{};
         e.M = (int)h->M;
         e.T = (int)h->T;
-        e.n_tiles = h->nt_a;
+        e.n_tiles = data_tiles(h);
         e.S = h->S;
         e.iter = h->iters_done;
         e.max_iters = h->max_iters;
@@ -283,6 +305,7 @@ void nfhmm_default_options(nfhmm_options *o) {
     o->device = 0;
     o->max_iters = 1024;
     o->free_energy = 1;
+    o->math = NFHMM_MATH_TC;
     o->stream = nullptr;
 }
 
@@ -293,7 +316,7 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
     nfhmm_default_options(&o);
     if (opt) o = *opt;
     if (F < 1 || T < 1 || S < 1 || N < 1 || K < 1 || o.n_mix < 1 || !(o.gamma >= 0.0) || !isfinite(o.gamma) ||
-        o.max_iters < 1)
+        o.max_iters < 1 || (o.math != NFHMM_MATH_TC && o.math != NFHMM_MATH_SIMT))
         return NFHMM_EINVAL;
     if (N > 128) return NFHMM_EINVAL;  // forward-backward keeps <= 4 states per lane
     const int64_t Kt = (int64_t)S * N * K;
@@ -319,6 +342,10 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
     h->Fa = (int)((F + h->bn_a - 1) / h->bn_a * h->bn_a);
     h->Kb = (int)((Kt + h->bn_b - 1) / h->bn_b * h->bn_b);
     h->nt_a = h->Fa / h->bn_a;
+    h->math = o.math == NFHMM_MATH_SIMT ? NFHMM_MATH_SIMT : NFHMM_MATH_TC;
+    h->bn_tc_a = tc_pick_bn(F);
+    h->bn_tc_b = tc_pick_bn(Kt);
+    h->nt_tc_a = (int)((F + h->bn_tc_a - 1) / h->bn_tc_a);
     // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)
     h->c_prior_T = (double)T * (lgamma((double)Kt + o.gamma * S * K) - (double)S * K * lgamma(1.0 + o.gamma));
     // no CUDA call here: dims/layout/workspace queries work without a device; the first call that
@@ -495,9 +522,9 @@ int nfhmm_posteriors(nfhmm_t *h, float *d_hat, float *alpha_hat, float *V_hat, d
         a.ldb = h->Fa;
         a.F = (int)h->F;
         a.Vhat = dev ? V_hat : h->vsrc;
-        a.n_tiles = h->nt_a;
         a.flags = h->flags;
-        LAUNCH(h, NFHMM_K_OTHER, launch_recon(h->bn_a, a, h->st));
+        r = run_recon(h, NFHMM_K_OTHER, a);
+        if (r) return r;
         if (!dev) CU(h, cudaMemcpyAsync(V_hat, h->vsrc, (size_t)h->frames * h->F * 4, cudaMemcpyDeviceToHost, h->st));
     }
     if (free_energy)
@@ -530,7 +557,8 @@ int nfhmm_separate(nfhmm_t *h, float *V_star, float *V_src) {
         a.S = h->S;
         a.s = s;
         a.flags = h->flags;
-        LAUNCH(h, NFHMM_K_SEPARATE, launch_recon(h->bn_a, a, h->st));
+        r = run_recon(h, NFHMM_K_SEPARATE, a);
+        if (r) return r;
     }
     const size_t n = (size_t)h->M * h->S * h->T * h->F;
     if (V_src) CU(h, cudaMemcpyAsync(V_src, h->vsrc, n * 4, cudaMemcpyDefault, h->st));

@@ -54,6 +54,12 @@ struct BackprojArgs {
 cudaError_t launch_recon(int bn, const ReconArgs &a, cudaStream_t st);
 cudaError_t launch_backproj(int bn, const BackprojArgs &a, cudaStream_t st);
 
+// tcgen05 3xTF32 variants (gemm_tc.cu).  recon: a.B = beta [F_pad][Kt_pad] K-major (ldb = Kt_pad);
+// backproj: a.B = betaT [Kt_pad][F_pad] K-major, a.Kpad = F_pad, a.ldb = row length of theta / n.
+int tc_pick_bn(int64_t n);
+cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st);
+cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st);
+
 struct DirichletArgs {
     int frames, T, S, N, K, Kt, ld;   // ld = padded row length of n/alpha/theta
     float gamma;

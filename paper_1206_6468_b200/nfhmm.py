@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libnfhmm.so")
 
 NFHMM_OK, NFHMM_EINVAL, NFHMM_ESTATE, NFHMM_ECUDA = 0, -1, -2, -3
 NFHMM_ENOMEM, NFHMM_EZEROSUPPORT, NFHMM_ENUMERIC = -4, -5, -6
+MATH_TC, MATH_SIMT = 0, 1          # NFHMM_MATH_TC (tcgen05 3xTF32), NFHMM_MATH_SIMT (FP32 FFMA)
 
 
 class NFHMMError(RuntimeError):
@@ -32,7 +33,7 @@ class NFHMMError(RuntimeError):
 
 class Options(ctypes.Structure):
     _fields_ = [("n_mix", ctypes.c_int64), ("gamma", ctypes.c_double), ("device", ctypes.c_int32),
-                ("max_iters", ctypes.c_int32), ("free_energy", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("max_iters", ctypes.c_int32), ("free_energy", ctypes.c_int32), ("math", ctypes.c_int32),
                 ("stream", ctypes.c_void_p)]
 
 
@@ -201,7 +202,7 @@ class NFHMM:
     torch uint8 CUDA tensor owned by this object."""
 
     def __init__(self, F, T, S, N, K, n_mix=1, gamma=1.0, device=0, max_iters=1024, free_energy=True,
-                 stream=None):
+                 stream=None, math="tc"):
         import torch
         self.F, self.T, self.S, self.N, self.K, self.n_mix = F, T, S, N, K, n_mix
         self.Kt = S * N * K
@@ -210,6 +211,8 @@ class NFHMM:
         opt = nfhmm_default_options()
         opt.n_mix, opt.gamma, opt.device = n_mix, gamma, device
         opt.max_iters, opt.free_energy = max_iters, 1 if free_energy else 0
+        opt.math = {"tc": MATH_TC, "simt": MATH_SIMT}[math]
+        self.math = math
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream

@@ -21,13 +21,14 @@ def make_inputs(c, **override):
     return cfg, model, V
 
 
-def run_gpu(cfg, model, V, iters, gamma=1.0, separate=True, max_iters=1024, device_io=False, split=None):
+def run_gpu(cfg, model, V, iters, gamma=1.0, separate=True, max_iters=1024, device_io=False, split=None,
+            math="tc"):
     """Run the CUDA path: set_model, set_observations, vb_iterate(iters) (optionally split into several
     calls), posteriors (+ separate).  Returns dict of host numpy arrays."""
     import torch
     from paper_1206_6468_b200.nfhmm import NFHMM
     M = V.shape[0]
-    h = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, gamma=gamma, max_iters=max_iters)
+    h = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, gamma=gamma, max_iters=max_iters, math=math)
     if device_io:
         h.set_model(torch.from_numpy(model.beta).cuda(), torch.from_numpy(model.trans).cuda(),
                     torch.from_numpy(model.prior).cuda())

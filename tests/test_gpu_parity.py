@@ -19,9 +19,12 @@ TOL_VSTAR = 1e-3
 TOL_L = 1e-5
 
 
-def check_parity(cfg, model, V, iters, gamma=1.0, mixtures=None, tol1=TOL1):
-    g1 = run_gpu(cfg, model, V, 1, gamma=gamma, separate=False)
-    gn = run_gpu(cfg, model, V, iters, gamma=gamma)
+MATHS = ["tc", "simt"]
+
+
+def check_parity(cfg, model, V, iters, gamma=1.0, mixtures=None, tol1=TOL1, math="tc"):
+    g1 = run_gpu(cfg, model, V, 1, gamma=gamma, separate=False, math=math)
+    gn = run_gpu(cfg, model, V, iters, gamma=gamma, math=math)
     for m in (mixtures if mixtures is not None else range(V.shape[0])):
         o1 = run_oracle(cfg, model, V[m], 1, gamma=gamma, separate=False)
         assert rel_l2(g1["d_hat"][m], o1["d_hat"]) <= tol1
@@ -38,44 +41,51 @@ def check_parity(cfg, model, V, iters, gamma=1.0, mixtures=None, tol1=TOL1):
     return g1, gn
 
 
-def test_cfg0_tiny_full():
+@pytest.mark.parametrize("math", MATHS)
+def test_cfg0_tiny_full(math):
     cfg, model, V = make_inputs(0)
-    g1, gn = check_parity(cfg, model, V, cfg.iters)
+    g1, gn = check_parity(cfg, model, V, cfg.iters, math=math)
     assert gn["iters_done"] == cfg.iters
 
 
-def test_cfg1_reduced_T200():
+@pytest.mark.parametrize("math", MATHS)
+def test_cfg1_reduced_T200(math):
     cfg, model, V = make_inputs(1, T=200)
-    check_parity(cfg, model, V, 30)
+    check_parity(cfg, model, V, 30, math=math)
 
 
-def test_cfg2_three_sources_reduced():
+@pytest.mark.parametrize("math", MATHS)
+def test_cfg2_three_sources_reduced(math):
     cfg, model, V = make_inputs(2, T=150)
-    check_parity(cfg, model, V, 20)
+    check_parity(cfg, model, V, 20, math=math)
 
 
-def test_cfg3_batched_reduced_multi_mixture():
+@pytest.mark.parametrize("math", MATHS)
+def test_cfg3_batched_reduced_multi_mixture(math):
     cfg, model, V = make_inputs(3, T=300, M=3)
-    check_parity(cfg, model, V, 15)
+    check_parity(cfg, model, V, 15, math=math)
 
 
-def test_cfg4_large_reduced():
+@pytest.mark.parametrize("math", MATHS)
+def test_cfg4_large_reduced(math):
     cfg, model, V = make_inputs(4, T=40, M=2)
-    check_parity(cfg, model, V, 4, mixtures=[1])
+    check_parity(cfg, model, V, 4, mixtures=[1], math=math)
 
 
 @pytest.mark.parametrize("gamma", [0.0, 2.5])
-def test_gamma_values(gamma):
+@pytest.mark.parametrize("math", MATHS)
+def test_gamma_values(gamma, math):
     cfg, model, V = make_inputs(0, T=70)
-    check_parity(cfg, model, V, 10, gamma=gamma)
+    check_parity(cfg, model, V, 10, gamma=gamma, math=math)
 
 
 @pytest.mark.parametrize("shape", [dict(S=1, N=3, K=2, F=17, T=1), dict(S=1, N=1, K=1, F=5, T=9),
                                    dict(S=2, N=1, K=5, F=64, T=129), dict(S=2, N=33, K=1, F=40, T=31),
                                    dict(S=3, N=2, K=3, F=9, T=257)])
-def test_edge_shapes(shape):
+@pytest.mark.parametrize("math", MATHS)
+def test_edge_shapes(shape, math):
     cfg, model, V = make_inputs(0, counts=500, **shape)
-    check_parity(cfg, model, V, 6)
+    check_parity(cfg, model, V, 6, math=math)
 
 
 def test_empty_frames_and_sharding_invariance():
