@@ -32,6 +32,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1206_6468_b200 import dist as pdist  # noqa: E402
 from paper_1206_6468_b200 import synth  # noqa: E402
 
 METRIC = "frame-iterations/sec (S=2,N=40,K=10,F=513) at 1/2/4/8 B200; % FP32/HBM roofline"
@@ -56,17 +57,8 @@ def parse():
     return ap.parse_args()
 
 
-def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
-
-
-def shard(M, world, rank):
-    lo = rank * M // world
-    hi = (rank + 1) * M // world
-    return list(range(lo, hi))
+dist_env = pdist.env
+shard = pdist.shard
 
 
 # ------------------------------------------------------------------------------------------------
@@ -272,9 +264,7 @@ def run_ours(args):
     clk = clocks.stop()
     elapsed = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([elapsed], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+        elapsed = pdist.max_over_ranks(elapsed, device=f"cuda:{dev}")
         dist.barrier()
     ms_per_step = elapsed / args.steps
     frame_iters = cfg.M * cfg.T * iters                     # whole job, all ranks
@@ -303,9 +293,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         el = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([el], dtype=torch.float64, device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+            el = pdist.max_over_ranks(el, device=f"cuda:{dev}")
         e2e = {"value": frame_iters / (el / args.steps / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(Vh.numel() * 4) * world, "d2h_bytes_per_step": int(out_h.numel() * 4) * world,
                "ms_per_step": el / args.steps}

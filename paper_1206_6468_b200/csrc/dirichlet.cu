@@ -3,8 +3,9 @@
 //   (c) Eq. 6:  alpha_k = n_k + gamma * d^{(s(k))}_{t, n(k)} + 1,  alpha_0 = sum_k alpha_k (FP64),
 //       Eq. 7 weights: theta_k = exp(psi(alpha_k) - psi(alpha_0));
 //   (d) Eq. 8:  phi_n^{(s)} = sum_{j<K} psi(alpha_{(sN+n)K+j}) - K psi(alpha_0), handed to the
-//       forward-backward as gamma * phi (DESIGN R1), centred per (s, t): ec = gamma (phi - max_n phi) in
-//       FP32 and eoff = gamma max_n phi in FP64 (the FB is shift-invariant per frame);
+//       forward-backward as gamma * phi (DESIGN R1), centred per (s, t): the emission
+//       e = exp(gamma (phi - max_n phi)) in (0, 1] (FP32) and eoff = gamma max_n phi in FP64 (the FB is
+//       shift-invariant per frame);
 //   bound term (DESIGN R8): H_t = sum_k [lnG(alpha_k) - (alpha_k - 1) psi(alpha_k)]
 //                                 - lnG(alpha_0) + (alpha_0 - Kt) psi(alpha_0)      (FP64 accumulation).
 // HBM-bound: per frame it reads n (Kt floats) + d (S N) and writes alpha, theta (2 Kt) + phi (S N).
@@ -15,6 +16,7 @@
 #include <math.h>
 
 #include "nfhmm_internal.cuh"
+#include "psi_lngamma_poly.cuh"
 
 namespace nfk {
 
@@ -22,35 +24,40 @@ namespace {
 
 constexpr int WPB = 8;   // frames (warps) per CTA
 
-// psi(x) and lnGamma(x) for x >= 1 (alpha >= 1 by Eq. 6), IEEE FP32 without fast-math (DESIGN R14).
-// x < 6 is shifted by 5 with psi(x) = psi(x+5) - sum_{i<5} 1/(x+i), the five reciprocals folded into
-// one quotient, and lnGamma(x) = lnGamma(x+5) - ln prod_{i<5}(x+i); then the asymptotic series
-// psi(y) = ln y - 1/(2y) - 1/(12y^2) + 1/(120y^4) - 1/(252y^6) + 1/(240y^8)   (trunc. < 2e-9 at y = 6)
-// lnG(y) = (y - 1/2) ln y - y + ln(2 pi)/2 + 1/(12y) - 1/(360y^3) + 1/(1260y^5)  (trunc. < 2e-8 at y = 6)
+// psi(x) and lnGamma(x) for x >= 1 (alpha >= 1 by Eq. 6), FP32 without fast-math (DESIGN R14).
+// x in [1, 6): degree-10 polynomials per unit interval (psi_lngamma_poly.cuh, float32 error <= 1.3e-7 /
+// 3.3e-7 absolute), read from a shared-memory copy of the tables (lanes in different intervals hit
+// different banks); x >= 6: the asymptotic series
+// psi(x) = ln x - 1/(2x) - 1/(12x^2) + 1/(120x^4) - 1/(252x^6) + 1/(240x^8)          (trunc. < 2e-9)
+// lnG(x) = (x - 1/2) ln x - x + ln(2 pi)/2 + 1/(12x) - 1/(360x^3) + 1/(1260x^5)       (trunc. < 2e-8)
 struct PsiLg {
-    float psi, lng;
+    float psi, lng, ly, r;   // ly = ln x, r = 1/x on the asymptotic branch (reused by gterm)
 };
-__device__ __forceinline__ PsiLg psi_lngamma(float x, bool want_lng) {
-    float rs = 0.f, lprod = 0.f;
+__device__ __forceinline__ PsiLg psi_lngamma(float x, bool want_lng, const float *tab) {
+    PsiLg o;
     if (x < 6.f) {
-        const float a0 = x, a1 = x + 1.f, a2 = x + 2.f, a3 = x + 3.f, a4 = x + 4.f;
-        const float p01 = a0 * a1, p23 = a2 * a3;
-        const float num4 = (a0 + a1) * p23 + (a2 + a3) * p01;
-        const float den4 = p01 * p23;
-        const float den = den4 * a4;
-        rs = (num4 * a4 + den4) / den;      // sum_{i<5} 1/(x+i)
-        if (want_lng) lprod = logf(den);
-        x += 5.f;
+        const int n = (int)x;                               // 1..5
+        const float v = 2.f * (x - (float)n) - 1.f;
+        const float *cp = tab + (n - 1) * 11, *cl = tab + 55 + (n - 1) * 11;
+        float ps = cp[10], lg = cl[10];
+#pragma unroll
+        for (int i = 9; i >= 0; --i) {
+            ps = fmaf(ps, v, cp[i]);
+            lg = fmaf(lg, v, cl[i]);
+        }
+        o.psi = ps;
+        o.lng = lg;
+        o.ly = o.r = 0.f;
+        return o;
     }
     const float r = 1.f / x;
     const float f = r * r;
     const float ly = logf(x);
-    const float ser = f * (-1.f / 12.f + f * (1.f / 120.f + f * (-1.f / 252.f + f * (1.f / 240.f))));
-    PsiLg o;
-    o.psi = ly - 0.5f * r + ser - rs;
+    o.psi = ly - 0.5f * r + f * (-1.f / 12.f + f * (1.f / 120.f + f * (-1.f / 252.f + f * (1.f / 240.f))));
     o.lng = 0.f;
-    if (want_lng)
-        o.lng = (x - 0.5f) * ly - x + 0.91893853320467274f + r * (1.f / 12.f + f * (-1.f / 360.f + f * (1.f / 1260.f))) - lprod;
+    o.ly = ly;
+    o.r = r;
+    if (want_lng) o.lng = (x - 0.5f) * ly - x + 0.91893853320467274f + r * (1.f / 12.f + f * (-1.f / 360.f + f * (1.f / 1260.f)));
     return o;
 }
 
@@ -71,9 +78,11 @@ __device__ double digamma_d(double x) {
 // g(x) = ln(x)/2 - x + ln(2 pi)/2 + 1/2 - 1/(3x) - 1/(12x^2) - 1/(90x^3) + 1/(120x^4) + 1/(1260x^5) + ...
 __device__ __forceinline__ double gterm(float a, const PsiLg &pl) {
     if (a < 64.f) return (double)(pl.lng - (a - 1.f) * pl.psi);
-    const double x = a, ix = 1.0 / x, ix2 = ix * ix;
-    const double series = -ix / 3.0 - ix2 / 12.0 - ix2 * ix / 90.0 + ix2 * ix2 / 120.0 + ix2 * ix2 * ix / 1260.0;
-    return 0.5 * log(x) - x + 0.91893853320467274178 + 0.5 + series;
+    // large a: the series terms in FP32 (|.| < 6e-3), the O(a) part assembled in FP64 from the FP32 ln a
+    const float ix = pl.r, ix2 = ix * ix;
+    const float series = ix * (-1.f / 3.f + ix * (-1.f / 12.f + ix * (-1.f / 90.f + ix * (1.f / 120.f + ix * (1.f / 1260.f)))));
+    (void)ix2;
+    return 0.5 * (double)pl.ly - (double)a + (0.91893853320467274178 + 0.5) + (double)series;
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -100,6 +109,9 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     float *ca = reinterpret_cast<float *>(base + sps_b + dsm_b);
     float *ct = ca + ((CK + 3) & ~3);
 
+    __shared__ float tab[110];   // psi / lnGamma polynomial tables (see psi_lngamma)
+    for (int i = threadIdx.x; i < 110; i += blockDim.x) tab[i] = i < 55 ? (&kPsiPoly[0][0])[i] : (&kLgPoly[0][0])[i - 55];
+    __syncthreads();
     const int f = blockIdx.x * WPB + warp;
     if (f >= p.frames) return;
     const int m = f / p.T, t = f - m * p.T;
@@ -146,7 +158,7 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
             double sp = 0.0;
             for (int j = 0; j < K; ++j) {
                 const float a = pa[j] + dv;
-                const PsiLg pl = psi_lngamma(a, want_h);
+                const PsiLg pl = psi_lngamma(a, want_h, tab);
                 const float th = expf(pl.psi - psi0f);
                 pa[j] = a;
                 pt[j] = th;
@@ -177,7 +189,7 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
         for (int n = lane; n < p.N; n += 32) mx = fmax(mx, sps[s * p.N + n]);
         mx = warp_max_d(mx);
         float *dst = p.ec + ((size_t)(m * p.S + s) * p.T + t) * p.N;
-        for (int n = lane; n < p.N; n += 32) dst[n] = (float)((double)gamma * (sps[s * p.N + n] - mx));
+        for (int n = lane; n < p.N; n += 32) dst[n] = expf((float)((double)gamma * (sps[s * p.N + n] - mx)));
         if (lane == 0) {
             const double off = (double)gamma * (mx - (double)K * psi0);
             p.eoff[(size_t)(m * p.S + s) * p.T + t] = off;

@@ -31,6 +31,7 @@ struct nfhmm {
     float *V = nullptr, *R = nullptr, *theta = nullptr, *alpha = nullptr;
     float *dhat = nullptr, *ec = nullptr, *fwd = nullptr, *cinv = nullptr;
     float *vt = nullptr, *scale = nullptr, *vsrc = nullptr;
+    float *bs_a = nullptr, *bs_b = nullptr;   // tensor-core path: pre-split beta for (a) and betaT for (b)
     double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
     unsigned *flags = nullptr;
 
@@ -150,6 +151,8 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take(fr * 4);                            h->vt = (float *)p;
     p = take(fr * 4);                            h->scale = (float *)p;
     p = take((size_t)h->M * h->S * h->T * h->F * 4); h->vsrc = (float *)p;
+    p = take(tc_presplit_floats(h->F, h->Kt, h->bn_tc_a) * 4); h->bs_a = (float *)p;
+    p = take(tc_presplit_floats(h->Kt, h->Fa, h->bn_tc_b) * 4); h->bs_b = (float *)p;
     p = take(256);                               h->flags = (unsigned *)p;
     return o;
 }
@@ -174,6 +177,8 @@ int check_flags(nfhmm_t *h) {
 int run_recon(nfhmm_t *h, int cls, ReconArgs a) {
     if (h->math == NFHMM_MATH_TC) {
         a.B = h->beta;      // [F_pad][Kt_pad], K-major rows
+        a.Bsplit = h->bs_a;
+        a.nkb_total = (h->Kt + 15) / 16;
         a.ldb = h->Kb;
         a.n_tiles = h->nt_tc_a;
         LAUNCH(h, cls, launch_recon_tc(h->bn_tc_a, a, h->st));
@@ -224,6 +229,8 @@ int sweep(nfhmm_t *h) {
     b.n_out = h->alpha;
     if (h->math == NFHMM_MATH_TC) {
         b.B = h->betaT;     // [Kt_pad][F_pad], K-major rows
+        b.Bsplit = h->bs_b;
+        b.nkb_total = (h->Fa + 15) / 16;
         LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj_tc(h->bn_tc_b, h->Kt, b, h->st));
     } else {
         LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj(h->bn_b, b, h->st));
@@ -431,6 +438,15 @@ int nfhmm_set_model(nfhmm_t *h, const float *dict, const float *trans, const flo
     CU(h, cudaMemcpy2DAsync(h->betaT, (size_t)h->Fa * 4, hd.data(), (size_t)h->F * 4, (size_t)h->F * 4, h->Kt,
                             cudaMemcpyHostToDevice, h->st));
     LAUNCH(h, NFHMM_K_OTHER, launch_transpose(h->betaT, h->Kt, (int)h->F, h->Fa, h->beta, h->Kb, h->st));
+    {   // tensor-core operand images of the static dictionary (split once, bulk-copied every stage)
+        std::vector<float> bsa(tc_presplit_floats(h->F, h->Kt, h->bn_tc_a));
+        std::vector<float> bsb(tc_presplit_floats(h->Kt, h->Fa, h->bn_tc_b));
+        tc_presplit_host(hd.data(), h->F, /*transposed=*/true, h->F, h->Kt, h->bn_tc_a, bsa.data());    // B[n=l][k]
+        tc_presplit_host(hd.data(), h->F, /*transposed=*/false, h->Kt, h->F, h->bn_tc_b, bsb.data());   // B[n=k][l]
+        CU(h, cudaMemcpyAsync(h->bs_a, bsa.data(), bsa.size() * 4, cudaMemcpyHostToDevice, h->st));
+        CU(h, cudaMemcpyAsync(h->bs_b, bsb.data(), bsb.size() * 4, cudaMemcpyHostToDevice, h->st));
+        CU(h, cudaStreamSynchronize(h->st));
+    }
     CU(h, cudaMemcpyAsync(h->trans, ht.data(), nt * 4, cudaMemcpyHostToDevice, h->st));
     CU(h, cudaMemcpyAsync(h->prior, hp.data(), np * 4, cudaMemcpyHostToDevice, h->st));
     CU(h, cudaStreamSynchronize(h->st));   // host vectors go out of scope

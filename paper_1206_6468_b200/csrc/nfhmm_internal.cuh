@@ -37,6 +37,8 @@ struct ReconArgs {
     float *out_src;           // SEPARATE: V_src base for this source
     int T, S, s;              // SEPARATE: address ((m*S + s)*T + t)*F + l
     unsigned *flags;
+    const float *Bsplit;      // tensor-core path: pre-split, pre-tiled beta (tc_presplit_host)
+    int nkb_total;
 };
 
 struct BackprojArgs {
@@ -48,6 +50,8 @@ struct BackprojArgs {
     int ldb;
     const float *theta;       // [M][ldb]
     float *n_out;             // [M][ldb]  n = theta .* (R beta)   (data term of Eq. 6)
+    const float *Bsplit;      // tensor-core path: pre-split, pre-tiled betaT
+    int nkb_total;
 };
 
 // Launchers (return cudaError_t of the launch).
@@ -57,6 +61,11 @@ cudaError_t launch_backproj(int bn, const BackprojArgs &a, cudaStream_t st);
 // tcgen05 3xTF32 variants (gemm_tc.cu).  recon: a.B = beta [F_pad][Kt_pad] K-major (ldb = Kt_pad);
 // backproj: a.B = betaT [Kt_pad][F_pad] K-major, a.Kpad = F_pad, a.ldb = row length of theta / n.
 int tc_pick_bn(int64_t n);
+// The static operand B[n][k] (n < n_rows, k < k_len; src[n*ld + k], or src[k*ld + n] if transposed) split
+// into tf32 hi/lo and re-tiled into the shared-memory image of each pipeline stage (host side, once).
+size_t tc_presplit_floats(int64_t n_rows, int64_t k_len, int bn);
+void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
+                      float *dst);
 cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st);
 cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st);
 
@@ -67,7 +76,7 @@ struct DirichletArgs {
     float *alpha;             // [frames][ld]  out: alpha (may alias n_in)
     float *theta;             // [frames][ld]  out: exp(psi(alpha) - psi(alpha_0))
     const float *d_hat;       // [M][S][T][N]  previous q(D) marginals
-    float *ec;                // [M][S][T][N]  out: centred log-emission gamma*(phi - max_n phi)
+    float *ec;                // [M][S][T][N]  out: emission exp(gamma*(phi - max_n phi)) in (0, 1]
     double *eoff;             // [M][S][T]     out: gamma * max_n phi (FP64)
     double *hdir;             // [frames]      out: Dirichlet entropy terms of the bound (or NULL)
     unsigned *flags;
@@ -76,7 +85,7 @@ cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st);
 
 struct FBArgs {
     int M, S, T, N;
-    const float *ec;          // [M][S][T][N]
+    const float *ec;          // [M][S][T][N]  emissions exp(gamma*(phi - max_n phi))
     const double *eoff;       // [M][S][T]
     const float *trans;       // [S][N][N]
     const float *prior;       // [S][N]

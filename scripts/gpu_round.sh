@@ -1,3 +1,5 @@
-set -x
-CMD="python bench.py --mixtures 16 --iters 2 --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
-$CMD > gpurun_out/plain.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tc_gemm_kernel|dirichlet_kernel" -s 6 -c 3 -o gpurun_out/prof_tc1 $CMD > gpurun_out/ncu.log 2>&1; echo ncu_exit=$?; tail -3 gpurun_out/ncu.log
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$?; tail -3 gpurun_out/gpu_tests.log
+timeout 300 python bench.py --mixtures 64 --iters 4 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline 2>&1 | python -c "
+import json,sys
+d=json.loads(sys.stdin.read().strip().splitlines()[-1]); k=d['kernels']
+print({n:round(v['ms_per_step']/v['launches_per_step'],3) for n,v in k.items()})"
