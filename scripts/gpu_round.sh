@@ -1,5 +1,6 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; echo tests_exit=$?; tail -3 gpurun_out/gpu_tests.log
-timeout 300 python bench.py --mixtures 64 --iters 4 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline 2>&1 | python -c "
-import json,sys
-d=json.loads(sys.stdin.read().strip().splitlines()[-1]); k=d['kernels']
-print({n:round(v['ms_per_step']/v['launches_per_step'],3) for n,v in k.items()})"
+set -x
+nproc
+CMD="python bench.py"
+timeout 900 $CMD > gpurun_out/bench_full.log 2>&1; echo bench_exit=$?; tail -c 3000 gpurun_out/bench_full.log
+timeout 900 $CMD > gpurun_out/plain.log 2>&1 && timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file gpurun_out/launches_r1.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo ncu1_exit=$?
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"tc_gemm_kernel" -s 8 -c 2 -o gpurun_out/prof_full_r1 $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2_exit=$?; tail -3 gpurun_out/ncu_full.log
