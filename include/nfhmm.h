@@ -160,6 +160,14 @@ int nfhmm_profile_enable(nfhmm_t *h, int on);
  * the last enable.  Both arrays have NFHMM_NUM_KERNEL_CLASSES entries; either may be NULL. */
 int nfhmm_profile_read(nfhmm_t *h, double *ms, int64_t *launches);
 
+/* Instrumentation: launch ONE kernel class (NFHMM_K_RECON, _BACKPROJ, _DIRICHLET or _FB) `reps` times
+ * back to back on the handle's current state and return the mean device time per launch (CUDA events
+ * on the handle's stream).  The repeated step leaves the iteration state inconsistent, so the call
+ * ends with nfhmm_reset (iters_done = 0, free-energy trace restarted).  Synchronises.
+ * Errors: NFHMM_ESTATE before model + observations; NFHMM_EINVAL for another class, reps < 1 or a NULL
+ * ms_per_launch. */
+int nfhmm_bench_kernel(nfhmm_t *h, int cls, int32_t reps, double *ms_per_launch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,6 +1,6 @@
 // gemm_tc.cu -- the (a) reconstruction and (b) back-projection contractions on the 5th-generation tensor
 // cores (tcgen05, sm_100a) with 3xTF32 splitting, so the products keep FP32 accuracy (BASELINE north_star:
-// "SIMT FFMA tiles or 3xTF32 split tcgen05 with ... dictionary tiles in shared memory").
+// "SIMT FFMA tiles or 3xTF32 split tcgen05 with TMA-staged dictionary tiles in shared memory").
 //
 // C[M x N] = A[M x K] * B[N x K]^T:
 //   (a) recon:    A = theta [frames][Kt_pad],  B = beta  (N = bins,     K = elements) -> V_hat   (Eq. 7)
@@ -9,7 +9,9 @@
 // a_lo*b_hi + a_hi*b_lo + a_hi*b_hi (the dropped a_lo*b_lo is ~2^-22 relative; every term is non-negative,
 // so there is no cancellation).  The dictionary (B) is static: it is split and re-tiled once, at
 // set_model, into the exact shared-memory image of a pipeline stage, so each stage of B is ONE
-// cp.async.bulk; the per-sweep operand A is split on the fly by converter warps.
+// cp.async.bulk.  The per-sweep operand A arrives by TMA (one 128-row x 16-float tensor copy per stage,
+// 64-byte swizzle); converter warps split it and store hi / lo into TENSOR MEMORY, from where the MMAs
+// read it (TS mode) -- A never goes through shared memory twice and never through L1.
 //
 // Accuracy of the accumulation (DESIGN "3xTF32 on tcgen05"): the tensor core's FP32 accumulator loses
 // about half an ulp per update (measured: the error grows linearly with K).  The MMAs therefore
@@ -18,16 +20,21 @@
 // The error is then independent of K (Kt = 800 ... 8000), and the register accumulator doubles as the
 // output double-buffer: the MMAs of tile i+1 run while the epilogue of tile i computes.
 //
-// One persistent CTA per SM, warp-specialised (22 warps):
-//   warps 0-7   converters, two groups of 4 alternating pipeline stages: FP32 A rows (prefetched one
-//               group-stage ahead in registers) -> hi/lo split -> shared memory in the canonical K-major
-//               no-swizzle UMMA layout (8-row x 16-byte core matrices);
-//   warp  8     TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=8 per instruction);
-//   warp  9     B producer: one cp.async.bulk per stage (mbarrier complete_tx);
-//   warps 10-21 epilogue: three warps per TMEM lane quarter, each owning every third 32-column chunk;
-//               thread = output row; 128-bit vector loads/stores of its row.
-// Epilogues: RATIO (R = V / V_hat, FP64 row partials of sum V log V_hat, zero-support flag, optional
-// V_hat), STORE (V_hat), SEPARATE (v_t/alpha_0 scaled V_src^(s)), BACKPROJ (n = theta .* C).
+// One persistent CTA per SM, warp-specialised (18 warps):
+//   warps 0-3   converters: thread t = A row t = TMEM lane t; A slab from the stage's smem copy (swizzled,
+//               conflict-free 128-bit reads) -> tf32 hi / lo -> tcgen05.st into the stage's TMEM columns;
+//   warps 4-15  epilogue: three warps per TMEM lane quarter, each owning every third 32-column chunk;
+//               thread = output row.  Per 32 x 16 sub-tile the epilogue operand (V or theta) is fetched
+//               by TMA into private smem (64-byte swizzle) when the tile starts, and the result (R or n)
+//               leaves by a TMA store of the same sub-tile: global traffic is fully coalesced, and a
+//               16-column tail chunk (BN = 176, 208, ...) never touches the next column tile;
+//   warp  16    TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=8 per instruction);
+//   warp  17    producer: per stage one cp.async.bulk (B image) + one TMA tensor copy (A), one mbarrier.
+// Epilogues: RATIO (R = V / V_hat, FP64 row partials of sum V log V_hat, zero-support flag), BACKPROJ
+// (n = theta .* C) through TMA; STORE (V_hat) and SEPARATE (v_t/alpha_0 scaled V_src^(s)), which run only
+// for posteriors / separation (off the sweep), write directly from registers.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -43,22 +50,31 @@ namespace {
 constexpr int TC_BM = 128;
 constexpr int TC_KB = 16;                  // k-elements per pipeline stage (2 MMAs of K=8 per split product)
 constexpr int CHUNK_KB = 4;                // k-blocks accumulated in TMEM before the epilogue drains the slot
-// Warp roles: warps 0-3 converters, 4-15 epilogue, 16 MMA issuer + TMEM allocator, 17 B producer
+// Warp roles: warps 0-3 converters, 4-15 epilogue, 16 MMA issuer + TMEM allocator, 17 producer
 constexpr int CONV_WARPS = 4;
 constexpr int W_EPI0 = 4;
 constexpr int EPI_PER_Q = 3;               // epilogue warps per TMEM lane quarter
 constexpr int EPI_WARPS = 4 * EPI_PER_Q;   // 12
 constexpr int W_MMA = 16;
-constexpr int W_BLOAD = 17;
-constexpr int TC_THREADS = 18 * 32;        // 576 -> up to 112 registers per thread
-constexpr int TC_SLOT_COLS = 256;          // TMEM columns per accumulation slot (2 slots)
+constexpr int W_PROD = 17;
+constexpr int TC_THREADS = 18 * 32;        // 576
 constexpr int TC_MAX_BN = 192;             // 6 x 32-column chunks = 2 per epilogue warp (64 FP32 registers)
 constexpr int EPI_CH = 2;                  // chunks per epilogue warp
-constexpr int RAW_DEPTH = 4;               // A stages in flight (cp.async) ahead of the converters
-constexpr int RAW_SLOTS = RAW_DEPTH + 1;
-constexpr int RAW_ROW = 20;                // floats per staged A row (16 + 4 pad: conflict-free 128-bit reads)
-constexpr int RAW_OFF = 4096;              // [0,1024) barriers, [1024,4096) row-partial exchange
-constexpr int RING_OFF = RAW_OFF + RAW_SLOTS * TC_BM * RAW_ROW * 4;   // then the hi/lo operand ring
+constexpr int A_STAGE_COLS = 2 * TC_KB;    // TMEM columns of one A stage: [hi 16][lo 16]
+constexpr int A_TILE_BYTES = TC_BM * TC_KB * 4;   // 8 KB smem copy of one A stage (TMA, 64-byte swizzle)
+constexpr int EPI_SUB_BYTES = 32 * 16 * 4;        // 2 KB epilogue sub-tile: 32 rows x 16 columns (TMA, 64-byte swizzle)
+constexpr int EPI_TILE_BYTES = 2 * EPI_SUB_BYTES; // per 32-column chunk
+constexpr int MAX_STAGES = 8;
+constexpr int XCH_OFF = 1024;                                      // [3][128] FP64 row partials
+constexpr int EPI_OFF = 4096;                                      // epilogue tiles [12][2][4 KB]
+constexpr int RING_OFF = EPI_OFF + EPI_WARPS * EPI_CH * EPI_TILE_BYTES;   // then the stage ring
+constexpr int SMEM_MAX = 227 * 1024;
+
+// TMEM map (512 columns): accumulation slots at [0, BN) and [BN, 2 BN); A stages from a_col0(BN).
+__host__ __device__ constexpr int a_col0(int bn) { return (2 * bn + 31) & ~31; }
+__host__ __device__ constexpr int tmem_a_stages(int bn) { return (512 - a_col0(bn)) / A_STAGE_COLS; }
+// one ring stage = [A copy 8 KB][B hi | B lo], 1 KB aligned (the A swizzle pattern is address-based)
+__host__ __device__ constexpr int stage_bytes_of(int bn) { return (A_TILE_BYTES + 2 * bn * TC_KB * 4 + 1023) & ~1023; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -88,6 +104,22 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// 2-D TMA tensor copies: c0 = element index along the contiguous dimension, c1 = row
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int c1, const void *src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
+                 "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -97,15 +129,25 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar) {
                  : "memory");
 }
 
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                            uint32_t accumulate) {
+// A from tensor memory (TS mode): a_tmem = TMEM address of the 128-lane x 8-column K-major A block.
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "setp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
         "}\n" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// 16 consecutive TMEM columns of this thread's lane <- v[0..15]
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
 }
 
 // K-major, no-swizzle UMMA shared-memory descriptor.  Core matrix = 8 rows x 16 bytes (contiguous);
@@ -172,19 +214,14 @@ struct TcParams {
     int bn;                 // tile width (multiple of 16, <= TC_MAX_BN)
     int k_begin, k_end;     // contraction window (global element index)
     int stages;
-    const float *A;
-    int lda;
+    int tma_epi;            // 1: epilogue operand in / result out through TMA (RATIO without V_hat, BACKPROJ)
     const float *Bsplit;    // pre-split, pre-tiled B: chunk (nt, kb) = [hi BN x 16][lo BN x 16] UMMA images
     int nkb_total;          // k-blocks per column tile in Bsplit
     // epilogue
     int ldc;                // row length of V / R (RATIO) or theta / n (BACKPROJ); a multiple of 8
     int F;                  // true bins (V_hat / V_src column bound)
-    const float *V;
-    float *R;
     float *Vhat;
     double *data_part;
-    const float *theta;
-    float *n_out;
     const float *row_scale;
     float *out_src;
     int T, S, s;
@@ -193,42 +230,21 @@ struct TcParams {
 };
 
 struct Smem {
-    uint64_t full[8], empty[8], pfull[2], pempty[2];
+    uint64_t full[MAX_STAGES], empty[MAX_STAGES], loaded[MAX_STAGES], pfull[2], pempty[2], ebar[EPI_WARPS];
     uint32_t tmem_base;
 };
 
-// One FP32 float4 of row `row` at column k, masked to the window [kb, ke) (zeros outside).
-__device__ __forceinline__ float4 ld_masked(const float *row, int k, int kb, int ke) {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (k < ke && k + 3 >= kb) {
-        v = __ldg(reinterpret_cast<const float4 *>(row + k));
-        if (k < kb || k + 4 > ke) {
-            if (k + 0 < kb || k + 0 >= ke) v.x = 0.f;
-            if (k + 1 < kb || k + 1 >= ke) v.y = 0.f;
-            if (k + 2 < kb || k + 2 >= ke) v.z = 0.f;
-            if (k + 3 < kb || k + 3 >= ke) v.w = 0.f;
-        }
-    }
-    return v;
-}
+// 16-byte chunk c of row r in a TMA tile with 64-B rows, 64-byte swizzle (bits [4,5] ^= bits [7,8])
+__device__ __forceinline__ uint32_t swz64(int r, int c) { return (uint32_t)r * 64u + (uint32_t)((c ^ (r >> 1)) & 3) * 16u; }
 
-__device__ __forceinline__ void split_store(unsigned char *hi_base, unsigned char *lo_base, uint32_t off, float4 v) {
-    float4 hi, lo;
-    hi.x = tf32_rn(v.x); lo.x = tf32_rn(v.x - hi.x);
-    hi.y = tf32_rn(v.y); lo.y = tf32_rn(v.y - hi.y);
-    hi.z = tf32_rn(v.z); lo.z = tf32_rn(v.z - hi.z);
-    hi.w = tf32_rn(v.w); lo.w = tf32_rn(v.w - hi.w);
-    *reinterpret_cast<float4 *>(hi_base + off) = hi;
-    *reinterpret_cast<float4 *>(lo_base + off) = lo;
-}
-
-__global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmIn,
+                   const __grid_constant__ CUtensorMap tmOut, TcParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const int BN = p.bn;
-    const uint32_t a_bytes = TC_BM * TC_KB * 4;           // one of hi / lo
-    const uint32_t b_bytes = (uint32_t)BN * TC_KB * 4;
-    const uint32_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
+    const uint32_t b_bytes = (uint32_t)BN * TC_KB * 4;     // one of hi / lo
+    const uint32_t stage_bytes = (uint32_t)stage_bytes_of(BN);
     unsigned char *ring = smem_raw + RING_OFF;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -241,18 +257,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.stages; ++i) {
-            mbar_init(&S.full[i], 128 + 1);   // the converters + the B producer's expect_tx arrive
-            mbar_init(&S.empty[i], 1);
+            mbar_init(&S.full[i], 128);      // the converters
+            mbar_init(&S.empty[i], 1);       // tcgen05.commit of the stage's MMAs
+            mbar_init(&S.loaded[i], 1);      // the producer's expect_tx (A + B bytes)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&S.pfull[i], 1);
             mbar_init(&S.pempty[i], EPI_WARPS * 32);
         }
+        for (int i = 0; i < EPI_WARPS; ++i) mbar_init(&S.ebar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == W_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&S.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (warp == W_PROD && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+        if (p.tma_epi) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmIn) : "memory");
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmOut) : "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -260,84 +285,66 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
     const uint32_t tmem = S.tmem_base;
 
     if (warp < CONV_WARPS) {
-        // ------------------------------------------------------------ converters (A operand)
-        // Thread t owns row t of every A tile: it copies the row's 16-float slab of stage it + RAW_DEPTH
-        // into a private staging slot with cp.async (no registers held, RAW_DEPTH stages in flight),
-        // then splits stage it from its slot into the hi/lo UMMA images.
+        // ------------------------------------------------------------ converters (A operand -> TMEM)
         const int t = threadIdx.x;
-        float *raw = reinterpret_cast<float *>(smem_raw + RAW_OFF);
-        int tile = blockIdx.x, kb = 0, tile2 = blockIdx.x, kb2 = 0;
-        auto advance = [&](int &tl, int &k_b) {
-            if (++k_b == n_kb) {
-                k_b = 0;
-                tl += gridDim.x;
-            }
-        };
-        auto issue = [&](int tl, int k_b, int slot) {
-            if (tl < n_total && !(p.dbg & 1)) {
-                const int mt = tl / p.n_tiles;
-                const int k0 = kstart + k_b * TC_KB;
-                const float *arow = p.A + (size_t)min(mt * TC_BM + t, p.M - 1) * p.lda;
-                const uint32_t dst = smem_u32(raw + ((size_t)slot * TC_BM + t) * RAW_ROW);
+        const uint32_t a_base = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)a_col0(BN);
+        uint32_t it = 0;
+        for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
+            for (int kb = 0; kb < n_kb; ++kb, ++it) {
+                const uint32_t st = it % p.stages, ph = (it / p.stages) & 1;
+                mbar_wait(&S.loaded[st], ph);
+                tc_fence_after();
+                const unsigned char *ab = ring + (size_t)st * stage_bytes;
+                float x[TC_KB];
 #pragma unroll
                 for (int c4 = 0; c4 < TC_KB / 4; ++c4) {
-                    const int k = k0 + 4 * c4;
-                    const bool in = k < p.k_end && k + 3 >= p.k_begin;   // whole float4 inside the row
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 16 * c4),
-                                 "l"(arow + (in ? k : 0)), "r"(in ? 16 : 0));
+                    const float4 v = (p.dbg & 1) ? make_float4(1.f, 1.f, 1.f, 1.f)
+                                                 : *reinterpret_cast<const float4 *>(ab + swz64(t, c4));
+                    x[4 * c4 + 0] = v.x;
+                    x[4 * c4 + 1] = v.y;
+                    x[4 * c4 + 2] = v.z;
+                    x[4 * c4 + 3] = v.w;
                 }
-            }
-            asm volatile("cp.async.commit_group;\n" ::: "memory");
-        };
-        for (int d = 0; d < RAW_DEPTH; ++d) {
-            issue(tile2, kb2, d);
-            advance(tile2, kb2);
-        }
-        uint32_t it = 0;
-        while (tile < n_total) {
-            asm volatile("cp.async.wait_group %0;\n" ::"n"(RAW_DEPTH - 1) : "memory");
-            const float *src = raw + ((size_t)(it % RAW_SLOTS) * TC_BM + t) * RAW_ROW;
-            float4 ca[TC_KB / 4];
+                const int k0 = kstart + kb * TC_KB;
+                if (k0 < p.k_begin || k0 + TC_KB > p.k_end) {   // window edges inside the slab
 #pragma unroll
-            for (int c4 = 0; c4 < TC_KB / 4; ++c4) {
-                ca[c4] = (p.dbg & 1) ? make_float4(1.f, 1.f, 1.f, 1.f) : *reinterpret_cast<const float4 *>(src + 4 * c4);
-                const int k = kstart + kb * TC_KB + 4 * c4;
-                if (k < p.k_begin || k + 4 > p.k_end) {   // window edges inside a float4
-                    if (k + 0 < p.k_begin || k + 0 >= p.k_end) ca[c4].x = 0.f;
-                    if (k + 1 < p.k_begin || k + 1 >= p.k_end) ca[c4].y = 0.f;
-                    if (k + 2 < p.k_begin || k + 2 >= p.k_end) ca[c4].z = 0.f;
-                    if (k + 3 < p.k_begin || k + 3 >= p.k_end) ca[c4].w = 0.f;
+                    for (int i = 0; i < TC_KB; ++i)
+                        if (k0 + i < p.k_begin || k0 + i >= p.k_end) x[i] = 0.f;
                 }
-            }
-            issue(tile2, kb2, (it + RAW_DEPTH) % RAW_SLOTS);
-            advance(tile2, kb2);
-            const uint32_t st = it % p.stages, ph = (it / p.stages) & 1;
-            mbar_wait(&S.empty[st], ph ^ 1);
-            unsigned char *sa_hi = ring + (size_t)st * stage_bytes;
-            unsigned char *sa_lo = sa_hi + a_bytes;
+                uint32_t hi[TC_KB], lo[TC_KB];
 #pragma unroll
-            for (int c4 = 0; c4 < TC_KB / 4; ++c4)
-                if (!(p.dbg & 8)) split_store(sa_hi, sa_lo, (uint32_t)c4 * (TC_BM * 16) + (uint32_t)t * 16, ca[c4]);
-            if (!(p.dbg & 16)) fence_proxy_async_smem();
-            mbar_arrive(&S.full[st]);
-            ++it;
-            advance(tile, kb);
+                for (int i = 0; i < TC_KB; ++i) {
+                    const float h = tf32_rn(x[i]);
+                    hi[i] = __float_as_uint(h);
+                    lo[i] = __float_as_uint(tf32_rn(x[i] - h));
+                }
+                if (!(p.dbg & 8)) {
+                    tmem_st16(a_base + st * A_STAGE_COLS, hi);
+                    tmem_st16(a_base + st * A_STAGE_COLS + TC_KB, lo);
+                    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                }
+                tc_fence_before();
+                mbar_arrive(&S.full[st]);
+            }
         }
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    } else if (warp == W_BLOAD) {
-        // ------------------------------------------------------------ B producer (static dictionary)
+    } else if (warp == W_PROD) {
+        // ------------------------------------------------------------ producer: B image + A tile per stage
         if (lane == 0) {
             uint32_t it = 0;
             for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
-                const int nt = tile % p.n_tiles;
+                const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
                 const float *bt = p.Bsplit + (size_t)nt * p.nkb_total * (2 * (size_t)BN * TC_KB);
                 for (int kb = 0; kb < n_kb; ++kb, ++it) {
                     const uint32_t st = it % p.stages, ph = (it / p.stages) & 1;
                     mbar_wait(&S.empty[st], ph ^ 1);
-                    unsigned char *sb = ring + (size_t)st * stage_bytes + 2 * a_bytes;
-                    if (p.dbg & 32) { mbar_arrive(&S.full[st]); continue; }
-                    mbar_arrive_expect_tx(&S.full[st], 2 * b_bytes);
-                    bulk_g2s(sb, bt + (size_t)(kb0 + kb) * (2 * (size_t)BN * TC_KB), 2 * b_bytes, &S.full[st]);
+                    unsigned char *sa = ring + (size_t)st * stage_bytes;
+                    const uint32_t bytes = ((p.dbg & 32) ? 0u : 2 * b_bytes) + ((p.dbg & 1) ? 0u : (uint32_t)A_TILE_BYTES);
+                    if (bytes == 0) { mbar_arrive(&S.loaded[st]); continue; }
+                    mbar_arrive_expect_tx(&S.loaded[st], bytes);
+                    if (!(p.dbg & 32))
+                        bulk_g2s(sa + A_TILE_BYTES, bt + (size_t)(kb0 + kb) * (2 * (size_t)BN * TC_KB), 2 * b_bytes,
+                                 &S.loaded[st]);
+                    if (!(p.dbg & 1)) tma_load_2d(sa, &tmA, kstart + kb * TC_KB, mt * TC_BM, &S.loaded[st]);
                 }
             }
         }
@@ -350,30 +357,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
                 const uint32_t slot = ch_it & 1, sph = (ch_it >> 1) & 1;
                 mbar_wait(&S.pempty[slot], sph ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem + slot * TC_SLOT_COLS;
+                const uint32_t d = tmem + slot * (uint32_t)BN;
                 const int kb_end = min(n_kb, (c + 1) * CHUNK_KB);
                 for (int kb = c * CHUNK_KB; kb < kb_end; ++kb, ++it) {
                     const uint32_t st = it % p.stages, ph = (it / p.stages) & 1;
-                    mbar_wait(&S.full[st], ph);
+                    mbar_wait(&S.loaded[st], ph);   // B image landed (async proxy)
+                    mbar_wait(&S.full[st], ph);     // A split into TMEM
                     tc_fence_after();
                     if (lane == 0) {
-                        const uint32_t a_hi = smem_u32(ring + (size_t)st * stage_bytes);
-                        const uint32_t a_lo = a_hi + a_bytes;
-                        const uint32_t b_hi = a_lo + a_bytes;
+                        const uint32_t a_hi = tmem + (uint32_t)a_col0(BN) + st * A_STAGE_COLS;
+                        const uint32_t a_lo = a_hi + TC_KB;
+                        const uint32_t b_hi = smem_u32(ring + (size_t)st * stage_bytes + A_TILE_BYTES);
                         const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
                         for (int kk = 0; kk < TC_KB / 8; ++kk) {
-                            // K = 8 per MMA = 2 core matrices along K = 2 * LBO bytes
-                            const uint32_t ao = (uint32_t)kk * 2 * (TC_BM * 16), bo = (uint32_t)kk * 2 * ((uint32_t)BN * 16);
-                            const uint64_t dah = umma_desc(a_hi + ao, TC_BM * 16, 128);
-                            const uint64_t dal = umma_desc(a_lo + ao, TC_BM * 16, 128);
+                            // K = 8 per MMA: 8 TMEM columns of A; 2 core matrices along K = 2 * LBO bytes of B
+                            const uint32_t bo = (uint32_t)kk * 2 * ((uint32_t)BN * 16);
                             const uint64_t dbh = umma_desc(b_hi + bo, (uint32_t)BN * 16, 128);
                             const uint64_t dbl = umma_desc(b_lo + bo, (uint32_t)BN * 16, 128);
                             const uint32_t first = (kb == c * CHUNK_KB && kk == 0) ? 0u : 1u;
                             if (p.dbg & 2) continue;
-                            tc_mma_tf32(d, dal, dbh, idesc, first);   // small terms first
-                            tc_mma_tf32(d, dah, dbl, idesc, 1u);
-                            tc_mma_tf32(d, dah, dbh, idesc, 1u);
+                            tc_mma_tf32_ts(d, a_lo + 8 * kk, dbh, idesc, first);   // small terms first
+                            tc_mma_tf32_ts(d, a_hi + 8 * kk, dbl, idesc, 1u);
+                            tc_mma_tf32_ts(d, a_hi + 8 * kk, dbh, idesc, 1u);
                         }
                         tc_commit(&S.empty[st]);
                     }
@@ -389,31 +395,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
         const int q = warp & 3;                   // TMEM lane quarter this warp may access
         const int cg = ew >> 2;                   // owns 32-column chunks cg, cg + 3
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-        double *xch = reinterpret_cast<double *>(smem_raw + 1024);   // [3][128] row partials
-        uint32_t ch_it = 0;
+        double *xch = reinterpret_cast<double *>(smem_raw + XCH_OFF);   // [3][128] row partials
+        unsigned char *etile = smem_raw + EPI_OFF + (size_t)ew * EPI_CH * EPI_TILE_BYTES;
+        const bool tma_epi = p.tma_epi && !(p.dbg & 4);
+        uint32_t ch_it = 0, e_ph = 0;
         unsigned bad = 0;
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
             const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
             const int m0 = mt * TC_BM, n0 = nt * BN;
+            const int r0 = m0 + 32 * q;            // first row of this warp's 32-row slice
+            uint32_t e_bytes = 0;
+#pragma unroll
+            for (int j = 0; j < EPI_CH; ++j)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+                    if (32 * (cg + EPI_PER_Q * j) + 16 * (hh + 1) <= BN) e_bytes += EPI_SUB_BYTES;
+            if (tma_epi && e_bytes) {
+                // fetch this warp's epilogue operand tiles now; they land while the tile accumulates
+                if (lane == 0) {
+                    bulk_wait_read_all();          // the previous tile's stores have read the buffers
+                    mbar_arrive_expect_tx(&S.ebar[ew], e_bytes);
+#pragma unroll
+                    for (int j = 0; j < EPI_CH; ++j)
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int c0 = 32 * (cg + EPI_PER_Q * j) + 16 * hh;
+                            if (c0 + 16 <= BN)
+                                tma_load_2d(etile + j * EPI_TILE_BYTES + hh * EPI_SUB_BYTES, &tmIn, n0 + c0, r0, &S.ebar[ew]);
+                        }
+                }
+                __syncwarp();
+            }
             float acc[EPI_CH][32];
 #pragma unroll
             for (int j = 0; j < EPI_CH; ++j)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) acc[j][i] = 0.f;
-            {   // warm L2 with this row's epilogue operand (V or theta) while the tile accumulates
-                const int prow = m0 + 32 * q + lane;
-                const float *pb = p.mode == TC_RATIO ? p.V : (p.mode == TC_BACKPROJ ? p.theta : nullptr);
-                if (pb && prow < p.M && !(p.dbg & 4)) {
-#pragma unroll
-                    for (int j = 0; j < EPI_CH; ++j) {
-                        const int col = n0 + 32 * (cg + EPI_PER_Q * j);
-                        if (col < p.ldc && 32 * (cg + EPI_PER_Q * j) < BN) {
-                            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pb + (size_t)prow * p.ldc + col));
-                            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pb + (size_t)prow * p.ldc + min(col + 31, p.ldc - 1)));
-                        }
-                    }
-                }
-            }
             for (int c = 0; c < n_chunks; ++c, ++ch_it) {
                 const uint32_t slot = ch_it & 1, sph = (ch_it >> 1) & 1;
                 mbar_wait(&S.pfull[slot], sph);
@@ -421,7 +438,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
 #pragma unroll
                 for (int j = 0; j < EPI_CH; ++j) {
                     const int c0 = 32 * (cg + EPI_PER_Q * j);
-                    const uint32_t ta = tmem + slot * TC_SLOT_COLS + lane_base + (uint32_t)c0;
+                    const uint32_t ta = tmem + slot * (uint32_t)BN + lane_base + (uint32_t)c0;
                     if (c0 + 32 <= BN) tmem_add32(ta, acc[j]);
                     else if (c0 + 16 <= BN) tmem_add16(ta, acc[j]);
                 }
@@ -429,62 +446,77 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
                 mbar_arrive(&S.pempty[slot]);
             }
             // the tile's full sum is in registers; the MMAs of the next tile are already running
-            const int row = m0 + 32 * q + lane;
+            const int row = r0 + lane;
             const bool row_ok = row < p.M;
             double part = 0.0;
+            if (tma_epi && e_bytes) {
+                mbar_wait(&S.ebar[ew], e_ph);
+                e_ph ^= 1;
 #pragma unroll
-            for (int j = 0; j < EPI_CH; ++j) {
-                const int c0 = 32 * (cg + EPI_PER_Q * j);
-                const int colb = n0 + c0;
-                if (c0 >= BN || !row_ok) continue;
-                const int w = min(32, BN - c0);
-                if (p.dbg & 4) {
-                    part += (double)acc[j][0];
-                } else if (p.mode == TC_RATIO || p.mode == TC_BACKPROJ) {
-                    const float *src = p.mode == TC_RATIO ? p.V : p.theta;
-                    float *dst = p.mode == TC_RATIO ? p.R : p.n_out;
+                for (int j = 0; j < EPI_CH; ++j) {
 #pragma unroll
-                    for (int i4 = 0; i4 < 8; ++i4) {
-                        const int col = colb + 4 * i4;
-                        if (4 * i4 >= w || col >= p.ldc) continue;
-                        const size_t o = (size_t)row * p.ldc + col;
-                        const float4 x = *reinterpret_cast<const float4 *>(src + o);
-                        const float xv[4] = {x.x, x.y, x.z, x.w};
-                        float y[4];
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int c0 = 32 * (cg + EPI_PER_Q * j) + 16 * hh;
+                        if (c0 + 16 > BN) continue;
+                        unsigned char *tb = etile + j * EPI_TILE_BYTES + hh * EPI_SUB_BYTES;
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float vh = acc[j][4 * i4 + e];
-                            if (p.mode == TC_BACKPROJ) {
-                                y[e] = xv[e] * vh;                       // n = theta .* (R beta)
-                            } else {
-                                y[e] = 0.f;                              // R = V / V_hat
-                                if (xv[e] > 0.f) {
-                                    if (vh > 0.f) {
-                                        y[e] = xv[e] / vh;
-                                        part += (double)xv[e] * (double)logf(vh);
-                                    } else {
-                                        bad |= FLAG_ZERO_SUPPORT;
+                        for (int i4 = 0; i4 < 4; ++i4) {
+                            float4 *px = reinterpret_cast<float4 *>(tb + swz64(lane, i4));
+                            const float4 x = *px;
+                            const float xv[4] = {x.x, x.y, x.z, x.w};
+                            float y[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float vh = acc[j][16 * hh + 4 * i4 + e];
+                                if (p.mode == TC_BACKPROJ) {
+                                    y[e] = xv[e] * vh;                       // n = theta .* (R beta)
+                                } else {
+                                    y[e] = 0.f;                              // R = V / V_hat
+                                    if (xv[e] > 0.f) {
+                                        if (vh > 0.f) {
+                                            y[e] = xv[e] / vh;
+                                            part += (double)xv[e] * (double)logf(vh);
+                                        } else {
+                                            bad |= FLAG_ZERO_SUPPORT;
+                                        }
                                     }
                                 }
-                                if (p.Vhat && col + e < p.F) p.Vhat[(size_t)row * p.F + col + e] = vh;
                             }
+                            *px = make_float4(y[0], y[1], y[2], y[3]);
                         }
-                        *reinterpret_cast<float4 *>(dst + o) = make_float4(y[0], y[1], y[2], y[3]);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmOut, n0 + c0, r0, tb);
+                            bulk_commit();
+                        }
                     }
-                } else if (p.mode == TC_STORE) {
+                }
+                if (!row_ok) part = 0.0;
+            } else {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (i < w && colb + i < p.F) p.Vhat[(size_t)row * p.F + colb + i] = acc[j][i];
-                } else {   // TC_SEPARATE
-                    const float sc = p.row_scale[row];
-                    const int m = row / p.T, tt = row - m * p.T;
-                    float *out = p.out_src + ((size_t)(m * p.S + p.s) * p.T + tt) * p.F;
+                for (int j = 0; j < EPI_CH; ++j) {
+                    const int c0 = 32 * (cg + EPI_PER_Q * j);
+                    const int colb = n0 + c0;
+                    if (c0 >= BN || !row_ok) continue;
+                    const int w = min(32, BN - c0);
+                    if (p.dbg & 4) {
+                        part += (double)acc[j][0];
+                    } else if (p.mode == TC_STORE) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (i < w && colb + i < p.F) out[colb + i] = acc[j][i] * sc;
+                        for (int i = 0; i < 32; ++i)
+                            if (i < w && colb + i < p.F) p.Vhat[(size_t)row * p.F + colb + i] = acc[j][i];
+                    } else if (p.mode == TC_SEPARATE) {
+                        const float sc = p.row_scale[row];
+                        const int m = row / p.T, tt = row - m * p.T;
+                        float *out = p.out_src + ((size_t)(m * p.S + p.s) * p.T + tt) * p.F;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < w && colb + i < p.F) out[colb + i] = acc[j][i] * sc;
+                    }
                 }
             }
-            if (p.mode == TC_RATIO) {
+            if (p.mode == TC_RATIO && p.data_part) {
                 // three warps share each row: combine their partials in a fixed order
                 const int rl = 32 * q + lane;
                 xch[cg * 128 + rl] = part;
@@ -494,6 +526,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
                 asm volatile("bar.sync 1, %0;\n" ::"r"(EPI_WARPS * 32) : "memory");
             }
         }
+        if (lane == 0) bulk_wait_all();
         if (bad) atomicOr(p.flags, bad);
     }
 
@@ -506,39 +539,68 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_gemm_kernel(TcParams p) {
 }
 
 int g_num_sms = 0;
-
-size_t stage_bytes_for(int bn) { return 2 * (size_t)TC_BM * TC_KB * 4 + 2 * (size_t)bn * TC_KB * 4; }
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 int stages_for(int bn) {
-    const size_t budget = 227 * 1024 - RING_OFF;
-    int s = (int)(budget / stage_bytes_for(bn));
-    return s > 8 ? 8 : s;
+    int s = (SMEM_MAX - RING_OFF) / stage_bytes_of(bn);
+    if (s > tmem_a_stages(bn)) s = tmem_a_stages(bn);
+    return s > MAX_STAGES ? MAX_STAGES : s;
 }
 
-cudaError_t launch_tc(const TcParams &p, cudaStream_t st) {
+// 2-D FP32 tensor map over rows x cols (row pitch ld floats), box box_c x box_r
+cudaError_t make_map(CUtensorMap *m, const float *base, int64_t cols, int64_t rows, int64_t ld, int box_c, int box_r,
+                     CUtensorMapSwizzle swz) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+        g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)box_c, (cuuint32_t)box_r};
+    const cuuint32_t es[2] = {1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// A [M][lda] (cols = lda); epilogue in / out [M][ldc]
+cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, float *eout, cudaStream_t st) {
     if (g_num_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     if (p.bn < 16 || p.bn > TC_MAX_BN || p.bn % 16 || p.stages < 2) return cudaErrorInvalidValue;
-    const size_t smem = RING_OFF + (size_t)p.stages * stage_bytes_for(p.bn);
+    const size_t smem = RING_OFF + (size_t)p.stages * stage_bytes_of(p.bn);
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
         if (e != cudaSuccess) return e;
         attr = true;
+    }
+    CUtensorMap mA, mIn, mOut;
+    cudaError_t e = make_map(&mA, A, lda, p.M, lda, TC_KB, TC_BM, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (e != cudaSuccess) return e;
+    mIn = mA;
+    mOut = mA;
+    if (p.tma_epi) {
+        e = make_map(&mIn, ein, p.ldc, p.M, p.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (e == cudaSuccess) e = make_map(&mOut, eout, p.ldc, p.M, p.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (e != cudaSuccess) return e;
     }
     const int n_total = ((p.M + TC_BM - 1) / TC_BM) * p.n_tiles;
     const int grid = n_total < g_num_sms ? n_total : g_num_sms;
     static int dbg = -1;
     if (dbg < 0) {
-        const char *e = getenv("NFHMM_TC_DEBUG");
-        dbg = e ? atoi(e) : 0;
+        const char *ev = getenv("NFHMM_TC_DEBUG");
+        dbg = ev ? atoi(ev) : 0;
     }
-    TcParams q = p;
-    q.dbg = dbg;
-    tc_gemm_kernel<<<grid, TC_THREADS, smem, st>>>(q);
+    p.dbg = dbg;
+    tc_gemm_kernel<<<grid, TC_THREADS, smem, st>>>(mA, mIn, mOut, p);
     return cudaGetLastError();
 }
 
@@ -594,14 +656,11 @@ cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st) {
     p.k_begin = a.k_begin;
     p.k_end = a.k_end;
     p.stages = stages_for(bn);
-    p.A = a.A;
-    p.lda = a.lda;
+    p.tma_epi = (p.mode == TC_RATIO && !a.Vhat) ? 1 : 0;
     p.Bsplit = a.Bsplit;
     p.nkb_total = a.nkb_total;
     p.ldc = a.ldv;
     p.F = a.F;
-    p.V = a.V;
-    p.R = a.R;
     p.Vhat = a.Vhat;
     p.data_part = a.data_part;
     p.row_scale = a.row_scale;
@@ -610,7 +669,8 @@ cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st) {
     p.S = a.S;
     p.s = a.s;
     p.flags = a.flags;
-    return launch_tc(p, st);
+    if (p.mode == TC_RATIO && a.Vhat) return cudaErrorInvalidValue;   // RATIO always goes through TMA
+    return launch_tc(p, a.A, a.lda, a.V, a.R, st);
 }
 
 cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st) {
@@ -622,14 +682,11 @@ cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaS
     p.k_begin = 0;
     p.k_end = a.Kpad;
     p.stages = stages_for(bn);
-    p.A = a.A;
-    p.lda = a.lda;
+    p.tma_epi = 1;
     p.Bsplit = a.Bsplit;
     p.nkb_total = a.nkb_total;
     p.ldc = a.ldb;
-    p.theta = a.theta;
-    p.n_out = a.n_out;
-    return launch_tc(p, st);
+    return launch_tc(p, a.A, a.lda, a.theta, a.n_out, st);
 }
 
 }  // namespace nfk

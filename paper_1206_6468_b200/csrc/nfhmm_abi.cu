@@ -211,13 +211,8 @@ int recon_ratio(nfhmm_t *h) {
     return run_recon(h, NFHMM_K_RECON, a);
 }
 
-int sweep(nfhmm_t *h) {
-    if (!h->R_valid) {
-        int r = recon_ratio(h);
-        if (r) return r;
-        h->R_valid = true;
-    }
-    // (b) n = theta .* (R beta): the Eq. 6 data term  sum_l V_lt z_{t,l,k}
+// (b) n = theta .* (R beta): the Eq. 6 data term  sum_l V_lt z_{t,l,k}
+int step_backproj(nfhmm_t *h) {
     BackprojArgs b{};
     b.M = (int)h->frames;
     b.Kpad = h->Fa;
@@ -235,7 +230,11 @@ int sweep(nfhmm_t *h) {
     } else {
         LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj(h->bn_b, b, h->st));
     }
-    // (c)+(d) Eq. 6, digamma/exp, Eq. 8
+    return NFHMM_OK;
+}
+
+// (c)+(d) Eq. 6, digamma/exp, Eq. 8
+int step_dirichlet(nfhmm_t *h) {
     DirichletArgs d{};
     d.frames = (int)h->frames;
     d.T = (int)h->T;
@@ -251,10 +250,15 @@ int sweep(nfhmm_t *h) {
     d.d_hat = h->dhat;
     d.ec = h->ec;
     d.eoff = h->eoff;
+    d.vt = h->vt;
     d.hdir = h->free_energy ? h->hdir : nullptr;
     d.flags = h->flags;
     LAUNCH(h, NFHMM_K_DIRICHLET, launch_dirichlet(d, h->st));
-    // (e) forward-backward per source
+    return NFHMM_OK;
+}
+
+// (e) forward-backward per source
+int step_fb(nfhmm_t *h) {
     FBArgs f{};
     f.M = (int)h->M;
     f.S = h->S;
@@ -270,8 +274,21 @@ int sweep(nfhmm_t *h) {
     f.logZ = h->logZ;
     f.flags = h->flags;
     LAUNCH(h, NFHMM_K_FB, launch_fb(f, h->st));
+    return NFHMM_OK;
+}
+
+int sweep(nfhmm_t *h) {
+    if (!h->R_valid) {
+        int r = recon_ratio(h);
+        if (r) return r;
+        h->R_valid = true;
+    }
+    int r = step_backproj(h);
+    if (!r) r = step_dirichlet(h);
+    if (!r) r = step_fb(h);
+    if (r) return r;
     // (a) z-step of the new alpha: R for the next sweep and the data term of L_i
-    int r = recon_ratio(h);
+    r = recon_ratio(h);
     if (r) return r;
     // (g) L_i
     if (h->free_energy && h->iters_done < h->max_iters) {
@@ -611,6 +628,39 @@ int nfhmm_profile_read(nfhmm_t *h, double *ms, int64_t *launches) {
         if (launches) launches[i] = cnt[i];
     }
     return NFHMM_OK;
+}
+
+int nfhmm_bench_kernel(nfhmm_t *h, int cls, int32_t reps, double *ms_per_launch) {
+    int r = enter(h);
+    if (r) return r;
+    if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
+    if (reps < 1 || !ms_per_launch) return fail(h, NFHMM_EINVAL, "reps >= 1 and ms_per_launch required");
+    if (cls < NFHMM_K_RECON || cls > NFHMM_K_FB) return fail(h, NFHMM_EINVAL, "cls must be RECON..FB");
+    cudaEvent_t a = prof_event(h), b = prof_event(h);
+    if (!a || !b) return fail(h, NFHMM_ECUDA, "event creation failed");
+    const bool prof = h->prof;
+    h->prof = false;
+    CU(h, cudaEventRecord(a, h->st));
+    for (int i = 0; i < reps && !r; ++i) {
+        switch (cls) {
+            case NFHMM_K_RECON: r = recon_ratio(h); break;
+            case NFHMM_K_BACKPROJ: r = step_backproj(h); break;
+            case NFHMM_K_DIRICHLET: r = step_dirichlet(h); break;
+            default: r = step_fb(h); break;
+        }
+    }
+    CU(h, cudaEventRecord(b, h->st));
+    h->prof = prof;
+    if (r) return r;
+    CU(h, cudaEventSynchronize(b));
+    float t = 0.f;
+    CU(h, cudaEventElapsedTime(&t, a, b));
+    *ms_per_launch = (double)t / reps;
+    // the repeated step left the state inconsistent: force a reset before the next sweep
+    h->R_valid = false;
+    h->iters_done = 0;
+    CU(h, cudaMemsetAsync(h->flags, 0, sizeof(unsigned), h->st));
+    return nfhmm_reset(h);
 }
 
 int nfhmm_destroy(nfhmm_t *h) {

@@ -76,6 +76,7 @@ struct DirichletArgs {
     float *alpha;             // [frames][ld]  out: alpha (may alias n_in)
     float *theta;             // [frames][ld]  out: exp(psi(alpha) - psi(alpha_0))
     const float *d_hat;       // [M][S][T][N]  previous q(D) marginals
+    const float *vt;          // [frames]      v_t = sum_l V[t,l]
     float *ec;                // [M][S][T][N]  out: emission exp(gamma*(phi - max_n phi)) in (0, 1]
     double *eoff;             // [M][S][T]     out: gamma * max_n phi (FP64)
     double *hdir;             // [frames]      out: Dirichlet entropy terms of the bound (or NULL)

@@ -58,6 +58,7 @@ SIGNATURES = {
     "nfhmm_kernel_launches": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
     "nfhmm_profile_enable": (ctypes.c_int, [_P, ctypes.c_int]),
     "nfhmm_profile_read": (ctypes.c_int, [_P, ctypes.POINTER(_D), ctypes.POINTER(_I64)]),
+    "nfhmm_bench_kernel": (ctypes.c_int, [_P, ctypes.c_int, _I32, ctypes.POINTER(_D)]),
     "nfhmm_layout": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32),
                                     ctypes.POINTER(_I32)]),
 }
@@ -185,6 +186,14 @@ def nfhmm_profile_enable(h, on=True):
     _check(h, _lib.nfhmm_profile_enable(h, 1 if on else 0))
 
 
+def nfhmm_bench_kernel(h, cls, reps):
+    """Mean device ms per launch of one kernel class run `reps` times back to back (ends with a reset)."""
+    ms = ctypes.c_double()
+    _check(h, _lib.nfhmm_bench_kernel(h, KERNEL_CLASSES.index(cls) if isinstance(cls, str) else cls, reps,
+                                      ctypes.byref(ms)))
+    return ms.value
+
+
 def nfhmm_profile_read(h):
     """{class: (device ms, launches)} accumulated since the last enable (synchronises)."""
     n = len(KERNEL_CLASSES)
@@ -262,6 +271,9 @@ class NFHMM:
 
     def profile_read(self):
         return nfhmm_profile_read(self.h)
+
+    def bench_kernel(self, cls, reps=10):
+        return nfhmm_bench_kernel(self.h, cls, reps)
 
     def posteriors(self, d_hat=True, alpha_hat=True, V_hat=True, free_energy=True):
         """Returns host numpy arrays: d_hat [M][S][T][N], alpha_hat [M][T][Kt], V_hat [M][T][F],
