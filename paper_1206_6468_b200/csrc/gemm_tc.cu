@@ -49,7 +49,7 @@ namespace {
 
 constexpr int TC_BM = 128;
 constexpr int TC_KB = 16;                  // k-elements per pipeline stage (2 MMAs of K=8 per split product)
-constexpr int CHUNK_KB = 4;                // k-blocks accumulated in TMEM before the epilogue drains the slot
+constexpr int CHUNK_KB = 16;               // default k-blocks accumulated in TMEM before the epilogue drains the slot
 // Warp roles: warps 0-3 converters, 4-15 epilogue, 16 MMA issuer + TMEM allocator, 17 producer
 constexpr int CONV_WARPS = 4;
 constexpr int W_EPI0 = 4;
@@ -65,9 +65,10 @@ constexpr int A_TILE_BYTES = TC_BM * TC_KB * 4;   // 8 KB smem copy of one A sta
 constexpr int EPI_SUB_BYTES = 32 * 16 * 4;        // 2 KB epilogue sub-tile: 32 rows x 16 columns (TMA, 64-byte swizzle)
 constexpr int EPI_TILE_BYTES = 2 * EPI_SUB_BYTES; // per 32-column chunk
 constexpr int MAX_STAGES = 8;
+constexpr int A_PREFETCH = 16;             // stages ahead at which the producer pulls A tiles into L2
 constexpr int XCH_OFF = 1024;                                      // [3][128] FP64 row partials
-constexpr int EPI_OFF = 4096;                                      // epilogue tiles [12][2][4 KB]
-constexpr int RING_OFF = EPI_OFF + EPI_WARPS * EPI_CH * EPI_TILE_BYTES;   // then the stage ring
+constexpr int EPI_OFF = 4096;                                      // epilogue tiles [12][4 KB]
+constexpr int RING_OFF = EPI_OFF + EPI_WARPS * EPI_TILE_BYTES;   // then the stage ring
 constexpr int SMEM_MAX = 227 * 1024;
 
 // TMEM map (512 columns): accumulation slots at [0, BN) and [BN, 2 BN); A stages from a_col0(BN).
@@ -98,6 +99,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Same, for roles off the MMA's critical path: the thread may be suspended until the phase completes
+// (hardware wake-up) instead of spinning and stealing issue slots from the MMA / converter warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+// ring position: stage index and phase parity, advanced without divisions
+struct RingPos {
+    uint32_t st = 0, ph = 0;
+    __device__ __forceinline__ void next(uint32_t n) {
+        if (++st == n) {
+            st = 0;
+            ph ^= 1;
+        }
+    }
+};
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
                      smem_u32(dst)),
@@ -111,6 +135,10 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
             smem_u32(dst)),
         "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
+}
+// L2 prefetch of a tensor tile (no shared memory, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n" ::"l"(map), "r"(c0), "r"(c1) : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int c1, const void *src) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map), "r"(c0),
@@ -214,6 +242,7 @@ struct TcParams {
     int bn;                 // tile width (multiple of 16, <= TC_MAX_BN)
     int k_begin, k_end;     // contraction window (global element index)
     int stages;
+    int chunk_kb;           // k-blocks per TMEM accumulation slot (CHUNK_KB)
     int tma_epi;            // 1: epilogue operand in / result out through TMA (RATIO without V_hat, BACKPROJ)
     const float *Bsplit;    // pre-split, pre-tiled B: chunk (nt, kb) = [hi BN x 16][lo BN x 16] UMMA images
     int nkb_total;          // k-blocks per column tile in Bsplit
@@ -226,7 +255,8 @@ struct TcParams {
     float *out_src;
     int T, S, s;
     unsigned *flags;
-    int dbg;                // performance experiments only (NFHMM_TC_DEBUG): 1 no A loads, 2 no MMAs, 4 no epilogue I/O
+    int dbg;                // performance experiments only (NFHMM_TC_DEBUG): 1 no A loads, 2 no MMAs, 4 no epilogue
+                            // I/O, 8 no A TMEM stores, 32 no B loads, 64 no drains, 128 no converter work
 };
 
 struct Smem {
@@ -253,7 +283,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int kstart = p.k_begin & ~(TC_KB - 1);          // k-blocks on the global 16-element grid of Bsplit
     const int kb0 = kstart / TC_KB;
     const int n_kb = (p.k_end - kstart + TC_KB - 1) / TC_KB;
-    const int n_chunks = (n_kb + CHUNK_KB - 1) / CHUNK_KB;
+    const int chunk_kb = p.chunk_kb;
+    const int n_chunks = (n_kb + chunk_kb - 1) / chunk_kb;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.stages; ++i) {
@@ -288,12 +319,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ------------------------------------------------------------ converters (A operand -> TMEM)
         const int t = threadIdx.x;
         const uint32_t a_base = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)a_col0(BN);
-        uint32_t it = 0;
+        RingPos rp;
+        const uint32_t nst = (uint32_t)p.stages;
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
-            for (int kb = 0; kb < n_kb; ++kb, ++it) {
-                const uint32_t st = it % p.stages, ph = (it / p.stages) & 1;
-                mbar_wait(&S.loaded[st], ph);
+            for (int kb = 0; kb < n_kb; ++kb, rp.next(nst)) {
+                const uint32_t st = rp.st;
+                mbar_wait(&S.loaded[st], rp.ph);
                 tc_fence_after();
+                if (p.dbg & 128) {
+                    mbar_arrive(&S.full[st]);
+                    continue;
+                }
                 const unsigned char *ab = ring + (size_t)st * stage_bytes;
                 float x[TC_KB];
 #pragma unroll
@@ -329,40 +365,62 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
     } else if (warp == W_PROD) {
         // ------------------------------------------------------------ producer: B image + A tile per stage
+        // The A rows stream from HBM on first touch: they are pulled into L2 A_PREFETCH stages ahead, so
+        // the ring's own loads (which bound the bytes in flight) see L2 latency only.
         if (lane == 0) {
-            uint32_t it = 0;
+            RingPos rp;
+            const uint32_t nst = (uint32_t)p.stages;
+            int pf_tile = blockIdx.x, pf_kb = 0;
+            auto pf_advance = [&]() {
+                if (++pf_kb == n_kb) {
+                    pf_kb = 0;
+                    pf_tile += gridDim.x;
+                }
+            };
+            auto pf_issue = [&]() {
+                if (pf_tile < n_total && !(p.dbg & 1))
+                    tma_prefetch_2d(&tmA, kstart + pf_kb * TC_KB, (pf_tile / p.n_tiles) * TC_BM);
+                pf_advance();
+            };
+            for (int i = 0; i < A_PREFETCH; ++i) pf_issue();
             for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
                 const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
                 const float *bt = p.Bsplit + (size_t)nt * p.nkb_total * (2 * (size_t)BN * TC_KB);
-                for (int kb = 0; kb < n_kb; ++kb, ++it) {
-                    const uint32_t st = it % p.stages, ph = (it / p.stages) & 1;
-                    mbar_wait(&S.empty[st], ph ^ 1);
+                for (int kb = 0; kb < n_kb; ++kb, rp.next(nst)) {
+                    const uint32_t st = rp.st;
+                    mbar_wait_sleep(&S.empty[st], rp.ph ^ 1);
                     unsigned char *sa = ring + (size_t)st * stage_bytes;
                     const uint32_t bytes = ((p.dbg & 32) ? 0u : 2 * b_bytes) + ((p.dbg & 1) ? 0u : (uint32_t)A_TILE_BYTES);
-                    if (bytes == 0) { mbar_arrive(&S.loaded[st]); continue; }
+                    if (bytes == 0) {
+                        mbar_arrive(&S.loaded[st]);
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&S.loaded[st], bytes);
                     if (!(p.dbg & 32))
                         bulk_g2s(sa + A_TILE_BYTES, bt + (size_t)(kb0 + kb) * (2 * (size_t)BN * TC_KB), 2 * b_bytes,
                                  &S.loaded[st]);
                     if (!(p.dbg & 1)) tma_load_2d(sa, &tmA, kstart + kb * TC_KB, mt * TC_BM, &S.loaded[st]);
+                    pf_issue();
                 }
             }
         }
     } else if (warp == W_MMA) {
         // ------------------------------------------------------------ MMA issuer
         const uint32_t idesc = idesc_tf32(BN);
-        uint32_t it = 0, ch_it = 0;
+        RingPos rp;
+        const uint32_t nst = (uint32_t)p.stages;
+        uint32_t ch_it = 0;
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
             for (int c = 0; c < n_chunks; ++c, ++ch_it) {
                 const uint32_t slot = ch_it & 1, sph = (ch_it >> 1) & 1;
                 mbar_wait(&S.pempty[slot], sph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + slot * (uint32_t)BN;
-                const int kb_end = min(n_kb, (c + 1) * CHUNK_KB);
-                for (int kb = c * CHUNK_KB; kb < kb_end; ++kb, ++it) {
-                    const uint32_t st = it % p.stages, ph = (it / p.stages) & 1;
-                    mbar_wait(&S.loaded[st], ph);   // B image landed (async proxy)
-                    mbar_wait(&S.full[st], ph);     // A split into TMEM
+                const int kb_end = min(n_kb, (c + 1) * chunk_kb);
+                for (int kb = c * chunk_kb; kb < kb_end; ++kb, rp.next(nst)) {
+                    const uint32_t st = rp.st;
+                    mbar_wait(&S.loaded[st], rp.ph);   // B image landed (async proxy)
+                    mbar_wait(&S.full[st], rp.ph);     // A split into TMEM
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t a_hi = tmem + (uint32_t)a_col0(BN) + st * A_STAGE_COLS;
@@ -375,7 +433,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             const uint32_t bo = (uint32_t)kk * 2 * ((uint32_t)BN * 16);
                             const uint64_t dbh = umma_desc(b_hi + bo, (uint32_t)BN * 16, 128);
                             const uint64_t dbl = umma_desc(b_lo + bo, (uint32_t)BN * 16, 128);
-                            const uint32_t first = (kb == c * CHUNK_KB && kk == 0) ? 0u : 1u;
+                            const uint32_t first = (kb == c * chunk_kb && kk == 0) ? 0u : 1u;
                             if (p.dbg & 2) continue;
                             tc_mma_tf32_ts(d, a_lo + 8 * kk, dbh, idesc, first);   // small terms first
                             tc_mma_tf32_ts(d, a_hi + 8 * kk, dbl, idesc, 1u);
@@ -396,36 +454,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int cg = ew >> 2;                   // owns 32-column chunks cg, cg + 3
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         double *xch = reinterpret_cast<double *>(smem_raw + XCH_OFF);   // [3][128] row partials
-        unsigned char *etile = smem_raw + EPI_OFF + (size_t)ew * EPI_CH * EPI_TILE_BYTES;
+        unsigned char *etile = smem_raw + EPI_OFF + (size_t)ew * EPI_TILE_BYTES;
         const bool tma_epi = p.tma_epi && !(p.dbg & 4);
         uint32_t ch_it = 0, e_ph = 0;
         unsigned bad = 0;
+        // operand tiles of chunk j: sub-tiles of 16 columns that lie inside the BN-wide column tile
+        auto chunk_bytes = [&](int j) {
+            uint32_t b = 0;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+                if (32 * (cg + EPI_PER_Q * j) + 16 * (hh + 1) <= BN) b += EPI_SUB_BYTES;
+            return b;
+        };
+        // lane 0: fetch chunk j's operand sub-tiles into the warp's buffer (after earlier stores read it)
+        auto fetch = [&](int j, int n0, int r0) {
+            const uint32_t b = chunk_bytes(j);
+            if (!b) return;
+            bulk_wait_read_all();
+            mbar_arrive_expect_tx(&S.ebar[ew], b);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int c0 = 32 * (cg + EPI_PER_Q * j) + 16 * hh;
+                if (c0 + 16 <= BN) tma_load_2d(etile + hh * EPI_SUB_BYTES, &tmIn, n0 + c0, r0, &S.ebar[ew]);
+            }
+        };
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
             const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
             const int m0 = mt * TC_BM, n0 = nt * BN;
             const int r0 = m0 + 32 * q;            // first row of this warp's 32-row slice
-            uint32_t e_bytes = 0;
-#pragma unroll
-            for (int j = 0; j < EPI_CH; ++j)
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh)
-                    if (32 * (cg + EPI_PER_Q * j) + 16 * (hh + 1) <= BN) e_bytes += EPI_SUB_BYTES;
-            if (tma_epi && e_bytes) {
-                // fetch this warp's epilogue operand tiles now; they land while the tile accumulates
-                if (lane == 0) {
-                    bulk_wait_read_all();          // the previous tile's stores have read the buffers
-                    mbar_arrive_expect_tx(&S.ebar[ew], e_bytes);
-#pragma unroll
-                    for (int j = 0; j < EPI_CH; ++j)
-#pragma unroll
-                        for (int hh = 0; hh < 2; ++hh) {
-                            const int c0 = 32 * (cg + EPI_PER_Q * j) + 16 * hh;
-                            if (c0 + 16 <= BN)
-                                tma_load_2d(etile + j * EPI_TILE_BYTES + hh * EPI_SUB_BYTES, &tmIn, n0 + c0, r0, &S.ebar[ew]);
-                        }
-                }
-                __syncwarp();
-            }
+            // chunk 0's operand lands while the tile accumulates; chunk 1's is fetched after chunk 0 left
+            if (tma_epi && lane == 0) fetch(0, n0, r0);
+            __syncwarp();
             float acc[EPI_CH][32];
 #pragma unroll
             for (int j = 0; j < EPI_CH; ++j)
@@ -433,12 +492,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int i = 0; i < 32; ++i) acc[j][i] = 0.f;
             for (int c = 0; c < n_chunks; ++c, ++ch_it) {
                 const uint32_t slot = ch_it & 1, sph = (ch_it >> 1) & 1;
-                mbar_wait(&S.pfull[slot], sph);
+                mbar_wait_sleep(&S.pfull[slot], sph);
                 tc_fence_after();
 #pragma unroll
                 for (int j = 0; j < EPI_CH; ++j) {
                     const int c0 = 32 * (cg + EPI_PER_Q * j);
                     const uint32_t ta = tmem + slot * (uint32_t)BN + lane_base + (uint32_t)c0;
+                    if (p.dbg & 64) continue;
                     if (c0 + 32 <= BN) tmem_add32(ta, acc[j]);
                     else if (c0 + 16 <= BN) tmem_add16(ta, acc[j]);
                 }
@@ -449,16 +509,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int row = r0 + lane;
             const bool row_ok = row < p.M;
             double part = 0.0;
-            if (tma_epi && e_bytes) {
-                mbar_wait(&S.ebar[ew], e_ph);
-                e_ph ^= 1;
+            if (tma_epi) {
 #pragma unroll
                 for (int j = 0; j < EPI_CH; ++j) {
+                    if (!chunk_bytes(j)) continue;
+                    if (j > 0) {
+                        if (lane == 0) fetch(j, n0, r0);
+                        __syncwarp();
+                    }
+                    mbar_wait_sleep(&S.ebar[ew], e_ph);
+                    e_ph ^= 1;
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         const int c0 = 32 * (cg + EPI_PER_Q * j) + 16 * hh;
                         if (c0 + 16 > BN) continue;
-                        unsigned char *tb = etile + j * EPI_TILE_BYTES + hh * EPI_SUB_BYTES;
+                        unsigned char *tb = etile + hh * EPI_SUB_BYTES;
+                        float lsum = 0.f;   // sum over the sub-tile's 16 columns of V log2 V_hat
 #pragma unroll
                         for (int i4 = 0; i4 < 4; ++i4) {
                             float4 *px = reinterpret_cast<float4 *>(tb + swz64(lane, i4));
@@ -471,11 +537,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                 if (p.mode == TC_BACKPROJ) {
                                     y[e] = xv[e] * vh;                       // n = theta .* (R beta)
                                 } else {
-                                    y[e] = 0.f;                              // R = V / V_hat
+                                    // R = V / V_hat: correctly rounded reciprocal times V (<= 1.5 ulp
+                                    // of the quotient); log2 on the SFU, scaled by ln 2 per sub-tile
+                                    float rc = __frcp_rn(vh);
+                                    y[e] = 0.f;
                                     if (xv[e] > 0.f) {
                                         if (vh > 0.f) {
-                                            y[e] = xv[e] / vh;
-                                            part += (double)xv[e] * (double)logf(vh);
+                                            y[e] = xv[e] * rc;
+                                            lsum = fmaf(xv[e], __log2f(vh), lsum);
                                         } else {
                                             bad |= FLAG_ZERO_SUPPORT;
                                         }
@@ -484,6 +553,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             }
                             *px = make_float4(y[0], y[1], y[2], y[3]);
                         }
+                        part += 0.69314718055994530942 * (double)lsum;
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
@@ -594,12 +664,15 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
     }
     const int n_total = ((p.M + TC_BM - 1) / TC_BM) * p.n_tiles;
     const int grid = n_total < g_num_sms ? n_total : g_num_sms;
-    static int dbg = -1;
+    static int dbg = -1, chunk = CHUNK_KB;
     if (dbg < 0) {
         const char *ev = getenv("NFHMM_TC_DEBUG");
         dbg = ev ? atoi(ev) : 0;
+        const char *ec = getenv("NFHMM_TC_CHUNK");   // accuracy / speed experiments only
+        if (ec && atoi(ec) > 0) chunk = atoi(ec);
     }
     p.dbg = dbg;
+    p.chunk_kb = chunk;
     tc_gemm_kernel<<<grid, TC_THREADS, smem, st>>>(mA, mIn, mOut, p);
     return cudaGetLastError();
 }
