@@ -85,6 +85,31 @@ __global__ void obs_stats_kernel(const float *__restrict__ V, int frames, int F,
 }
 
 // scale_t = v_t / alpha_0 (posterior mean E[theta] = alpha / alpha_0, DESIGN R9; v_t from S:408).
+__device__ double digamma_fp64(double x) {
+    double r = 0.0;
+    while (x < 10.0) {
+        r -= 1.0 / x;
+        x += 1.0;
+    }
+    const double f = 1.0 / (x * x);
+    const double t = f * (-1.0 / 12 + f * (1.0 / 120 + f * (-1.0 / 252 + f * (1.0 / 240 + f * (-1.0 / 132 +
+                     f * (691.0 / 32760 + f * (-1.0 / 12)))))));
+    return r + log(x) - 0.5 / x + t;
+}
+
+// alpha_0 = v_t + Kt + gamma S K (Eq. 6 summed over k; DESIGN R19) and the frame's scalar bound terms
+__global__ void frame_consts_kernel(const float *__restrict__ vt, int frames, int Kt, double gamma, int S, int K,
+                                    double *fc) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= frames) return;
+    const double a0 = (double)vt[f] + (double)Kt + gamma * (double)S * (double)K;
+    const double psi0 = digamma_fp64(a0);
+    fc[4 * (size_t)f + 0] = a0;
+    fc[4 * (size_t)f + 1] = psi0;
+    fc[4 * (size_t)f + 2] = -a0 - lgamma(a0) + (a0 - (double)Kt) * psi0;
+    fc[4 * (size_t)f + 3] = exp(-psi0);
+}
+
 __global__ void sep_scale_kernel(const float *__restrict__ alpha, int frames, int Kt, int ld, const float *vt, float *scale) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= frames) return;
@@ -143,6 +168,12 @@ cudaError_t launch_transpose(const float *src, int rows, int cols, int ld_src, f
 
 cudaError_t launch_obs_stats(const float *V, int frames, int F, int ld, float *vt, unsigned *flags, cudaStream_t st) {
     obs_stats_kernel<<<(frames * 32 + 255) / 256, 256, 0, st>>>(V, frames, F, ld, vt, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_frame_consts(const float *vt, int frames, int Kt, double gamma, int S, int K, double *fc,
+                                cudaStream_t st) {
+    frame_consts_kernel<<<(frames + 127) / 128, 128, 0, st>>>(vt, frames, Kt, gamma, S, K, fc);
     return cudaGetLastError();
 }
 

@@ -33,6 +33,7 @@ struct nfhmm {
     float *vt = nullptr, *scale = nullptr, *vsrc = nullptr;
     float *bs_a = nullptr, *bs_b = nullptr;   // tensor-core path: pre-split beta for (a) and betaT for (b)
     double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
+    double *fconst = nullptr;   // per-frame alpha_0, psi(alpha_0), bound constant (set_observations)
     unsigned *flags = nullptr;
 
     bool have_model = false, have_obs = false, R_valid = false;
@@ -147,6 +148,7 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take((size_t)h->M * h->S * 8);           h->logZ = (double *)p;
     p = take(fr * (size_t)(h->nt_a > h->nt_tc_a ? h->nt_a : h->nt_tc_a) * 8); h->data_part = (double *)p;
     p = take(fr * 8);                            h->hdir = (double *)p;
+    p = take(fr * 4 * 8);                        h->fconst = (double *)p;
     p = take((size_t)h->M * h->max_iters * 8);   h->fe = (double *)p;
     p = take(fr * 4);                            h->vt = (float *)p;
     p = take(fr * 4);                            h->scale = (float *)p;
@@ -234,7 +236,7 @@ int step_backproj(nfhmm_t *h) {
 }
 
 // (c)+(d) Eq. 6, digamma/exp, Eq. 8
-int step_dirichlet(nfhmm_t *h) {
+int step_dirichlet(nfhmm_t *h, bool write_alpha) {
     DirichletArgs d{};
     d.frames = (int)h->frames;
     d.T = (int)h->T;
@@ -250,7 +252,8 @@ int step_dirichlet(nfhmm_t *h) {
     d.d_hat = h->dhat;
     d.ec = h->ec;
     d.eoff = h->eoff;
-    d.vt = h->vt;
+    d.fconst = h->fconst;
+    d.write_alpha = write_alpha ? 1 : 0;
     d.hdir = h->free_energy ? h->hdir : nullptr;
     d.flags = h->flags;
     LAUNCH(h, NFHMM_K_DIRICHLET, launch_dirichlet(d, h->st));
@@ -277,14 +280,15 @@ int step_fb(nfhmm_t *h) {
     return NFHMM_OK;
 }
 
-int sweep(nfhmm_t *h) {
+// One VB sweep.  `last`: the final sweep of this call, which also stores alpha (posteriors, separation).
+int sweep(nfhmm_t *h, bool last) {
     if (!h->R_valid) {
         int r = recon_ratio(h);
         if (r) return r;
         h->R_valid = true;
     }
     int r = step_backproj(h);
-    if (!r) r = step_dirichlet(h);
+    if (!r) r = step_dirichlet(h, last);
     if (!r) r = step_fb(h);
     if (r) return r;
     // (a) z-step of the new alpha: R for the next sweep and the data term of L_i
@@ -505,6 +509,7 @@ int nfhmm_set_observations(nfhmm_t *h, const float *V) {
     CU(h, cudaMemcpy2DAsync(h->V, (size_t)h->Fa * 4, V, (size_t)h->F * 4, (size_t)h->F * 4, (size_t)h->frames,
                             cudaMemcpyDefault, h->st));
     LAUNCH(h, NFHMM_K_OTHER, launch_obs_stats(h->V, (int)h->frames, (int)h->F, h->Fa, h->vt, h->flags, h->st));
+    LAUNCH(h, NFHMM_K_OTHER, launch_frame_consts(h->vt, (int)h->frames, h->Kt, h->gamma, h->S, h->K, h->fconst, h->st));
     h->have_obs = true;
     return nfhmm_reset(h);
 }
@@ -515,7 +520,7 @@ int nfhmm_vb_iterate_async(nfhmm_t *h, int32_t n_iters) {
     if (n_iters < 0) return fail(h, NFHMM_EINVAL, "n_iters < 0");
     if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
     for (int i = 0; i < n_iters; ++i) {
-        r = sweep(h);
+        r = sweep(h, i == n_iters - 1);
         if (r) return r;
     }
     return NFHMM_OK;
@@ -645,7 +650,7 @@ int nfhmm_bench_kernel(nfhmm_t *h, int cls, int32_t reps, double *ms_per_launch)
         switch (cls) {
             case NFHMM_K_RECON: r = recon_ratio(h); break;
             case NFHMM_K_BACKPROJ: r = step_backproj(h); break;
-            case NFHMM_K_DIRICHLET: r = step_dirichlet(h); break;
+            case NFHMM_K_DIRICHLET: r = step_dirichlet(h, true); break;
             default: r = step_fb(h); break;
         }
     }

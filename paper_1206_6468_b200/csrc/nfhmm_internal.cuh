@@ -76,7 +76,9 @@ struct DirichletArgs {
     float *alpha;             // [frames][ld]  out: alpha (may alias n_in)
     float *theta;             // [frames][ld]  out: exp(psi(alpha) - psi(alpha_0))
     const float *d_hat;       // [M][S][T][N]  previous q(D) marginals
-    const float *vt;          // [frames]      v_t = sum_l V[t,l]
+    const double *fconst;     // [frames][4]   alpha_0, psi(alpha_0), -alpha_0 - lnG(alpha_0) + (alpha_0 - Kt) psi(alpha_0),
+                              //               e^{-psi(alpha_0)}
+    int write_alpha;          // 1: store alpha (last sweep of a call); 0: only theta / e (alpha is not read in the loop)
     float *ec;                // [M][S][T][N]  out: emission exp(gamma*(phi - max_n phi)) in (0, 1]
     double *eoff;             // [M][S][T]     out: gamma * max_n phi (FP64)
     double *hdir;             // [frames]      out: Dirichlet entropy terms of the bound (or NULL)
@@ -118,6 +120,11 @@ cudaError_t launch_transpose(const float *src, int rows, int cols, int ld_src, f
 // Observation checks + per-frame row sums v_t (FP32 exact for integer counts; FP64 accumulate).
 cudaError_t launch_obs_stats(const float *V, int frames, int F, int ld, float *vt, unsigned *flags,
                              cudaStream_t st);
+// Per-frame constants of the Dirichlet step (DESIGN R19: alpha_0 = v_t + Kt + gamma S K is the same in
+// every sweep): fc[4f] = alpha_0, fc[4f+1] = psi(alpha_0), fc[4f+2] = -alpha_0 - lnG(alpha_0) + (alpha_0 - Kt)
+// psi(alpha_0), fc[4f+3] = e^{-psi(alpha_0)} (FP64).
+cudaError_t launch_frame_consts(const float *vt, int frames, int Kt, double gamma, int S, int K, double *fc,
+                                cudaStream_t st);
 // Per-row scale v_t / alpha_0 for separation.
 cudaError_t launch_sep_scale(const float *alpha, int frames, int Kt, int ld, const float *vt, float *scale,
                              cudaStream_t st);
