@@ -98,10 +98,23 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     const int m = f / p.T, t = f - m * p.T;
     const float gamma = p.gamma;
 
-    // per-block prior pseudo-counts gamma d + 1 of Eq. 6 (d of the previous sweep, one row of N per source)
+    // per-block prior pseudo-counts gamma d + 1 of Eq. 6: d of the previous sweep = the FB's unnormalised
+    // q_{s,t} divided by its sum over n (one row of N per source)
+    unsigned bad = 0;
     for (int s = 0; s < p.S; ++s) {
         const float *src = p.d_hat + ((size_t)(m * p.S + s) * p.T + t) * p.N;
-        for (int n = lane; n < p.N; n += 32) dvs[s * p.N + n] = fmaf(gamma, src[n], 1.f);
+        float qs = 0.f;
+        for (int n = lane; n < p.N; n += 32) {
+            const float v = src[n];
+            dvs[s * p.N + n] = v;
+            qs += v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, o);
+        if (!(qs > 0.f) || !(qs < INFINITY)) bad |= FLAG_NONFINITE;
+        const float gq = gamma / qs;
+        __syncwarp();
+        for (int n = lane; n < p.N; n += 32) dvs[s * p.N + n] = fmaf(gq, dvs[s * p.N + n], 1.f);
     }
     const double psi0 = p.fconst[4 * (size_t)f + 1];
     const float e0 = (float)p.fconst[4 * (size_t)f + 3];   // e^{-psi(alpha_0)}
@@ -113,7 +126,6 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     float4 *tout = reinterpret_cast<float4 *>(p.theta + (size_t)f * p.ld);
     const bool want_h = p.hdir != nullptr, want_a = p.write_alpha != 0;
     float hg = 0.f;   // sum of g~ over this lane's elements
-    unsigned bad = 0;
     for (int c0 = 0; c0 < p.Kt; c0 += CK) {
         const int cn = min(CK, p.Kt - c0), b0 = c0 / K;
         // flat, coalesced pass over the chunk: alpha, psi, theta, g~ per element (independent -> ILP);

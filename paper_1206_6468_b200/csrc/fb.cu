@@ -1,22 +1,28 @@
 // fb.cu -- kernel (e): scaled forward-backward per source chain, batched over all mixtures.
 //
 // q(D^(s)) is the chain posterior with log-likelihood gamma * phi (DESIGN R1).  One warp
-// per chain (m, s); lane l owns states j = l + 32 q (q < NQ).  The recursion is latency-bound (2T
-// dependent steps per chain), so a step is kept to: broadcast the previous message through shared
-// memory (128-bit loads) -> fully unrolled dot products -> one multiply -> store.
-//   * A_s (row-stochastic, A[i][j] = P(j | i), DESIGN R4) lives in REGISTERS for N <= 64 (lane j holds
-//     column j for the forward pass, row j for the backward pass), zero-padded to a compile-time NMAX;
-//     for 64 < N <= 128 it is read from shared memory in the same unrolled pattern.
-//   * Scaling is by exact powers of two (no division, no FP64, no warp reduction on the critical path):
-//     every lane also sums the broadcast message it just loaded, and the next message is multiplied by
-//     2^-E with E the binary exponent of that sum.  Forward:
-//       u_0 = pi .* e_0;   u_t = ((u_{t-1} A) .* e_t) 2^-E_t,  E_t = exponent(sum u_{t-1});
-//       a_t = u_t / sum u_t (stored, off the critical path);
-//       log Z = ln(sum u_{T-1}) + ln 2 * sum_t E_t + sum_t eoff_t   (FP64, after the loop).
-//     Backward: b_{T-1} = 1;  b_t = (A (e_{t+1} .* b_{t+1})) 2^-E'_t;  d_t = a_t .* b_t / sum(a_t .* b_t).
-//   * Emissions e = exp(gamma (phi - max_n phi)) in (0, 1] come precomputed from the Dirichlet kernel;
-//     the eoff are their FP64 per-frame offsets.  Inputs for the next CH steps are staged into shared
-//     memory with cp.async (double-buffered chunks).
+// per chain (m, s).  The recursion is latency-bound (2T dependent steps per chain), so one step is kept
+// to: broadcast the previous message through shared memory (128-bit loads) -> unrolled dot products ->
+// one multiply -> store, with the dot products and the running sum in packed FP32 pairs (FFMA2 / FADD2).
+//
+// State ownership (NMAX = N rounded up): lane l owns states 32 q + l, q < ceil(NMAX / 32), and computes
+// their full dot products with packed FP32 pairs (for N = 40: 2 x 20 FFMA2 per lane per step).  A build
+// option (NFHMM_FB_SPLIT=1) instead splits the NMAX % 32 remainder states over lane groups with a
+// butterfly: fewer FMAs, but the two shuffles on the critical path made the step ~1.7x slower (measured).
+//   A_s (row-stochastic, A[i][j] = P(j | i), DESIGN R4) lives in REGISTERS when it fits (columns for the
+//   forward pass, rows for the backward pass), else is read from shared memory in the same pattern.
+// Scaling by exact powers of two (no division, no FP64, no warp reduction on the critical path): every
+// lane also sums the broadcast vector it loads, and the next message is multiplied by 2^-E with E the
+// binary exponent of that sum:
+//   u_0 = pi .* e_0;   u_t = ((u_{t-1} A) .* e_t) 2^-E_t,  E_t = exponent(sum u_{t-1});
+//   log Z = ln(sum u_{T-1}) + ln 2 * sum_t E_t + sum_t eoff_t   (FP64, after the loop).
+//   b_{T-1} = 1;  x_t = e_{t+1} .* b_{t+1};  b_t = (A x_t) 2^-E'_t,  E'_t = exponent(sum x_t);
+//   d_t = q_t / sum_n q_t with q_t = u_t .* b_t: the forward messages are stored unnormalised (their
+//   per-t normalisation cancels in d_t), and q_t itself is stored unnormalised -- the Dirichlet kernel
+//   and nfhmm_posteriors divide by the per-(s, t) sum, keeping every warp reduction out of this loop.
+// Emissions e = exp(gamma (phi - max_n phi)) in (0, 1] come precomputed from the Dirichlet kernel; eoff
+// are their FP64 per-frame offsets.  Inputs for the next CH steps are staged into shared memory with
+// cp.async (double-buffered chunks).
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -26,12 +32,23 @@ namespace nfk {
 
 namespace {
 
+__host__ __device__ constexpr int pow2ceil(int x) { return x <= 1 ? x : 2 * pow2ceil((x + 1) / 2); }
+
+#ifndef NFHMM_FB_SPLIT
+#define NFHMM_FB_SPLIT 0   // 1: split the remainder states over lane groups (butterfly); 0: one more round
+#endif
 template <int NMAX>
 struct FBCfg {
-    static constexpr int WPB = NMAX <= 64 ? 4 : 2;  // chains (warps) per CTA, sharing the CTA's copy of A_s
-    static constexpr int NQ = (NMAX + 31) / 32;
-    static constexpr bool REG = NMAX <= 64;        // A in registers
-    static constexpr int CH = NMAX <= 64 ? 32 : 16; // time steps per staged chunk
+    static constexpr int NQ = NFHMM_FB_SPLIT ? NMAX / 32 : (NMAX + 31) / 32;   // rounds of 32 states
+    static constexpr int REM = NFHMM_FB_SPLIT ? NMAX % 32 : 0;                // remainder states
+    static constexpr int REMP = pow2ceil(REM);               // 0, 1, 2, 4, 8, 16, 32
+    static constexpr int G = REMP ? 32 / REMP : 1;           // lanes per remainder state
+    static constexpr int SEG = REMP ? ((NMAX + G - 1) / G + 3) / 4 * 4 : 0;   // inputs per lane (x4)
+    static constexpr int NB = (NMAX > G * SEG ? NMAX : G * SEG);            // broadcast buffer length
+    static constexpr int NBP = (NB + 3) / 4 * 4;
+    static constexpr bool REG = NQ * NMAX + SEG <= 96;       // A in registers
+    static constexpr int WPB = REG ? 4 : 2;                  // chains (warps) per CTA
+    static constexpr int CH = NMAX <= 64 ? 32 : 16;          // time steps per staged chunk
 };
 
 __device__ __forceinline__ void cp_async4(float *smem_dst, const float *gsrc) {
@@ -59,54 +76,101 @@ __device__ __forceinline__ float warp_sum(float v) {
 __device__ __forceinline__ int exponent_of(float x) { return (int)((__float_as_uint(x) >> 23) & 0xFF) - 127; }
 __device__ __forceinline__ float pow2_neg(int E) { return __uint_as_float((uint32_t)(127 - E) << 23); }
 
-// acc[q] = sum_i x[i] * M(i, j_q) over i < NMAX with x broadcast from shared memory (zero-padded), and
-// xsum = sum_i x[i] (every lane computes it from the values it loaded).
-template <int NMAX, int RQ, int RN>
-__device__ __forceinline__ void dot_bcast(float (&acc)[FBCfg<NMAX>::NQ], float &xsum, const float *x,
-                                          const float (&reg)[RQ][RN], const float *Ms,
-                                          const int (&js)[FBCfg<NMAX>::NQ]) {
-    constexpr int NQ = FBCfg<NMAX>::NQ;
-    float a[NQ][4];
-    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+// Packed FP32 pairs (sm_100 FFMA2 / FADD2: two FP32 lanes per instruction, each IEEE round-to-nearest).
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void fma2(uint64_t &d, uint64_t a, uint64_t b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void add2(uint64_t &d, uint64_t a) { asm("add.rn.f32x2 %0, %1, %0;" : "+l"(d) : "l"(a)); }
+__device__ __forceinline__ float hsum2(uint64_t v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return a + b;
+}
+
+// One message step's products.  x: broadcast vector in shared memory (NBP floats, zero-padded).
+//   main[q] = sum_i x[i] M(i, 32 q + lane)                (q < NQ)
+//   ext     = sum_i x[i] M(i, 32 NQ + lane / G), butterflied over the lane's group of G
+//   xsum    = sum_i x[i]  (every lane, from the values it loads: no shuffle chain on the critical path)
+// M(i, j) for the main states: packed register pairs Mr[q][i/2] = (M(i, j), M(i+1, j)) or shared Ms[i *
+// NMAX + j]; for the remainder state's segment i = g SEG + i': Me[i'/2].
+template <int NMAX>
+__device__ __forceinline__ void step_products(float (&main)[FBCfg<NMAX>::NQ ? FBCfg<NMAX>::NQ : 1], float &ext, float &xsum,
+                                              const float *x, const uint64_t (&Mr)[FBCfg<NMAX>::REG ? FBCfg<NMAX>::NQ + 1 : 1][FBCfg<NMAX>::REG ? NMAX / 2 : 1],
+                                              const uint64_t (&Me)[FBCfg<NMAX>::SEG ? FBCfg<NMAX>::SEG / 2 : 1], const float *Ms,
+                                              int lane, int g) {
+    using C = FBCfg<NMAX>;
+    constexpr int NQ = C::NQ;
+    {
+        uint64_t a[NQ ? NQ : 1][2];
+        uint64_t s2[2] = {0ull, 0ull};
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) a[q][0] = a[q][1] = a[q][2] = a[q][3] = 0.f;
-    const float4 *x4 = reinterpret_cast<const float4 *>(x);
+        for (int q = 0; q < NQ; ++q) a[q][0] = a[q][1] = 0ull;
+        const ulonglong2 *x4 = reinterpret_cast<const ulonglong2 *>(x);
 #pragma unroll
-    for (int i4 = 0; i4 < NMAX / 4; ++i4) {
-        const float4 v = x4[i4];
-        const float xv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int i = 4 * i4 + r;
-            s4[r] += xv[r];
+        for (int i4 = 0; i4 < NMAX / 4; ++i4) {
+            const ulonglong2 v = x4[i4];   // (x[4i4], x[4i4+1]) | (x[4i4+2], x[4i4+3])
+            add2(s2[0], v.x);
+            add2(s2[1], v.y);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const float m = FBCfg<NMAX>::REG ? reg[RQ > 1 ? q : 0][RN > 1 ? i : 0] : Ms[i * NMAX + js[q]];
-                a[q][r] = fmaf(xv[r], m, a[q][r]);
+                uint64_t m0, m1;
+                if (C::REG) {
+                    m0 = Mr[C::REG ? q : 0][C::REG ? 2 * i4 : 0];
+                    m1 = Mr[C::REG ? q : 0][C::REG ? 2 * i4 + 1 : 0];
+                } else {
+                    const int j = min(32 * q + lane, NMAX - 1), i = 4 * i4;   // (lanes past NMAX: discarded)
+                    m0 = pk2(Ms[i * NMAX + j], Ms[(i + 1) * NMAX + j]);
+                    m1 = pk2(Ms[(i + 2) * NMAX + j], Ms[(i + 3) * NMAX + j]);
+                }
+                fma2(a[q][0], v.x, m0);
+                fma2(a[q][1], v.y, m1);
             }
         }
-    }
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) acc[q] = (a[q][0] + a[q][1]) + (a[q][2] + a[q][3]);
-    xsum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        for (int q = 0; q < NQ; ++q) {
+            add2(a[q][0], a[q][1]);
+            main[q] = hsum2(a[q][0]);
+        }
+        add2(s2[0], s2[1]);
+        xsum = hsum2(s2[0]);
+    }
+    ext = 0.f;
+    if (C::SEG > 0) {
+        uint64_t b2[2] = {0ull, 0ull};
+        const ulonglong2 *xs = reinterpret_cast<const ulonglong2 *>(x + g * C::SEG);
+#pragma unroll
+        for (int i4 = 0; i4 < C::SEG / 4; ++i4) {
+            const ulonglong2 v = xs[i4];
+            fma2(b2[0], v.x, Me[C::SEG ? 2 * i4 : 0]);
+            fma2(b2[1], v.y, Me[C::SEG ? 2 * i4 + 1 : 0]);
+        }
+        add2(b2[0], b2[1]);
+        ext = hsum2(b2[0]);
+#pragma unroll
+        for (int o = 1; o < C::G; o <<= 1) ext += __shfl_xor_sync(0xffffffffu, ext, o);
+    }
 }
 
 template <int NMAX>
 __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
-    constexpr int WPB = FBCfg<NMAX>::WPB;
-    constexpr int NQ = FBCfg<NMAX>::NQ;
-    constexpr int CH = FBCfg<NMAX>::CH;
-    constexpr bool REG = FBCfg<NMAX>::REG;
+    using C = FBCfg<NMAX>;
+    constexpr int WPB = C::WPB, NQ = C::NQ, CH = C::CH, G = C::G, SEG = C::SEG, NBP = C::NBP;
+    constexpr bool REG = C::REG;
     extern __shared__ __align__(16) float sm[];
     const int N = p.N;
     float *As = sm;                       // [NMAX][NMAX]  As[i][j] = A[i][j]  (zero-padded)
     float *AT = As + NMAX * NMAX;         // [NMAX][NMAX]  AT[j][i] = A[i][j]
     float *wbase = AT + NMAX * NMAX;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // per warp: u[2][NMAX] | e chunks [2][CH][N] | a chunks [2][CH][N]
-    const int per_warp = 2 * NMAX + 4 * CH * N;
+    // per warp: u[2][NBP] | e chunks [2][CH][N] | u chunks [2][CH][N]
+    const int per_warp = 2 * NBP + 4 * CH * N;
     float *ubuf = wbase + warp * per_warp;
-    float *ech = ubuf + 2 * NMAX;
+    float *ech = ubuf + 2 * NBP;
     float *ach = ech + 2 * CH * N;
 
     const int s = blockIdx.y;
@@ -118,7 +182,7 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
         As[idx] = v;
         AT[c * NMAX + r] = v;
     }
-    for (int idx = lane; idx < 2 * NMAX; idx += 32) ubuf[idx] = 0.f;
+    for (int idx = lane; idx < 2 * NBP; idx += 32) ubuf[idx] = 0.f;
     __syncthreads();
     if (m >= p.M) return;
 
@@ -129,25 +193,39 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
     float *dh = p.d_hat + chain * T * N;
     unsigned bad = 0;
 
-    int js[NQ];
-    bool jv[NQ];
+    // owned states: main js[q] = 32 q + lane; remainder jx = 32 NQ + lane / G (group member g)
+    const int g = lane % G;
+    const int jx = 32 * NQ + lane / G;
+    const bool xv_ok = SEG > 0 && jx < N, x_lead = xv_ok && g == 0;
+    bool jv[NQ ? NQ : 1];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        js[q] = lane + 32 * q;
-        jv[q] = js[q] < N;
-    }
-    float Areg[REG ? NQ : 1][REG ? NMAX : 1];
-    if (REG) {   // forward: column j_q of A
+    for (int q = 0; q < NQ; ++q) jv[q] = 32 * q + lane < N;
+
+    uint64_t Mr[REG ? NQ + 1 : 1][REG ? NMAX / 2 : 1];
+    uint64_t Me[SEG ? SEG / 2 : 1];
+    auto load_regs = [&](const float *M) {   // M[i * NMAX + j]: column j of M for the lane's states, in pairs
+        if (REG) {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
+            for (int q = 0; q < NQ; ++q)
 #pragma unroll
-            for (int i = 0; i < NMAX; ++i) Areg[q][i] = js[q] < NMAX ? As[i * NMAX + js[q]] : 0.f;
-    }
+                for (int i = 0; i < NMAX; i += 2)
+                    Mr[REG ? q : 0][REG ? i / 2 : 0] = 32 * q + lane < NMAX
+                        ? pk2(M[i * NMAX + 32 * q + lane], M[(i + 1) * NMAX + 32 * q + lane]) : 0ull;
+        }
+#pragma unroll
+        for (int i = 0; i < SEG; i += 2) {
+            const int ii = g * SEG + i;
+            const float m0 = (ii < NMAX && jx < NMAX) ? M[ii * NMAX + jx] : 0.f;
+            const float m1 = (ii + 1 < NMAX && jx < NMAX) ? M[(ii + 1) * NMAX + jx] : 0.f;
+            Me[SEG ? i / 2 : 0] = pk2(m0, m1);
+        }
+    };
+    load_regs(As);   // forward: columns of A
 
     // ---------------- forward ----------------
     const int nch = (T + CH - 1) / CH;
     stage_rows(ech, em, N, 0, min(CH, T), lane);
-    float u[NQ];
+    float u[NQ ? NQ : 1], ux = 0.f;
     int esum = 0;            // sum of the power-of-two scale exponents applied
     for (int c = 0; c < nch; ++c) {
         const int t0 = c * CH, n = min(CH, T - t0);
@@ -157,47 +235,49 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
         if (c + 1 < nch) stage_rows(ech + ((c + 1) & 1) * CH * N, em, N, t0 + CH, min(CH, T - t0 - CH), lane);
         for (int tt = 0; tt < n; ++tt) {
             const int t = t0 + tt;
+            const float *et = ecur + tt * N;
             if (t == 0) {
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? p.prior[s * N + js[q]] * ecur[js[q]] : 0.f;
+                for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * et[32 * q + lane] : 0.f;
+                ux = xv_ok ? p.prior[s * N + jx] * et[jx] : 0.f;
             } else {
-                float acc[NQ], sprev;
-                dot_bcast<NMAX>(acc, sprev, ubuf + ((t - 1) & 1) * NMAX, Areg, As, js);
-                if (!(sprev > 0.f) || !(sprev < INFINITY)) bad |= FLAG_NONFINITE;
-                const int E = exponent_of(sprev);
+                float acc[NQ ? NQ : 1], accx, usum;
+                step_products<NMAX>(acc, accx, usum, ubuf + ((t - 1) & 1) * NBP, Mr, Me, As, lane, g);
+                if (!(usum > 0.f) || !(usum < INFINITY)) bad |= FLAG_NONFINITE;
+                const int E = exponent_of(usum);
                 const float sc = pow2_neg(E);
                 esum += E;
-                // off the critical path: the normalised message a_{t-1} for the backward pass
-                const float inv = 1.f / sprev;
 #pragma unroll
-                for (int q = 0; q < NQ; ++q)
-                    if (jv[q]) fwd[(size_t)(t - 1) * N + js[q]] = u[q] * inv;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? acc[q] * ecur[tt * N + js[q]] * sc : 0.f;
+                for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? acc[q] * et[32 * q + lane] * sc : 0.f;
+                ux = xv_ok ? accx * et[jx] * sc : 0.f;
             }
-            float *un = ubuf + (t & 1) * NMAX;
+            float *un = ubuf + (t & 1) * NBP;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q)
-                if (jv[q]) un[js[q]] = u[q];
+            for (int q = 0; q < NQ; ++q) {
+                if (jv[q]) {
+                    un[32 * q + lane] = u[q];
+                    fwd[(size_t)t * N + 32 * q + lane] = u[q];
+                }
+            }
+            if (x_lead) {
+                un[jx] = ux;
+                fwd[(size_t)t * N + jx] = ux;
+            }
             __syncwarp();
         }
     }
-    {   // last message and log Z
-        float ps = 0.f;
+    {   // log Z
+        float part = x_lead ? ux : 0.f;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) ps += u[q];
-        const float sl = warp_sum(ps);
-        if (!(sl > 0.f) || !(sl < INFINITY)) bad |= FLAG_NONFINITE;
-        const float inv = 1.f / sl;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-            if (jv[q]) fwd[(size_t)(T - 1) * N + js[q]] = u[q] * inv;
+        for (int q = 0; q < NQ; ++q) part += u[q];
+        const float usum = warp_sum(part);
+        if (!(usum > 0.f) || !(usum < INFINITY)) bad |= FLAG_NONFINITE;
         double offsum = 0.0;   // lane-parallel, fixed order
         for (int t = lane; t < T; t += 32) offsum += p.eoff[chain * T + t];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) offsum += __shfl_xor_sync(0xffffffffu, offsum, o);
         if (lane == 0) {
-            const double lz = log((double)sl) + (double)esum * 0.69314718055994530942 + offsum;
+            const double lz = log((double)usum) + (double)esum * 0.69314718055994530942 + offsum;
             p.logZ[chain] = lz;
             if (!isfinite(lz)) bad |= FLAG_NONFINITE;
         }
@@ -206,16 +286,11 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
     __syncwarp();
 
     // ---------------- backward ----------------
-    if (REG) {   // backward: row j_q of A  (b_t[j] = sum_k A[j][k] x[k])
+    load_regs(AT);   // backward: b_t[j] = sum_k A[j][k] x[k] = sum_k AT[k][j] x[k]
+    float b[NQ ? NQ : 1], bx = xv_ok ? 1.f : 0.f;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-#pragma unroll
-            for (int k = 0; k < NMAX; ++k) Areg[q][k] = js[q] < NMAX ? AT[k * NMAX + js[q]] : 0.f;
-    }
-    float b[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) b[q] = 1.f;
-    // chunk c covers t in [t0, t0 + n), processed in descending t; needs e_{t+1} and a_t
+    for (int q = 0; q < NQ; ++q) b[q] = jv[q] ? 1.f : 0.f;
+    // chunk c covers t in [t0, t0 + n), processed in descending t; needs e_{t+1} and u_t
     auto stage_back = [&](int cc, int buf) {
         const int t0 = cc * CH, n = min(CH, T - t0);
         stage_rows(ach + buf * CH * N, fwd, N, t0, n, lane);
@@ -234,32 +309,28 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
         for (int tt = n - 1; tt >= 0; --tt) {
             const int t = t0 + tt;
             if (t < T - 1) {
-                float *xb = ubuf + (t & 1) * NMAX;
+                const float *en = ecur + tt * N;
+                float *xb = ubuf + (t & 1) * NBP;
 #pragma unroll
                 for (int q = 0; q < NQ; ++q)
-                    if (jv[q]) xb[js[q]] = ecur[tt * N + js[q]] * b[q];
+                    if (jv[q]) xb[32 * q + lane] = en[32 * q + lane] * b[q];
+                if (x_lead) xb[jx] = en[jx] * bx;
                 __syncwarp();
-                float acc[NQ], xs;
-                dot_bcast<NMAX>(acc, xs, xb, Areg, AT, js);
-                if (!(xs > 0.f) || !(xs < INFINITY)) bad |= FLAG_NONFINITE;
-                const float sc = pow2_neg(exponent_of(xs));
+                float acc[NQ ? NQ : 1], accx, xsum;
+                step_products<NMAX>(acc, accx, xsum, xb, Mr, Me, AT, lane, g);
+                if (!(xsum > 0.f) || !(xsum < INFINITY)) bad |= FLAG_NONFINITE;
+                const float sc = pow2_neg(exponent_of(xsum));
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) b[q] = acc[q] * sc;
+                for (int q = 0; q < NQ; ++q) b[q] = jv[q] ? acc[q] * sc : 0.f;
+                bx = xv_ok ? accx * sc : 0.f;
             }
-            // off the critical path: d_t = a_t .* b_t / sum
-            float dv[NQ];
-            float ps = 0.f;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                dv[q] = jv[q] ? acur[tt * N + js[q]] * b[q] : 0.f;
-                ps += dv[q];
-            }
-            const float z = warp_sum(ps);
-            const float iz = 1.f / z;
-            if (!(z > 0.f)) bad |= FLAG_NONFINITE;
+            // q_t = u_t .* b_t, stored UNnormalised: its consumers (the Dirichlet kernel, posteriors)
+            // divide by sum_n q_t (keeps the warp reduction off this latency-bound loop)
+            const float *ut = acur + tt * N;
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
-                if (jv[q]) dh[(size_t)t * N + js[q]] = dv[q] * iz;
+                if (jv[q]) dh[(size_t)t * N + 32 * q + lane] = ut[32 * q + lane] * b[q];
+            if (x_lead) dh[(size_t)t * N + jx] = ut[jx] * bx;
         }
     }
     if (bad) atomicOr(p.flags, bad);
@@ -267,18 +338,17 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
 
 template <int NMAX>
 cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
+    using C = FBCfg<NMAX>;
     const int N = a.N;
-    constexpr int CH = FBCfg<NMAX>::CH;
-    constexpr int WPB = FBCfg<NMAX>::WPB;
-    const size_t smem = ((size_t)2 * NMAX * NMAX + (size_t)WPB * (2 * NMAX + 4 * CH * N)) * sizeof(float);
+    const size_t smem = ((size_t)2 * NMAX * NMAX + (size_t)C::WPB * (2 * C::NBP + 4 * C::CH * N)) * sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && attr < smem) {
         cudaError_t e = cudaFuncSetAttribute(fb_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    dim3 grid((a.M + WPB - 1) / WPB, a.S);
-    fb_kernel<NMAX><<<grid, WPB * 32, smem, st>>>(a);
+    dim3 grid((a.M + C::WPB - 1) / C::WPB, a.S);
+    fb_kernel<NMAX><<<grid, C::WPB * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -286,6 +356,7 @@ cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
 
 cudaError_t launch_fb(const FBArgs &a, cudaStream_t st) {
     const int N = a.N;
+    if (N <= 4) return launch_fb_t<4>(a, st);
     if (N <= 8) return launch_fb_t<8>(a, st);
     if (N <= 16) return launch_fb_t<16>(a, st);
     if (N <= 24) return launch_fb_t<24>(a, st);
@@ -294,6 +365,7 @@ cudaError_t launch_fb(const FBArgs &a, cudaStream_t st) {
     if (N <= 48) return launch_fb_t<48>(a, st);
     if (N <= 64) return launch_fb_t<64>(a, st);
     if (N <= 96) return launch_fb_t<96>(a, st);
+    if (N <= 104) return launch_fb_t<104>(a, st);
     if (N <= 128) return launch_fb_t<128>(a, st);
     return cudaErrorInvalidValue;
 }

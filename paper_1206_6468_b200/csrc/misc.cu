@@ -48,6 +48,20 @@ __global__ void init_state_kernel(int frames, int ld, int Kt, float a0, float th
     }
 }
 
+// d[r][n] = q[r][n] / sum_n q[r][n]: the FB's unnormalised marginals -> q(D) marginals (one warp per row)
+__global__ void normalize_rows_kernel(const float *__restrict__ q, float *__restrict__ d, long long rows, int N) {
+    const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const float *src = q + r * N;
+    float s = 0.f;
+    for (int n = lane; n < N; n += 32) s += src[n];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float is = 1.f / s;
+    for (int n = lane; n < N; n += 32) d[r * N + n] = src[n] * is;
+}
+
 __global__ void fill_kernel(float *p, long long n, float v) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         p[i] = v;
@@ -157,6 +171,11 @@ cudaError_t launch_init_state(int frames, int ld, int Kt, float alpha0, float th
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     fill_kernel<<<grid_for((size_t)d_count, 256), 256, 0, st>>>(d_hat, d_count, d0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_normalize_rows(const float *q, float *d, long long rows, int N, cudaStream_t st) {
+    normalize_rows_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(q, d, rows, N);
     return cudaGetLastError();
 }
 

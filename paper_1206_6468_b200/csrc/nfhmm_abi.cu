@@ -544,7 +544,11 @@ int nfhmm_posteriors(nfhmm_t *h, float *d_hat, float *alpha_hat, float *V_hat, d
     if (r) return r;
     if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
     const size_t chainTN = (size_t)h->M * h->S * h->T * h->N;
-    if (d_hat) CU(h, cudaMemcpyAsync(d_hat, h->dhat, chainTN * 4, cudaMemcpyDefault, h->st));
+    if (d_hat) {   // the FB keeps unnormalised marginals: normalise per (m, s, t) on the way out
+        const bool dev = is_device_ptr(d_hat);
+        LAUNCH(h, NFHMM_K_OTHER, launch_normalize_rows(h->dhat, dev ? d_hat : h->fwd, (long long)h->M * h->S * h->T, h->N, h->st));
+        if (!dev) CU(h, cudaMemcpyAsync(d_hat, h->fwd, chainTN * 4, cudaMemcpyDeviceToHost, h->st));
+    }
     if (alpha_hat)
         CU(h, cudaMemcpy2DAsync(alpha_hat, (size_t)h->Kt * 4, h->alpha, (size_t)h->Kb * 4, (size_t)h->Kt * 4,
                                 (size_t)h->frames, cudaMemcpyDefault, h->st));
