@@ -21,7 +21,7 @@
 // Each chunk of 32 (s, n) blocks is processed flat (lane = float4 of consecutive elements, coalesced
 // loads and stores straight from / to HBM, independent elements for ILP), psi parked in shared memory;
 // then lane b sums the K psi values of block b in FP64 for Eq. 8.
-// HBM-bound: per frame it reads n (Kt floats) + d (S N) and writes theta (Kt) + e (S N) (+ alpha on the
+// HBM-bound: per frame it reads n (Kt floats) + u, b (2 S N) and writes theta (Kt) + e (S N) (+ alpha on the
 // last sweep of a call: alpha is not read inside the sweep loop).
 #include <cuda_runtime.h>
 #include <math.h>
@@ -98,14 +98,14 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     const int m = f / p.T, t = f - m * p.T;
     const float gamma = p.gamma;
 
-    // per-block prior pseudo-counts gamma d + 1 of Eq. 6: d of the previous sweep = the FB's unnormalised
-    // q_{s,t} divided by its sum over n (one row of N per source)
+    // per-block prior pseudo-counts gamma d + 1 of Eq. 6: d of the previous sweep = the FB messages'
+    // product u .* b divided by its sum over n (one row of N per source)
     unsigned bad = 0;
     for (int s = 0; s < p.S; ++s) {
-        const float *src = p.d_hat + ((size_t)(m * p.S + s) * p.T + t) * p.N;
+        const size_t row = ((size_t)(m * p.S + s) * p.T + t) * p.N;
         float qs = 0.f;
         for (int n = lane; n < p.N; n += 32) {
-            const float v = src[n];
+            const float v = p.u_fwd[row + n] * p.b_bwd[row + n];
             dvs[s * p.N + n] = v;
             qs += v;
         }

@@ -1,28 +1,26 @@
 // fb.cu -- kernel (e): scaled forward-backward per source chain, batched over all mixtures.
 //
-// q(D^(s)) is the chain posterior with log-likelihood gamma * phi (DESIGN R1).  One warp
-// per chain (m, s).  The recursion is latency-bound (2T dependent steps per chain), so one step is kept
-// to: broadcast the previous message through shared memory (128-bit loads) -> unrolled dot products ->
-// one multiply -> store, with the dot products and the running sum in packed FP32 pairs (FFMA2 / FADD2).
+// q(D^(s)) is the chain posterior with log-likelihood gamma * phi (DESIGN R1).  The two
+// recursions are independent -- the backward messages b_t never read the forward messages u_t, only the
+// marginals d_t ~ u_t .* b_t combine them -- so each chain gets TWO warps that run concurrently: warp 2c
+// the forward pass, warp 2c+1 the backward pass.  Both store their messages and the consumers (the
+// Dirichlet kernel, nfhmm_posteriors) form d_t = u_t .* b_t / sum_n(u_t .* b_t).
 //
-// State ownership (NMAX = N rounded up): lane l owns states 32 q + l, q < ceil(NMAX / 32), and computes
-// their full dot products with packed FP32 pairs (for N = 40: 2 x 20 FFMA2 per lane per step).  A build
-// option (NFHMM_FB_SPLIT=1) instead splits the NMAX % 32 remainder states over lane groups with a
-// butterfly: fewer FMAs, but the two shuffles on the critical path made the step ~1.7x slower (measured).
-//   A_s (row-stochastic, A[i][j] = P(j | i), DESIGN R4) lives in REGISTERS when it fits (columns for the
-//   forward pass, rows for the backward pass), else is read from shared memory in the same pattern.
-// Scaling by exact powers of two (no division, no FP64, no warp reduction on the critical path): every
-// lane also sums the broadcast vector it loads, and the next message is multiplied by 2^-E with E the
-// binary exponent of that sum:
+// Each recursion is latency-bound (T dependent steps), so one step is kept to: broadcast the previous
+// message through shared memory (128-bit loads) -> unrolled dot products in packed FP32 pairs (FFMA2) ->
+// one multiply -> store; no division, no FP64 and no warp reduction inside the loop.  Lane l owns states
+// 32 q + l, q < ceil(NMAX / 32) (for N = 40: 2 x 20 FFMA2 per lane per step).  Splitting the N % 32
+// remainder states over lane groups (fewer FMAs, a shuffle butterfly per step) measured ~1.7x slower.
+// A_s (row-stochastic, A[i][j] = P(j | i), DESIGN R4) lives in registers when it fits (columns for the
+// forward pass, rows for the backward pass), else is read from shared memory in the same pattern.
+// Scaling is by exact powers of two: every lane also sums the broadcast vector it loads, and the next
+// message is multiplied by 2^-E with E the binary exponent of that sum:
 //   u_0 = pi .* e_0;   u_t = ((u_{t-1} A) .* e_t) 2^-E_t,  E_t = exponent(sum u_{t-1});
-//   log Z = ln(sum u_{T-1}) + ln 2 * sum_t E_t + sum_t eoff_t   (FP64, after the loop).
-//   b_{T-1} = 1;  x_t = e_{t+1} .* b_{t+1};  b_t = (A x_t) 2^-E'_t,  E'_t = exponent(sum x_t);
-//   d_t = q_t / sum_n q_t with q_t = u_t .* b_t: the forward messages are stored unnormalised (their
-//   per-t normalisation cancels in d_t), and q_t itself is stored unnormalised -- the Dirichlet kernel
-//   and nfhmm_posteriors divide by the per-(s, t) sum, keeping every warp reduction out of this loop.
+//   log Z = ln(sum u_{T-1}) + ln 2 * sum_t E_t + sum_t eoff_t   (FP64, after the loop);
+//   b_{T-1} = 1;  x_t = e_{t+1} .* b_{t+1};  b_t = (A x_t) 2^-E'_t,  E'_t = exponent(sum x_t).
 // Emissions e = exp(gamma (phi - max_n phi)) in (0, 1] come precomputed from the Dirichlet kernel; eoff
-// are their FP64 per-frame offsets.  Inputs for the next CH steps are staged into shared memory with
-// cp.async (double-buffered chunks).
+// are their FP64 per-frame offsets.  The emissions of the next CH steps are staged into shared memory
+// with cp.async (double-buffered chunks).
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -32,23 +30,13 @@ namespace nfk {
 
 namespace {
 
-__host__ __device__ constexpr int pow2ceil(int x) { return x <= 1 ? x : 2 * pow2ceil((x + 1) / 2); }
-
-#ifndef NFHMM_FB_SPLIT
-#define NFHMM_FB_SPLIT 0   // 1: split the remainder states over lane groups (butterfly); 0: one more round
-#endif
 template <int NMAX>
 struct FBCfg {
-    static constexpr int NQ = NFHMM_FB_SPLIT ? NMAX / 32 : (NMAX + 31) / 32;   // rounds of 32 states
-    static constexpr int REM = NFHMM_FB_SPLIT ? NMAX % 32 : 0;                // remainder states
-    static constexpr int REMP = pow2ceil(REM);               // 0, 1, 2, 4, 8, 16, 32
-    static constexpr int G = REMP ? 32 / REMP : 1;           // lanes per remainder state
-    static constexpr int SEG = REMP ? ((NMAX + G - 1) / G + 3) / 4 * 4 : 0;   // inputs per lane (x4)
-    static constexpr int NB = (NMAX > G * SEG ? NMAX : G * SEG);            // broadcast buffer length
-    static constexpr int NBP = (NB + 3) / 4 * 4;
-    static constexpr bool REG = NQ * NMAX + SEG <= 96;       // A in registers
-    static constexpr int WPB = REG ? 4 : 2;                  // chains (warps) per CTA
-    static constexpr int CH = NMAX <= 64 ? 32 : 16;          // time steps per staged chunk
+    static constexpr int NQ = (NMAX + 31) / 32;       // rounds of 32 states per lane
+    static constexpr bool REG = NQ * NMAX <= 96;      // A (packed pairs) in registers
+    static constexpr int CPB = REG ? 2 : 1;           // chains per CTA (2 warps each)
+    static constexpr int WPB = 2 * CPB;
+    static constexpr int CH = NMAX <= 64 ? 32 : 16;   // time steps per staged chunk
 };
 
 __device__ __forceinline__ void cp_async4(float *smem_dst, const float *gsrc) {
@@ -92,74 +80,53 @@ __device__ __forceinline__ float hsum2(uint64_t v) {
     return a + b;
 }
 
-// One message step's products.  x: broadcast vector in shared memory (NBP floats, zero-padded).
-//   main[q] = sum_i x[i] M(i, 32 q + lane)                (q < NQ)
-//   ext     = sum_i x[i] M(i, 32 NQ + lane / G), butterflied over the lane's group of G
-//   xsum    = sum_i x[i]  (every lane, from the values it loads: no shuffle chain on the critical path)
-// M(i, j) for the main states: packed register pairs Mr[q][i/2] = (M(i, j), M(i+1, j)) or shared Ms[i *
-// NMAX + j]; for the remainder state's segment i = g SEG + i': Me[i'/2].
+// One message step.  x: broadcast vector in shared memory (NMAX floats, zero-padded).
+//   out[q] = sum_i x[i] M(i, 32 q + lane),  xsum = sum_i x[i] (every lane, from the values it loads)
+// M(i, j): packed register pairs Mr[q][i/2] = (M(i, j), M(i+1, j)), or shared Ms[i * NMAX + j].
 template <int NMAX>
-__device__ __forceinline__ void step_products(float (&main)[FBCfg<NMAX>::NQ ? FBCfg<NMAX>::NQ : 1], float &ext, float &xsum,
-                                              const float *x, const uint64_t (&Mr)[FBCfg<NMAX>::REG ? FBCfg<NMAX>::NQ + 1 : 1][FBCfg<NMAX>::REG ? NMAX / 2 : 1],
-                                              const uint64_t (&Me)[FBCfg<NMAX>::SEG ? FBCfg<NMAX>::SEG / 2 : 1], const float *Ms,
-                                              int lane, int g) {
+__device__ __forceinline__ void step_products(float (&out)[FBCfg<NMAX>::NQ], float &xsum, const float *x,
+                                              const uint64_t (&Mr)[FBCfg<NMAX>::REG ? FBCfg<NMAX>::NQ : 1][FBCfg<NMAX>::REG ? NMAX / 2 : 1],
+                                              const float *Ms, int lane) {
     using C = FBCfg<NMAX>;
     constexpr int NQ = C::NQ;
-    {
-        uint64_t a[NQ ? NQ : 1][2];
-        uint64_t s2[2] = {0ull, 0ull};
+    uint64_t a[NQ][2];
+    uint64_t s2[2] = {0ull, 0ull};
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) a[q][0] = a[q][1] = 0ull;
-        const ulonglong2 *x4 = reinterpret_cast<const ulonglong2 *>(x);
+    for (int q = 0; q < NQ; ++q) a[q][0] = a[q][1] = 0ull;
+    const ulonglong2 *x4 = reinterpret_cast<const ulonglong2 *>(x);
 #pragma unroll
-        for (int i4 = 0; i4 < NMAX / 4; ++i4) {
-            const ulonglong2 v = x4[i4];   // (x[4i4], x[4i4+1]) | (x[4i4+2], x[4i4+3])
-            add2(s2[0], v.x);
-            add2(s2[1], v.y);
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                uint64_t m0, m1;
-                if (C::REG) {
-                    m0 = Mr[C::REG ? q : 0][C::REG ? 2 * i4 : 0];
-                    m1 = Mr[C::REG ? q : 0][C::REG ? 2 * i4 + 1 : 0];
-                } else {
-                    const int j = min(32 * q + lane, NMAX - 1), i = 4 * i4;   // (lanes past NMAX: discarded)
-                    m0 = pk2(Ms[i * NMAX + j], Ms[(i + 1) * NMAX + j]);
-                    m1 = pk2(Ms[(i + 2) * NMAX + j], Ms[(i + 3) * NMAX + j]);
-                }
-                fma2(a[q][0], v.x, m0);
-                fma2(a[q][1], v.y, m1);
-            }
-        }
+    for (int i4 = 0; i4 < NMAX / 4; ++i4) {
+        const ulonglong2 v = x4[i4];   // (x[4i4], x[4i4+1]) | (x[4i4+2], x[4i4+3])
+        add2(s2[0], v.x);
+        add2(s2[1], v.y);
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            add2(a[q][0], a[q][1]);
-            main[q] = hsum2(a[q][0]);
+            uint64_t m0, m1;
+            if (C::REG) {
+                m0 = Mr[C::REG ? q : 0][C::REG ? 2 * i4 : 0];
+                m1 = Mr[C::REG ? q : 0][C::REG ? 2 * i4 + 1 : 0];
+            } else {
+                const int j = min(32 * q + lane, NMAX - 1), i = 4 * i4;   // (lanes past NMAX: discarded)
+                m0 = pk2(Ms[i * NMAX + j], Ms[(i + 1) * NMAX + j]);
+                m1 = pk2(Ms[(i + 2) * NMAX + j], Ms[(i + 3) * NMAX + j]);
+            }
+            fma2(a[q][0], v.x, m0);
+            fma2(a[q][1], v.y, m1);
         }
-        add2(s2[0], s2[1]);
-        xsum = hsum2(s2[0]);
     }
-    ext = 0.f;
-    if (C::SEG > 0) {
-        uint64_t b2[2] = {0ull, 0ull};
-        const ulonglong2 *xs = reinterpret_cast<const ulonglong2 *>(x + g * C::SEG);
 #pragma unroll
-        for (int i4 = 0; i4 < C::SEG / 4; ++i4) {
-            const ulonglong2 v = xs[i4];
-            fma2(b2[0], v.x, Me[C::SEG ? 2 * i4 : 0]);
-            fma2(b2[1], v.y, Me[C::SEG ? 2 * i4 + 1 : 0]);
-        }
-        add2(b2[0], b2[1]);
-        ext = hsum2(b2[0]);
-#pragma unroll
-        for (int o = 1; o < C::G; o <<= 1) ext += __shfl_xor_sync(0xffffffffu, ext, o);
+    for (int q = 0; q < NQ; ++q) {
+        add2(a[q][0], a[q][1]);
+        out[q] = hsum2(a[q][0]);
     }
+    add2(s2[0], s2[1]);
+    xsum = hsum2(s2[0]);
 }
 
 template <int NMAX>
 __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
     using C = FBCfg<NMAX>;
-    constexpr int WPB = C::WPB, NQ = C::NQ, CH = C::CH, G = C::G, SEG = C::SEG, NBP = C::NBP;
+    constexpr int CPB = C::CPB, NQ = C::NQ, CH = C::CH;
     constexpr bool REG = C::REG;
     extern __shared__ __align__(16) float sm[];
     const int N = p.N;
@@ -167,14 +134,14 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
     float *AT = As + NMAX * NMAX;         // [NMAX][NMAX]  AT[j][i] = A[i][j]
     float *wbase = AT + NMAX * NMAX;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // per warp: u[2][NBP] | e chunks [2][CH][N] | u chunks [2][CH][N]
-    const int per_warp = 2 * NBP + 4 * CH * N;
+    const bool backward = warp & 1;
+    // per warp: message broadcast buffer [2][NMAX] | emission chunks [2][CH][N]
+    const int per_warp = 2 * NMAX + 2 * CH * N;
     float *ubuf = wbase + warp * per_warp;
-    float *ech = ubuf + 2 * NBP;
-    float *ach = ech + 2 * CH * N;
+    float *ech = ubuf + 2 * NMAX;
 
     const int s = blockIdx.y;
-    const int m = blockIdx.x * WPB + warp;
+    const int m = blockIdx.x * CPB + (warp >> 1);
     const float *Ag = p.trans + (size_t)s * N * N;
     for (int idx = threadIdx.x; idx < NMAX * NMAX; idx += blockDim.x) {
         const int r = idx / NMAX, c = idx - r * NMAX;
@@ -182,92 +149,71 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
         As[idx] = v;
         AT[c * NMAX + r] = v;
     }
-    for (int idx = lane; idx < 2 * NBP; idx += 32) ubuf[idx] = 0.f;
+    for (int idx = lane; idx < 2 * NMAX; idx += 32) ubuf[idx] = 0.f;
     __syncthreads();
     if (m >= p.M) return;
 
     const int T = p.T;
     const size_t chain = (size_t)m * p.S + s;
     const float *em = p.ec + chain * T * N;     // emissions e_t(n)
-    float *fwd = p.fwd + chain * T * N;
-    float *dh = p.d_hat + chain * T * N;
     unsigned bad = 0;
-
-    // owned states: main js[q] = 32 q + lane; remainder jx = 32 NQ + lane / G (group member g)
-    const int g = lane % G;
-    const int jx = 32 * NQ + lane / G;
-    const bool xv_ok = SEG > 0 && jx < N, x_lead = xv_ok && g == 0;
-    bool jv[NQ ? NQ : 1];
+    bool jv[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) jv[q] = 32 * q + lane < N;
 
-    uint64_t Mr[REG ? NQ + 1 : 1][REG ? NMAX / 2 : 1];
-    uint64_t Me[SEG ? SEG / 2 : 1];
-    auto load_regs = [&](const float *M) {   // M[i * NMAX + j]: column j of M for the lane's states, in pairs
-        if (REG) {
+    // forward: columns of A; backward: b_t[j] = sum_k A[j][k] x[k] = sum_k AT[k][j] x[k]
+    const float *M = backward ? AT : As;
+    uint64_t Mr[REG ? NQ : 1][REG ? NMAX / 2 : 1];
+    if (REG) {
 #pragma unroll
-            for (int q = 0; q < NQ; ++q)
+        for (int q = 0; q < NQ; ++q)
 #pragma unroll
-                for (int i = 0; i < NMAX; i += 2)
-                    Mr[REG ? q : 0][REG ? i / 2 : 0] = 32 * q + lane < NMAX
-                        ? pk2(M[i * NMAX + 32 * q + lane], M[(i + 1) * NMAX + 32 * q + lane]) : 0ull;
-        }
-#pragma unroll
-        for (int i = 0; i < SEG; i += 2) {
-            const int ii = g * SEG + i;
-            const float m0 = (ii < NMAX && jx < NMAX) ? M[ii * NMAX + jx] : 0.f;
-            const float m1 = (ii + 1 < NMAX && jx < NMAX) ? M[(ii + 1) * NMAX + jx] : 0.f;
-            Me[SEG ? i / 2 : 0] = pk2(m0, m1);
-        }
-    };
-    load_regs(As);   // forward: columns of A
-
-    // ---------------- forward ----------------
-    const int nch = (T + CH - 1) / CH;
-    stage_rows(ech, em, N, 0, min(CH, T), lane);
-    float u[NQ ? NQ : 1], ux = 0.f;
-    int esum = 0;            // sum of the power-of-two scale exponents applied
-    for (int c = 0; c < nch; ++c) {
-        const int t0 = c * CH, n = min(CH, T - t0);
-        const float *ecur = ech + (c & 1) * CH * N;
-        cp_async_wait_all();
-        __syncwarp();
-        if (c + 1 < nch) stage_rows(ech + ((c + 1) & 1) * CH * N, em, N, t0 + CH, min(CH, T - t0 - CH), lane);
-        for (int tt = 0; tt < n; ++tt) {
-            const int t = t0 + tt;
-            const float *et = ecur + tt * N;
-            if (t == 0) {
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * et[32 * q + lane] : 0.f;
-                ux = xv_ok ? p.prior[s * N + jx] * et[jx] : 0.f;
-            } else {
-                float acc[NQ ? NQ : 1], accx, usum;
-                step_products<NMAX>(acc, accx, usum, ubuf + ((t - 1) & 1) * NBP, Mr, Me, As, lane, g);
-                if (!(usum > 0.f) || !(usum < INFINITY)) bad |= FLAG_NONFINITE;
-                const int E = exponent_of(usum);
-                const float sc = pow2_neg(E);
-                esum += E;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? acc[q] * et[32 * q + lane] * sc : 0.f;
-                ux = xv_ok ? accx * et[jx] * sc : 0.f;
-            }
-            float *un = ubuf + (t & 1) * NBP;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                if (jv[q]) {
-                    un[32 * q + lane] = u[q];
-                    fwd[(size_t)t * N + 32 * q + lane] = u[q];
-                }
-            }
-            if (x_lead) {
-                un[jx] = ux;
-                fwd[(size_t)t * N + jx] = ux;
-            }
-            __syncwarp();
-        }
+            for (int i = 0; i < NMAX; i += 2)
+                Mr[REG ? q : 0][REG ? i / 2 : 0] =
+                    32 * q + lane < NMAX ? pk2(M[i * NMAX + 32 * q + lane], M[(i + 1) * NMAX + 32 * q + lane]) : 0ull;
     }
-    {   // log Z
-        float part = x_lead ? ux : 0.f;
+    const int nch = (T + CH - 1) / CH;
+
+    if (!backward) {
+        // ---------------- forward: u_t -> p.fwd, log Z ----------------
+        float *fwd = p.fwd + chain * T * N;
+        stage_rows(ech, em, N, 0, min(CH, T), lane);
+        float u[NQ];
+        int esum = 0;            // sum of the power-of-two scale exponents applied
+        for (int c = 0; c < nch; ++c) {
+            const int t0 = c * CH, n = min(CH, T - t0);
+            const float *ecur = ech + (c & 1) * CH * N;
+            cp_async_wait_all();
+            __syncwarp();
+            if (c + 1 < nch) stage_rows(ech + ((c + 1) & 1) * CH * N, em, N, t0 + CH, min(CH, T - t0 - CH), lane);
+            for (int tt = 0; tt < n; ++tt) {
+                const int t = t0 + tt;
+                const float *et = ecur + tt * N;
+                if (t == 0) {
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * et[32 * q + lane] : 0.f;
+                } else {
+                    float acc[NQ], usum;
+                    step_products<NMAX>(acc, usum, ubuf + ((t - 1) & 1) * NMAX, Mr, M, lane);
+                    if (!(usum > 0.f) || !(usum < INFINITY)) bad |= FLAG_NONFINITE;
+                    const int E = exponent_of(usum);
+                    const float sc = pow2_neg(E);
+                    esum += E;
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? acc[q] * et[32 * q + lane] * sc : 0.f;
+                }
+                float *un = ubuf + (t & 1) * NMAX;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    if (jv[q]) {
+                        un[32 * q + lane] = u[q];
+                        fwd[(size_t)t * N + 32 * q + lane] = u[q];
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        float part = 0.f;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) part += u[q];
         const float usum = warp_sum(part);
@@ -281,56 +227,47 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
             p.logZ[chain] = lz;
             if (!isfinite(lz)) bad |= FLAG_NONFINITE;
         }
-    }
-    __threadfence_block();
-    __syncwarp();
-
-    // ---------------- backward ----------------
-    load_regs(AT);   // backward: b_t[j] = sum_k A[j][k] x[k] = sum_k AT[k][j] x[k]
-    float b[NQ ? NQ : 1], bx = xv_ok ? 1.f : 0.f;
+    } else {
+        // ---------------- backward: b_t -> p.bwd ----------------
+        float *bwd = p.bwd + chain * T * N;
+        float b[NQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) b[q] = jv[q] ? 1.f : 0.f;
-    // chunk c covers t in [t0, t0 + n), processed in descending t; needs e_{t+1} and u_t
-    auto stage_back = [&](int cc, int buf) {
-        const int t0 = cc * CH, n = min(CH, T - t0);
-        stage_rows(ach + buf * CH * N, fwd, N, t0, n, lane);
-        const int ne = min(n, T - 1 - t0);   // rows t0+1 .. t0+ne
-        if (ne > 0) stage_rows(ech + buf * CH * N, em, N, t0 + 1, ne, lane);
-    };
-    stage_back(nch - 1, (nch - 1) & 1);
-    for (int c = nch - 1; c >= 0; --c) {
-        const int t0 = c * CH, n = min(CH, T - t0);
-        const int buf = c & 1;
-        const float *acur = ach + buf * CH * N;
-        const float *ecur = ech + buf * CH * N;   // row r holds e_{t0 + 1 + r}
-        cp_async_wait_all();
-        __syncwarp();
-        if (c > 0) stage_back(c - 1, buf ^ 1);
-        for (int tt = n - 1; tt >= 0; --tt) {
-            const int t = t0 + tt;
-            if (t < T - 1) {
+        for (int q = 0; q < NQ; ++q) {
+            b[q] = jv[q] ? 1.f : 0.f;
+            if (jv[q]) bwd[(size_t)(T - 1) * N + 32 * q + lane] = 1.f;
+        }
+        // chunk c covers x_t for t in [t0, t0 + n) in descending t: needs e_{t+1}, rows t0+1 .. t0+n
+        auto stage_back = [&](int cc, int buf) {
+            const int t0 = cc * CH, ne = min(CH, T - 1 - t0);
+            stage_rows(ech + buf * CH * N, em, N, t0 + 1, ne, lane);
+        };
+        const int ncb = (T - 1 + CH - 1) / CH;   // chunks of t in [0, T-1)
+        if (ncb > 0) stage_back(ncb - 1, (ncb - 1) & 1);
+        for (int c = ncb - 1; c >= 0; --c) {
+            const int t0 = c * CH, n = min(CH, T - 1 - t0);
+            const int buf = c & 1;
+            const float *ecur = ech + buf * CH * N;   // row r holds e_{t0 + 1 + r}
+            cp_async_wait_all();
+            __syncwarp();
+            if (c > 0) stage_back(c - 1, buf ^ 1);
+            for (int tt = n - 1; tt >= 0; --tt) {
+                const int t = t0 + tt;
                 const float *en = ecur + tt * N;
-                float *xb = ubuf + (t & 1) * NBP;
+                float *xb = ubuf + (t & 1) * NMAX;
 #pragma unroll
                 for (int q = 0; q < NQ; ++q)
                     if (jv[q]) xb[32 * q + lane] = en[32 * q + lane] * b[q];
-                if (x_lead) xb[jx] = en[jx] * bx;
                 __syncwarp();
-                float acc[NQ ? NQ : 1], accx, xsum;
-                step_products<NMAX>(acc, accx, xsum, xb, Mr, Me, AT, lane, g);
+                float acc[NQ], xsum;
+                step_products<NMAX>(acc, xsum, xb, Mr, M, lane);
                 if (!(xsum > 0.f) || !(xsum < INFINITY)) bad |= FLAG_NONFINITE;
                 const float sc = pow2_neg(exponent_of(xsum));
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) b[q] = jv[q] ? acc[q] * sc : 0.f;
-                bx = xv_ok ? accx * sc : 0.f;
+                for (int q = 0; q < NQ; ++q) {
+                    b[q] = jv[q] ? acc[q] * sc : 0.f;
+                    if (jv[q]) bwd[(size_t)t * N + 32 * q + lane] = b[q];
+                }
             }
-            // q_t = u_t .* b_t, stored UNnormalised: its consumers (the Dirichlet kernel, posteriors)
-            // divide by sum_n q_t (keeps the warp reduction off this latency-bound loop)
-            const float *ut = acur + tt * N;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q)
-                if (jv[q]) dh[(size_t)t * N + 32 * q + lane] = ut[32 * q + lane] * b[q];
-            if (x_lead) dh[(size_t)t * N + jx] = ut[jx] * bx;
         }
     }
     if (bad) atomicOr(p.flags, bad);
@@ -340,14 +277,14 @@ template <int NMAX>
 cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
     using C = FBCfg<NMAX>;
     const int N = a.N;
-    const size_t smem = ((size_t)2 * NMAX * NMAX + (size_t)C::WPB * (2 * C::NBP + 4 * C::CH * N)) * sizeof(float);
+    const size_t smem = ((size_t)2 * NMAX * NMAX + (size_t)C::WPB * (2 * NMAX + 2 * C::CH * N)) * sizeof(float);
     static size_t attr = 0;
     if (smem > 48 * 1024 && attr < smem) {
         cudaError_t e = cudaFuncSetAttribute(fb_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    dim3 grid((a.M + C::WPB - 1) / C::WPB, a.S);
+    dim3 grid((a.M + C::CPB - 1) / C::CPB, a.S);
     fb_kernel<NMAX><<<grid, C::WPB * 32, smem, st>>>(a);
     return cudaGetLastError();
 }

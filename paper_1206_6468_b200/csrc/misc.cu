@@ -48,18 +48,18 @@ __global__ void init_state_kernel(int frames, int ld, int Kt, float a0, float th
     }
 }
 
-// d[r][n] = q[r][n] / sum_n q[r][n]: the FB's unnormalised marginals -> q(D) marginals (one warp per row)
-__global__ void normalize_rows_kernel(const float *__restrict__ q, float *__restrict__ d, long long rows, int N) {
+// d[r][n] = u[r][n] b[r][n] / sum_n u[r][n] b[r][n]: q(D) marginals from the FB messages (warp per row)
+__global__ void marginals_kernel(const float *__restrict__ u, const float *__restrict__ b, float *__restrict__ d,
+                                 long long rows, int N) {
     const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (r >= rows) return;
-    const float *src = q + r * N;
     float s = 0.f;
-    for (int n = lane; n < N; n += 32) s += src[n];
+    for (int n = lane; n < N; n += 32) s += u[r * N + n] * b[r * N + n];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const float is = 1.f / s;
-    for (int n = lane; n < N; n += 32) d[r * N + n] = src[n] * is;
+    for (int n = lane; n < N; n += 32) d[r * N + n] = u[r * N + n] * b[r * N + n] * is;
 }
 
 __global__ void fill_kernel(float *p, long long n, float v) {
@@ -165,17 +165,21 @@ cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// alpha, theta of DESIGN R5; u = b = 1 so that the marginals u .* b / sum are the uniform d = 1/N
 cudaError_t launch_init_state(int frames, int ld, int Kt, float alpha0, float theta0, float *alpha, float *theta,
-                              float *d_hat, long long d_count, float d0, cudaStream_t st) {
+                              float *u_fwd, float *b_bwd, long long d_count, cudaStream_t st) {
     init_state_kernel<<<grid_for((size_t)frames * ld, 256), 256, 0, st>>>(frames, ld, Kt, alpha0, theta0, alpha, theta);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fill_kernel<<<grid_for((size_t)d_count, 256), 256, 0, st>>>(d_hat, d_count, d0);
+    fill_kernel<<<grid_for((size_t)d_count, 256), 256, 0, st>>>(u_fwd, d_count, 1.f);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fill_kernel<<<grid_for((size_t)d_count, 256), 256, 0, st>>>(b_bwd, d_count, 1.f);
     return cudaGetLastError();
 }
 
-cudaError_t launch_normalize_rows(const float *q, float *d, long long rows, int N, cudaStream_t st) {
-    normalize_rows_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(q, d, rows, N);
+cudaError_t launch_marginals(const float *u, const float *b, float *d, long long rows, int N, cudaStream_t st) {
+    marginals_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(u, b, d, rows, N);
     return cudaGetLastError();
 }
 

@@ -29,7 +29,7 @@ struct nfhmm {
 
     float *betaT = nullptr, *beta = nullptr, *trans = nullptr, *prior = nullptr;
     float *V = nullptr, *R = nullptr, *theta = nullptr, *alpha = nullptr;
-    float *dhat = nullptr, *ec = nullptr, *fwd = nullptr, *cinv = nullptr;
+    float *bwd = nullptr, *ec = nullptr, *fwd = nullptr;   // FB messages b, u (q(D) = u .* b / sum), emissions
     float *vt = nullptr, *scale = nullptr, *vsrc = nullptr;
     float *bs_a = nullptr, *bs_b = nullptr;   // tensor-core path: pre-split beta for (a) and betaT for (b)
     double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
@@ -140,10 +140,9 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take(fr * Fa * 4);                       h->R = (float *)p;
     p = take(fr * Kb * 4);                       h->theta = (float *)p;
     p = take(fr * Kb * 4);                       h->alpha = (float *)p;
-    p = take(chainTN * 4);                       h->dhat = (float *)p;
+    p = take(chainTN * 4);                       h->bwd = (float *)p;
     p = take(chainTN * 4);                       h->ec = (float *)p;
     p = take(chainTN * 4);                       h->fwd = (float *)p;
-    p = take(chainT * 4);                        h->cinv = (float *)p;
     p = take(chainT * 8);                        h->eoff = (double *)p;
     p = take((size_t)h->M * h->S * 8);           h->logZ = (double *)p;
     p = take(fr * (size_t)(h->nt_a > h->nt_tc_a ? h->nt_a : h->nt_tc_a) * 8); h->data_part = (double *)p;
@@ -249,7 +248,8 @@ int step_dirichlet(nfhmm_t *h, bool write_alpha) {
     d.n_in = h->alpha;
     d.alpha = h->alpha;
     d.theta = h->theta;
-    d.d_hat = h->dhat;
+    d.u_fwd = h->fwd;
+    d.b_bwd = h->bwd;
     d.ec = h->ec;
     d.eoff = h->eoff;
     d.fconst = h->fconst;
@@ -271,9 +271,8 @@ int step_fb(nfhmm_t *h) {
     f.eoff = h->eoff;
     f.trans = h->trans;
     f.prior = h->prior;
-    f.d_hat = h->dhat;
     f.fwd = h->fwd;
-    f.cinv = h->cinv;
+    f.bwd = h->bwd;
     f.logZ = h->logZ;
     f.flags = h->flags;
     LAUNCH(h, NFHMM_K_FB, launch_fb(f, h->st));
@@ -489,8 +488,8 @@ int nfhmm_reset(nfhmm_t *h) {
         return res + log(x) - 0.5 / x - f * (1.0 / 12 - f * (1.0 / 120 - f / 252));
     };
     const float th0 = (float)exp(dg(a0) - dg(a0 * h->Kt));
-    LAUNCH(h, NFHMM_K_OTHER, launch_init_state((int)h->frames, h->Kb, h->Kt, (float)a0, th0, h->alpha, h->theta, h->dhat,
-                                (long long)h->M * h->S * h->T * h->N, (float)(1.0 / h->N), h->st));
+    LAUNCH(h, NFHMM_K_OTHER, launch_init_state((int)h->frames, h->Kb, h->Kt, (float)a0, th0, h->alpha, h->theta, h->fwd,
+                                h->bwd, (long long)h->M * h->S * h->T * h->N, h->st));
     CU(h, cudaMemsetAsync(h->fe, 0, (size_t)h->M * h->max_iters * 8, h->st));
     h->R_valid = false;
     r = recon_ratio(h);
@@ -544,10 +543,10 @@ int nfhmm_posteriors(nfhmm_t *h, float *d_hat, float *alpha_hat, float *V_hat, d
     if (r) return r;
     if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
     const size_t chainTN = (size_t)h->M * h->S * h->T * h->N;
-    if (d_hat) {   // the FB keeps unnormalised marginals: normalise per (m, s, t) on the way out
+    if (d_hat) {   // the FB keeps its messages u, b: marginals u .* b / sum per (m, s, t) on the way out
         const bool dev = is_device_ptr(d_hat);
-        LAUNCH(h, NFHMM_K_OTHER, launch_normalize_rows(h->dhat, dev ? d_hat : h->fwd, (long long)h->M * h->S * h->T, h->N, h->st));
-        if (!dev) CU(h, cudaMemcpyAsync(d_hat, h->fwd, chainTN * 4, cudaMemcpyDeviceToHost, h->st));
+        LAUNCH(h, NFHMM_K_OTHER, launch_marginals(h->fwd, h->bwd, dev ? d_hat : h->ec, (long long)h->M * h->S * h->T, h->N, h->st));
+        if (!dev) CU(h, cudaMemcpyAsync(d_hat, h->ec, chainTN * 4, cudaMemcpyDeviceToHost, h->st));
     }
     if (alpha_hat)
         CU(h, cudaMemcpy2DAsync(alpha_hat, (size_t)h->Kt * 4, h->alpha, (size_t)h->Kb * 4, (size_t)h->Kt * 4,

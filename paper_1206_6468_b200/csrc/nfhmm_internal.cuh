@@ -75,7 +75,8 @@ struct DirichletArgs {
     const float *n_in;        // [frames][ld]  data term of Eq. 6 (sum_l V z)
     float *alpha;             // [frames][ld]  out: alpha (may alias n_in)
     float *theta;             // [frames][ld]  out: exp(psi(alpha) - psi(alpha_0))
-    const float *d_hat;       // [M][S][T][N]  previous q(D) marginals, unnormalised (FB output; divided by sum_n)
+    const float *u_fwd;       // [M][S][T][N]  previous sweep's FB messages: q(D) marginals are
+    const float *b_bwd;       // [M][S][T][N]  d = u .* b / sum_n(u .* b)
     const double *fconst;     // [frames][4]   alpha_0, psi(alpha_0), -alpha_0 - lnG(alpha_0) + (alpha_0 - Kt) psi(alpha_0),
                               //               e^{-psi(alpha_0)}
     int write_alpha;          // 1: store alpha (last sweep of a call); 0: only theta / e (alpha is not read in the loop)
@@ -92,9 +93,8 @@ struct FBArgs {
     const double *eoff;       // [M][S][T]
     const float *trans;       // [S][N][N]
     const float *prior;       // [S][N]
-    float *d_hat;             // [M][S][T][N] out: UNnormalised marginals q = u .* b (consumers divide by sum_n)
-    float *fwd;               // [M][S][T][N] scratch: normalised forward messages
-    float *cinv;              // [M][S][T]    scratch: 1 / c_t
+    float *fwd;               // [M][S][T][N] out: scaled forward messages u_t
+    float *bwd;               // [M][S][T][N] out: scaled backward messages b_t (d_t = u_t .* b_t / sum)
     double *logZ;             // [M][S] out
     unsigned *flags;
 };
@@ -112,10 +112,9 @@ cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st);
 
 // Initial state (DESIGN R5): alpha = 1 + gamma/N, theta = exp(psi(a) - psi(Kt a)), d = 1/N.
 cudaError_t launch_init_state(int frames, int ld, int Kt, float alpha0, float theta0, float *alpha,
-                              float *theta, float *d_hat, long long d_count, float d0,
-                              cudaStream_t st);
-// d[r][:] = q[r][:] / sum(q[r][:]) over rows of N (the FB stores unnormalised marginals q = u .* b)
-cudaError_t launch_normalize_rows(const float *q, float *d, long long rows, int N, cudaStream_t st);
+                              float *theta, float *u_fwd, float *b_bwd, long long d_count, cudaStream_t st);
+// d[r][:] = u[r][:] .* b[r][:] / sum(u[r][:] .* b[r][:]) over rows of N (q(D) marginals from the FB messages)
+cudaError_t launch_marginals(const float *u, const float *b, float *d, long long rows, int N, cudaStream_t st);
 // betaT [rows][ldT] -> beta [ldT][ldb] transpose (rows = Kt, cols = F)
 cudaError_t launch_transpose(const float *src, int rows, int cols, int ld_src, float *dst, int ld_dst,
                              cudaStream_t st);
