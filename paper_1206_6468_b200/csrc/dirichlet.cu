@@ -18,9 +18,8 @@
 // exp(-u/2 - u^2 G) (one SFU exp2 of a small argument); lnG(x) - (x-1) psi(x) + x =
 // ln(x)/2 + ln(2 pi)/2 + 1/2 + u (H(2u-1) - 1/2) + (u - u^2) G(2u-1), which is O(ln x) -- the O(x ln x)
 // parts cancel analytically, and the -x is added back once per frame as -alpha_0 in FP64.
-// Each chunk of 32 (s, n) blocks is processed flat (lane = float4 of consecutive elements, coalesced
-// loads and stores straight from / to HBM, independent elements for ILP), psi parked in shared memory;
-// then lane b sums the K psi values of block b in FP64 for Eq. 8.
+// Lane b owns (s, n) block b (rounds of 32 blocks): the Eq. 6 pseudo-count is one register, the Eq. 8
+// block sum is lane-local (FP64), and elements go two at a time through a packed FFMA2 pipeline.
 // HBM-bound: per frame it reads n (Kt floats) + u, b (2 S N) and writes theta (Kt) + e (S N) (+ alpha on the
 // last sweep of a call: alpha is not read inside the sweep loop).
 #include <cuda_runtime.h>
@@ -35,63 +34,59 @@ namespace {
 
 constexpr int WPB = 8;   // frames (warps) per CTA
 
-struct PsiU {
-    float psi, lx, u, G, r;
-};
-// ln x for x >= 1 (normal): exponent * ln 2 + lg2(mantissa) * ln 2 on the SFU (|error| <= ~1.1e-7 for the
-// mantissa part, plus the final rounding)
-__device__ __forceinline__ float ln_sfu(float x) {
-    const uint32_t b = __float_as_uint(x);
-    const float m = __uint_as_float((b & 0x007FFFFFu) | 0x3F800000u);   // [1, 2)
-    float l2m;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2m) : "f"(m));
-    return fmaf((float)((int)(b >> 23) - 127), 0.693147180559945309f, l2m * 0.693147180559945309f);
+// ln of a pair, both >= 1 (normal): exponent ln 2 + lg2(mantissa) ln 2 (SFU), assembled packed
+__device__ __forceinline__ uint64_t ln_sfu2(float x0, float x1) {
+    const uint32_t b0 = __float_as_uint(x0), b1 = __float_as_uint(x1);
+    float l0, l1;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0) : "f"(__uint_as_float((b0 & 0x007FFFFFu) | 0x3F800000u)));
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1) : "f"(__uint_as_float((b1 & 0x007FFFFFu) | 0x3F800000u)));
+    const uint64_t e = f2pack((float)((int)(b0 >> 23) - 127), (float)((int)(b1 >> 23) - 127));
+    return f2fma(e, f2c(0.693147180559945309f), f2mul(f2pack(l0, l1), f2c(0.693147180559945309f)));
 }
-// psi(x) = ln x - r, r = u/2 + u^2 G(2u - 1), x >= 1 (alpha >= 1 by Eq. 6), FP32 (DESIGN R14)
-__device__ __forceinline__ PsiU psi_u(float x) {
-    PsiU o;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(o.u) : "f"(x));
-    o.lx = ln_sfu(x);
-    o.G = dig_G(fmaf(2.f, o.u, -1.f));
-    o.r = fmaf(o.u * o.u, o.G, 0.5f * o.u);
-    o.psi = o.lx - o.r;
-    return o;
+__device__ __forceinline__ float rcp_sfu(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
-// theta = exp(psi(x) - psi_0) = x e^{-psi_0} exp(-r): the exponent is small (r <= 0.58), so the SFU exp2 is
-// accurate to ~2^-22 relative (e0 = e^{-psi_0} is a per-frame FP64-derived constant)
-__device__ __forceinline__ float theta_of(float x, const PsiU &o, float e0) {
-    float er;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(er) : "f"(-1.44269504088896341f * o.r));
-    return (x * e0) * er;
+__device__ __forceinline__ float ex2_sfu(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
-// g~(x) = lnG(x) - (x - 1) psi(x) + x, from the pieces of psi_u (no cancellation)
-__device__ __forceinline__ float gtilde(const PsiU &o) {
-    const float H = lng_H(fmaf(2.f, o.u, -1.f));
-    return fmaf(0.5f, o.lx, 1.41893853320467274f) + fmaf(o.u, H - 0.5f, (o.u - o.u * o.u) * o.G);
-}
-
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-__device__ __forceinline__ double warp_max_d(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
+// Two elements at once (packed FFMA2 pipeline): alpha pair a -> psi, theta, and the running g~ sum
+//   u = 1/a, t = 2u - 1, r = u/2 + u^2 G(t), psi = ln a - r, theta = a e^{-psi_0} exp(-r),
+//   g~ = ln(a)/2 + ln(2 pi)/2 + 1/2 + u (H(t) - 1/2) + (u - u^2) G(t)
+__device__ __forceinline__ void elem_pair(float a0, float a1, uint64_t e0_2, bool want_h, uint64_t &psi2,
+                                          uint64_t &th2, uint64_t &g2t) {
+    const uint64_t a2 = f2pack(a0, a1);
+    const uint64_t u2 = f2pack(rcp_sfu(a0), rcp_sfu(a1));
+    const uint64_t lx2 = ln_sfu2(a0, a1);
+    const uint64_t t2 = f2fma(u2, f2c(2.f), f2c(-1.f));
+    const uint64_t G2 = dig_G2(t2);
+    const uint64_t uu2 = f2mul(u2, u2);
+    const uint64_t r2 = f2fma(uu2, G2, f2mul(u2, f2c(0.5f)));
+    psi2 = f2sub(lx2, r2);
+    float q0, q1;
+    f2unpack(f2mul(r2, f2c(-1.44269504088896341f)), q0, q1);
+    th2 = f2mul(f2mul(a2, e0_2), f2pack(ex2_sfu(q0), ex2_sfu(q1)));
+    if (want_h) {
+        const uint64_t H2 = lng_H2(t2);
+        const uint64_t g2 = f2fma(f2c(0.5f), lx2, f2c(1.41893853320467274f));
+        g2t = f2add(g2, f2fma(u2, f2sub(H2, f2c(0.5f)), f2mul(f2sub(u2, uu2), G2)));
+    } else {
+        g2t = 0ull;
+    }
 }
 
 __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int SN = p.S * p.N, K = p.K, CK = 32 * K;   // CK = elements per chunk of 32 blocks
+    const int SN = p.S * p.N, K = p.K;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // per warp: sps [SN] doubles | dvs [SN] floats | psis [CK] floats (16-B aligned pieces)
+    // per warp: sps [SN] doubles (Eq. 8 block sums) | dvs [SN] floats (prior pseudo-counts), 16-B aligned
     const size_t sps_b = ((size_t)SN * 8 + 15) & ~size_t(15), dvs_b = ((size_t)SN * 4 + 15) & ~size_t(15);
-    const size_t per_warp = sps_b + dvs_b + (((size_t)CK * 4 + 15) & ~size_t(15));   // multiple of 16
-    unsigned char *base = smem_raw + warp * per_warp;
+    unsigned char *base = smem_raw + warp * (sps_b + dvs_b);
     double *sps = reinterpret_cast<double *>(base);
     float *dvs = reinterpret_cast<float *>(base + sps_b);
-    float *psis = reinterpret_cast<float *>(base + sps_b + dvs_b);
 
     const int f = blockIdx.x * WPB + warp;
     if (f >= p.frames) return;
@@ -117,55 +112,78 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
         for (int n = lane; n < p.N; n += 32) dvs[s * p.N + n] = fmaf(gq, dvs[s * p.N + n], 1.f);
     }
     const double psi0 = p.fconst[4 * (size_t)f + 1];
-    const float e0 = (float)p.fconst[4 * (size_t)f + 3];   // e^{-psi(alpha_0)}
-    const float invK = 1.f / (float)K;
+    const uint64_t e0_2 = f2c((float)p.fconst[4 * (size_t)f + 3]);   // e^{-psi(alpha_0)}
     __syncwarp();
 
-    const float4 *nin = reinterpret_cast<const float4 *>(p.n_in + (size_t)f * p.ld);
-    float4 *aout = reinterpret_cast<float4 *>(p.alpha + (size_t)f * p.ld);
-    float4 *tout = reinterpret_cast<float4 *>(p.theta + (size_t)f * p.ld);
+    // lane b owns (s, n) block b of each round of 32 blocks: its K elements are contiguous, so the
+    // pseudo-count is one register, the Eq. 8 sum is lane-local, and I/O is in 8-byte pairs (K even;
+    // the warp's accesses of one pair index cover 32 K consecutive floats)
+    const float *nrow = p.n_in + (size_t)f * p.ld;
+    float *arow = p.alpha + (size_t)f * p.ld;
+    float *trow = p.theta + (size_t)f * p.ld;
     const bool want_h = p.hdir != nullptr, want_a = p.write_alpha != 0;
-    float hg = 0.f;   // sum of g~ over this lane's elements
-    for (int c0 = 0; c0 < p.Kt; c0 += CK) {
-        const int cn = min(CK, p.Kt - c0), b0 = c0 / K;
-        // flat, coalesced pass over the chunk: alpha, psi, theta, g~ per element (independent -> ILP);
-        // psi parked in shared memory for the Eq. 8 block sums
-        for (int q = lane; 4 * q < cn; q += 32) {
-            const float4 v = nin[(c0 >> 2) + q];
-            const float nv[4] = {v.x, v.y, v.z, v.w};
-            float av[4], tv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int i = 4 * q + e;
-                av[e] = tv[e] = 0.f;
-                if (i < cn) {
-                    const int bl = (int)(((float)i + 0.5f) * invK);      // block of element i (i < 32 K)
-                    const float a = nv[e] + dvs[b0 + bl];
-                    const PsiU o = psi_u(a);
-                    av[e] = a;
-                    tv[e] = theta_of(a, o, e0);
-                    psis[i] = o.psi;
-                    if (want_h) hg += gtilde(o);   // (non-finite alpha propagates to eoff: checked there)
+    uint64_t hg2 = 0ull;   // packed running sum of g~ over this lane's elements
+    for (int b = lane; b - lane < SN; b += 32) {
+        if (b < SN) {
+            const float dv = dvs[b];
+            const uint64_t dv2 = f2c(dv);
+            const int k0 = b * K;
+            double sp = 0.0;
+            if ((K & 1) == 0) {
+                for (int j = 0; j < K; j += 2) {
+                    const float2 nv = *reinterpret_cast<const float2 *>(nrow + k0 + j);
+                    uint64_t a2 = f2add(f2pack(nv.x, nv.y), dv2);
+                    float a0, a1;
+                    f2unpack(a2, a0, a1);
+                    uint64_t ps2, th2, g2;
+                    elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                    float p0, p1, t0, t1;
+                    f2unpack(ps2, p0, p1);
+                    f2unpack(th2, t0, t1);
+                    sp += (double)p0 + (double)p1;
+                    hg2 = f2add(hg2, g2);
+                    if (want_a) *reinterpret_cast<float2 *>(arow + k0 + j) = make_float2(a0, a1);
+                    *reinterpret_cast<float2 *>(trow + k0 + j) = make_float2(t0, t1);
+                }
+            } else {   // odd K: scalar I/O, pairs (j, j+1) with a dummy partner for the last element
+                for (int j = 0; j < K; j += 2) {
+                    const bool two = j + 1 < K;
+                    const float a0 = nrow[k0 + j] + dv, a1 = two ? nrow[k0 + j + 1] + dv : 1.f;
+                    uint64_t ps2, th2, g2;
+                    elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                    float p0, p1, t0, t1, g0, g1;
+                    f2unpack(ps2, p0, p1);
+                    f2unpack(th2, t0, t1);
+                    f2unpack(g2, g0, g1);
+                    sp += (double)p0 + (two ? (double)p1 : 0.0);
+                    hg2 = f2add(hg2, f2pack(g0, two ? g1 : 0.f));
+                    if (want_a) arow[k0 + j] = a0;
+                    trow[k0 + j] = t0;
+                    if (two) {
+                        if (want_a) arow[k0 + j + 1] = a1;
+                        trow[k0 + j + 1] = t1;
+                    }
                 }
             }
-            if (want_a) aout[(c0 >> 2) + q] = make_float4(av[0], av[1], av[2], av[3]);
-            tout[(c0 >> 2) + q] = make_float4(tv[0], tv[1], tv[2], tv[3]);
+            sps[b] = sp;
         }
-        __syncwarp();
-        // Eq. 8 segment sums: lane b owns block b0 + b (FP64)
-        if (lane * K < cn) {
-            double sp = 0.0;
-            for (int j = 0; j < K; ++j) sp += (double)psis[lane * K + j];
-            sps[b0 + lane] = sp;
-        }
-        __syncwarp();
     }
+    float hg;
+    {
+        float h0, h1;
+        f2unpack(hg2, h0, h1);
+        hg = h0 + h1;
+    }
+    __syncwarp();
 
-    // Eq. 8: centre per source and emit
+    // Eq. 8: centre per source and emit.  Any offset works (the FB is shift-invariant per frame)
+    // as long as e and eoff use the same one: the max is taken in FP32, the differences in FP64.
     for (int s = 0; s < p.S; ++s) {
-        double mx = -INFINITY;
-        for (int n = lane; n < p.N; n += 32) mx = fmax(mx, sps[s * p.N + n]);
-        mx = warp_max_d(mx);
+        float mxf = -INFINITY;
+        for (int n = lane; n < p.N; n += 32) mxf = fmaxf(mxf, (float)sps[s * p.N + n]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+        const double mx = (double)mxf;
         float *dst = p.ec + ((size_t)(m * p.S + s) * p.T + t) * p.N;
         for (int n = lane; n < p.N; n += 32) dst[n] = expf((float)((double)gamma * (sps[s * p.N + n] - mx)));
         if (lane == 0) {
@@ -174,9 +192,10 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
             if (!isfinite(off)) bad |= FLAG_NONFINITE;
         }
     }
-    if (want_h) {
-        const double h = warp_sum_d((double)hg);
-        if (lane == 0) p.hdir[f] = h + p.fconst[4 * (size_t)f + 2];
+    if (want_h) {   // (FP32 warp sum: |sum g~| ~ 3e3 per frame, error ~1e-4 against a tolerance of ~6 per frame)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) hg += __shfl_xor_sync(0xffffffffu, hg, o);
+        if (lane == 0) p.hdir[f] = (double)hg + p.fconst[4 * (size_t)f + 2];
     }
     if (bad) atomicOr(p.flags, bad);
 }
@@ -184,9 +203,8 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
 }  // namespace
 
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
-    const int SN = a.S * a.N, CK = 32 * a.K;
-    const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15)) +
-                            (((size_t)CK * 4 + 15) & ~size_t(15));
+    const int SN = a.S * a.N;
+    const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15));
     const size_t smem = per_warp * WPB;
     static size_t attr = 0;
     if (smem > 48 * 1024 && attr < smem) {
