@@ -303,32 +303,44 @@ def run_ours(args):
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12      # TFLOP/s, FFMA pipe (DESIGN "Rooflines")
     hbm_peak = float(peaks.get("hbm_gbs", 6539.2))
-    dom = max(("recon", "backproj", "dirichlet", "fb"), key=lambda k: prof[k][0])
-    ms_k, n_k = prof[dom]
     frames_local = M * cfg.T
-    if dom in ("recon", "backproj"):
-        flops = 2.0 * frames_local * cfg.F * cfg.Kt       # algorithmic FLOPs per launch (true F, Kt)
-        achieved = flops / (ms_k / n_k / 1000.0) / 1e12
-        if args.math == "tc":
-            # FP32 contraction as 3xTF32 on tcgen05: TF32 dense = measured bf16 burst x 1/2 (nominal
-            # 1.1 / 2.25 PFLOP/s), three MMAs per product -> FP32-equivalent peak = TF32 / 3
-            tf32 = float(peaks.get("bf16_tflops", 1645.8)) * 0.5
-            peak = tf32 / 3.0
-            roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak,
-                    "peak_note": f"3xTF32 FP32-equivalent: measured bf16 {peaks.get('bf16_tflops', 1645.8)} TF/s x 1/2 (TF32) / 3",
-                    "fp32_ffma_peak": fp32_peak}
-        else:
-            roof = {"kernel": dom, "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+    SN = cfg.S * cfg.N
+
+    def roofline_of(k):
+        """Algorithmic work per launch of kernel class k (DESIGN "Kernels, rooflines") over its live
+        CUDA-event launch time, against the kernel's roofline."""
+        ms_k, n_k = prof[k]
+        if not n_k:
+            return None
+        t_launch = ms_k / n_k / 1000.0
+        if k in ("recon", "backproj"):
+            flops = 2.0 * frames_local * cfg.F * cfg.Kt       # algorithmic FLOPs per launch (true F, Kt)
+            achieved = flops / t_launch / 1e12
+            if args.math == "tc":
+                # FP32 contraction as 3xTF32 on tcgen05: TF32 dense = measured bf16 burst x 1/2 (nominal
+                # 1.1 / 2.25 PFLOP/s), three MMAs per product -> FP32-equivalent peak = TF32 / 3
+                tf32 = float(peaks.get("bf16_tflops", 1645.8)) * 0.5
+                peak = tf32 / 3.0
+                return {"kernel": k, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": achieved / peak,
+                        "peak_note": f"3xTF32 FP32-equivalent: measured bf16 {peaks.get('bf16_tflops', 1645.8)} TF/s x 1/2 (TF32) / 3",
+                        "fp32_ffma_peak": fp32_peak}
+            return {"kernel": k, "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                     "frac": achieved / fp32_peak, "peak_note": f"FP32 FFMA 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz"}
-    else:
-        if dom == "dirichlet":
-            byts = frames_local * (3 * cfg.Kt * 4 + cfg.S * cfg.N * 4 * 2 + cfg.S * 8 + 8)
-        else:
-            byts = M * cfg.S * cfg.T * (cfg.N * 4 * 4 + 4 * 2 + 8)
-        achieved = byts / (ms_k / n_k / 1000.0) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+        if k == "dirichlet":
+            # read n (Kt) + FB messages u, b (2 S N) + frame constants (32 B); write theta (Kt) + emissions
+            # (S N) + offsets (8 S) + bound term (8); alpha (Kt) on the last sweep of the call only
+            byts = frames_local * (2 * cfg.Kt * 4 + 3 * SN * 4 + cfg.S * 8 + 8 + 32 + cfg.Kt * 4 / iters)
+        else:   # fb: read emissions (N) + offsets (8), write u and b (2 N) per chain-frame
+            byts = M * cfg.S * cfg.T * (3 * cfg.N * 4 + 8)
+        achieved = byts / t_launch / 1e9
+        return {"kernel": k, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak}
+
+    dom = max(("recon", "backproj", "dirichlet", "fb"), key=lambda k: prof[k][0])
+    roof = roofline_of(dom)
+    roof_all = {k: {kk: v for kk, v in (roofline_of(k) or {}).items() if kk in ("bound", "achieved", "frac", "unit")}
+                for k in ("recon", "backproj", "dirichlet", "fb")}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -354,7 +366,7 @@ def run_ours(args):
                        "l2": "no flush: per-step inputs/state exceed L2 (V %.2f GB, theta %.2f GB per GPU)" % (
                            M * cfg.T * h.layout()["F_pad"] * 4 / 1e9, M * cfg.T * h.layout()["Kt_pad"] * 4 / 1e9),
                        "step": "reset + iters sweeps + separate, inputs resident in HBM"},
-            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "roofline": roof, "rooflines": roof_all, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches, "gen_seconds": round(t_gen, 2),
         }
         print(json.dumps(line), flush=True)

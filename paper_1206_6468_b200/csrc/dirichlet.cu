@@ -200,10 +200,210 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     if (bad) atomicOr(p.flags, bad);
 }
 
+__device__ __forceinline__ void cp_async_n(void *smem_dst, const void *gsrc, int bytes16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc));
+    (void)bytes16;
+}
+__device__ __forceinline__ void cp_async_4(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_8(void *smem_dst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// Per-warp shared-memory layout of the pipelined kernel (bytes, 16-B aligned pieces): Eq. 8 block sums,
+// pseudo-counts, and two frame buffers [n row (Kt rounded to 4) | u (S N) | b (S N) | 4 frame constants].
+struct PipeLayout {
+    size_t sps, dvs, buf0, nb, ub, bb, cb, buf_bytes, total;
+    __host__ __device__ PipeLayout(int S, int N, int Kt) {
+        const int SN = S * N;
+        size_t o = 0;
+        sps = o; o += ((size_t)SN * 8 + 15) & ~size_t(15);
+        dvs = o; o += ((size_t)SN * 4 + 15) & ~size_t(15);
+        buf0 = o;
+        nb = 0;
+        ub = ((size_t)((Kt + 3) & ~3)) * 4;
+        bb = ub + (((size_t)SN * 4 + 15) & ~size_t(15));
+        cb = bb + (((size_t)SN * 4 + 15) & ~size_t(15));
+        buf_bytes = cb + 32;
+        total = buf0 + 2 * buf_bytes;
+    }
+};
+
+// Software-pipelined variant (per-warp smem small enough): persistent warps walk a strided set of frames
+// and cp.async the NEXT frame's n row, FB messages and constants into the other buffer while computing
+// the current one, so the kernel is bound by issue / HBM instead of one outstanding load per warp.
+// theta is written back in place and leaves with coalesced float4 stores.  Same arithmetic as
+// dirichlet_kernel (results are bitwise identical).
+__global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int SN = p.S * p.N, K = p.K, Kt = p.Kt;
+    const PipeLayout L(p.S, p.N, Kt);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *base = smem_raw + warp * L.total;
+    double *sps = reinterpret_cast<double *>(base + L.sps);
+    float *dvs = reinterpret_cast<float *>(base + L.dvs);
+    const int nwarps = gridDim.x * WPB;
+    const float gamma = p.gamma;
+    const bool want_h = p.hdir != nullptr, want_a = p.write_alpha != 0;
+    const int Kt4 = (Kt + 3) >> 2;
+    unsigned bad = 0;
+
+    auto issue = [&](int f, int slot) {
+        unsigned char *bf = base + L.buf0 + slot * L.buf_bytes;
+        const float *nrow = p.n_in + (size_t)f * p.ld;
+        for (int q = lane; q < Kt4; q += 32) cp_async_n(bf + L.nb + 16 * q, nrow + 4 * q, 16);
+        const int m = f / p.T, t = f - m * p.T;
+        for (int i = lane; i < SN; i += 32) {
+            const int s = i / p.N, n = i - s * p.N;
+            const size_t row = ((size_t)(m * p.S + s) * p.T + t) * p.N + n;
+            cp_async_4(bf + L.ub + 4 * i, p.u_fwd + row);
+            cp_async_4(bf + L.bb + 4 * i, p.b_bwd + row);
+        }
+        if (lane < 4) cp_async_8(bf + L.cb + 8 * lane, p.fconst + 4 * (size_t)f + lane);
+        cp_commit();
+    };
+
+    int f = blockIdx.x * WPB + warp;
+    if (f < p.frames) issue(f, 0);
+    for (int it = 0; f < p.frames; ++it) {
+        const int fn = f + nwarps;
+        if (fn < p.frames) issue(fn, (it + 1) & 1);
+        else cp_commit();
+        cp_wait1();
+        __syncwarp();
+        unsigned char *bf = base + L.buf0 + (it & 1) * L.buf_bytes;
+        float *nbuf = reinterpret_cast<float *>(bf + L.nb);
+        const float *ub = reinterpret_cast<const float *>(bf + L.ub);
+        const float *bb = reinterpret_cast<const float *>(bf + L.bb);
+        const double *fc = reinterpret_cast<const double *>(bf + L.cb);
+        const int m = f / p.T, t = f - m * p.T;
+
+        // pseudo-counts gamma d + 1 (d = u .* b / sum_n per source)
+        for (int s = 0; s < p.S; ++s) {
+            float qs = 0.f;
+            for (int n = lane; n < p.N; n += 32) {
+                const float v = ub[s * p.N + n] * bb[s * p.N + n];
+                dvs[s * p.N + n] = v;
+                qs += v;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, o);
+            if (!(qs > 0.f) || !(qs < INFINITY)) bad |= FLAG_NONFINITE;
+            const float gq = gamma / qs;
+            __syncwarp();
+            for (int n = lane; n < p.N; n += 32) dvs[s * p.N + n] = fmaf(gq, dvs[s * p.N + n], 1.f);
+        }
+        const double psi0 = fc[1];
+        const uint64_t e0_2 = f2c((float)fc[3]);
+        __syncwarp();
+
+        // block-owner element pass over the staged row; theta replaces n in place
+        float *arow = p.alpha + (size_t)f * p.ld;
+        uint64_t hg2 = 0ull;
+        for (int b = lane; b - lane < SN; b += 32) {
+            if (b < SN) {
+                const uint64_t dv2 = f2c(dvs[b]);
+                float *pn = nbuf + b * K;
+                double sp = 0.0;
+                for (int j = 0; j < K; j += 2) {
+                    const bool two = j + 1 < K;
+                    const uint64_t a2 = f2add(f2pack(pn[j], two ? pn[j + 1] : 0.f), dv2);
+                    float a0, a1;
+                    f2unpack(a2, a0, a1);
+                    uint64_t ps2, th2, g2;
+                    elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                    float p0, p1, t0, t1, g0, g1;
+                    f2unpack(ps2, p0, p1);
+                    f2unpack(th2, t0, t1);
+                    f2unpack(g2, g0, g1);
+                    sp += (double)p0 + (two ? (double)p1 : 0.0);
+                    hg2 = f2add(hg2, f2pack(g0, two ? g1 : 0.f));
+                    pn[j] = t0;
+                    if (two) pn[j + 1] = t1;
+                    if (want_a) {
+                        arow[b * K + j] = a0;
+                        if (two) arow[b * K + j + 1] = a1;
+                    }
+                }
+                sps[b] = sp;
+            }
+        }
+        __syncwarp();
+        float4 *trow = reinterpret_cast<float4 *>(p.theta + (size_t)f * p.ld);
+        for (int q = lane; q < Kt4; q += 32) {
+            float4 tv = reinterpret_cast<const float4 *>(nbuf)[q];
+            const int k = 4 * q;
+            if (k + 1 >= Kt) tv.y = 0.f;   // (the row padding past Kt stays zero)
+            if (k + 2 >= Kt) tv.z = 0.f;
+            if (k + 3 >= Kt) tv.w = 0.f;
+            trow[q] = tv;
+        }
+        float hg;
+        {
+            float h0, h1;
+            f2unpack(hg2, h0, h1);
+            hg = h0 + h1;
+        }
+        // Eq. 8: centre per source and emit (see dirichlet_kernel)
+        for (int s = 0; s < p.S; ++s) {
+            float mxf = -INFINITY;
+            for (int n = lane; n < p.N; n += 32) mxf = fmaxf(mxf, (float)sps[s * p.N + n]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+            const double mx = (double)mxf;
+            float *dst = p.ec + ((size_t)(m * p.S + s) * p.T + t) * p.N;
+            for (int n = lane; n < p.N; n += 32) dst[n] = expf((float)((double)gamma * (sps[s * p.N + n] - mx)));
+            if (lane == 0) {
+                const double off = (double)gamma * (mx - (double)K * psi0);
+                p.eoff[(size_t)(m * p.S + s) * p.T + t] = off;
+                if (!isfinite(off)) bad |= FLAG_NONFINITE;
+            }
+        }
+        if (want_h) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) hg += __shfl_xor_sync(0xffffffffu, hg, o);
+            if (lane == 0) p.hdir[f] = (double)hg + fc[2];
+        }
+        __syncwarp();   // this buffer is refilled two frames from now
+        f = fn;
+    }
+    if (bad) atomicOr(p.flags, bad);
+}
+
 }  // namespace
 
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
     const int SN = a.S * a.N;
+    const PipeLayout L(a.S, a.N, a.Kt);
+    if (L.total <= 12 * 1024) {   // pipelined variant (configs 0-3); config 4's 32 KB rows use the other
+        const size_t smem = L.total * WPB;
+        static size_t attr_p = 0;
+        if (smem > 48 * 1024 && attr_p < smem) {
+            cudaError_t e = cudaFuncSetAttribute(dirichlet_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            attr_p = smem;
+        }
+        static int sms = 0, per_sm = 0;
+        static size_t per_sm_smem = 0;
+        if (!sms || per_sm_smem != smem) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dirichlet_pipe_kernel, WPB * 32, smem);
+            if (per_sm < 1) per_sm = 1;
+            per_sm_smem = smem;
+        }
+        const long long need = (a.frames + WPB - 1) / WPB;
+        const int grid = (int)(need < (long long)sms * per_sm ? need : (long long)sms * per_sm);
+        dirichlet_pipe_kernel<<<grid, WPB * 32, smem, st>>>(a);
+        return cudaGetLastError();
+    }
     const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15));
     const size_t smem = per_warp * WPB;
     static size_t attr = 0;

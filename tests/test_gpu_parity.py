@@ -158,3 +158,26 @@ def test_errors_are_explicit():
     assert e.value.status == NFHMM_EZEROSUPPORT
     h.close()
     h2.close()
+
+
+def test_bench_kernel_instrumentation_resets_state():
+    """nfhmm_bench_kernel (per-kernel timing) leaves the handle reset: a run after it equals a fresh run
+    bitwise; classes outside RECON..FB and reps < 1 are rejected."""
+    from paper_1206_6468_b200.nfhmm import NFHMM, NFHMMError, NFHMM_EINVAL
+    cfg, model, V = make_inputs(3, T=150, M=2, counts=2000)
+    ref = run_gpu(cfg, model, V, 4, separate=False)
+    h = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=2)
+    h.set_model(model.beta, model.trans, model.prior)
+    h.set_observations(np.ascontiguousarray(V))
+    h.vb_iterate(2)
+    for cls in ("recon", "backproj", "dirichlet", "fb"):
+        assert h.bench_kernel(cls, 3) > 0.0
+    for bad in (("elbo", 1), ("recon", 0)):
+        with pytest.raises(NFHMMError) as e:
+            h.bench_kernel(*bad)
+        assert e.value.status == NFHMM_EINVAL
+    h.vb_iterate(4)
+    out = h.posteriors()
+    h.close()
+    for key in ("d_hat", "alpha_hat", "V_hat", "free_energy"):
+        np.testing.assert_array_equal(out[key], ref[key], err_msg=key)
