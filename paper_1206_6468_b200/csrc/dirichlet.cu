@@ -240,6 +240,7 @@ struct PipeLayout {
 // the current one, so the kernel is bound by issue / HBM instead of one outstanding load per warp.
 // theta is written back in place and leaves with coalesced float4 stores.  Same arithmetic as
 // dirichlet_kernel (results are bitwise identical).
+template <bool EVEN>   // K even: element pairs never straddle a block end (no pairing selects)
 __global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int SN = p.S * p.N, K = p.K, Kt = p.Kt;
@@ -259,11 +260,21 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs 
         const float *nrow = p.n_in + (size_t)f * p.ld;
         for (int q = lane; q < Kt4; q += 32) cp_async_n(bf + L.nb + 16 * q, nrow + 4 * q, 16);
         const int m = f / p.T, t = f - m * p.T;
-        for (int i = lane; i < SN; i += 32) {
-            const int s = i / p.N, n = i - s * p.N;
-            const size_t row = ((size_t)(m * p.S + s) * p.T + t) * p.N + n;
-            cp_async_4(bf + L.ub + 4 * i, p.u_fwd + row);
-            cp_async_4(bf + L.bb + 4 * i, p.b_bwd + row);
+        if ((p.N & 3) == 0) {   // rows of N floats are 16-byte aligned: 16-byte copies
+            const int N4 = p.N >> 2;
+            for (int i = lane; i < p.S * N4; i += 32) {
+                const int s = i / N4, n4 = i - s * N4;
+                const size_t row = ((size_t)(m * p.S + s) * p.T + t) * p.N + 4 * n4;
+                cp_async_n(bf + L.ub + 16 * i, p.u_fwd + row, 16);
+                cp_async_n(bf + L.bb + 16 * i, p.b_bwd + row, 16);
+            }
+        } else {
+            for (int i = lane; i < SN; i += 32) {
+                const int s = i / p.N, n = i - s * p.N;
+                const size_t row = ((size_t)(m * p.S + s) * p.T + t) * p.N + n;
+                cp_async_4(bf + L.ub + 4 * i, p.u_fwd + row);
+                cp_async_4(bf + L.bb + 4 * i, p.b_bwd + row);
+            }
         }
         if (lane < 4) cp_async_8(bf + L.cb + 8 * lane, p.fconst + 4 * (size_t)f + lane);
         cp_commit();
@@ -311,24 +322,42 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs 
                 const uint64_t dv2 = f2c(dvs[b]);
                 float *pn = nbuf + b * K;
                 double sp = 0.0;
-                for (int j = 0; j < K; j += 2) {
-                    const bool two = j + 1 < K;
-                    const uint64_t a2 = f2add(f2pack(pn[j], two ? pn[j + 1] : 0.f), dv2);
-                    float a0, a1;
-                    f2unpack(a2, a0, a1);
-                    uint64_t ps2, th2, g2;
-                    elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
-                    float p0, p1, t0, t1, g0, g1;
-                    f2unpack(ps2, p0, p1);
-                    f2unpack(th2, t0, t1);
-                    f2unpack(g2, g0, g1);
-                    sp += (double)p0 + (two ? (double)p1 : 0.0);
-                    hg2 = f2add(hg2, f2pack(g0, two ? g1 : 0.f));
-                    pn[j] = t0;
-                    if (two) pn[j + 1] = t1;
-                    if (want_a) {
-                        arow[b * K + j] = a0;
-                        if (two) arow[b * K + j + 1] = a1;
+                if (EVEN) {
+                    for (int j = 0; j < K; j += 2) {
+                        const float2 nv = *reinterpret_cast<const float2 *>(pn + j);
+                        const uint64_t a2 = f2add(f2pack(nv.x, nv.y), dv2);
+                        float a0, a1;
+                        f2unpack(a2, a0, a1);
+                        uint64_t ps2, th2, g2;
+                        elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                        float p0, p1, t0, t1;
+                        f2unpack(ps2, p0, p1);
+                        f2unpack(th2, t0, t1);
+                        sp += (double)p0 + (double)p1;
+                        hg2 = f2add(hg2, g2);
+                        *reinterpret_cast<float2 *>(pn + j) = make_float2(t0, t1);
+                        if (want_a) *reinterpret_cast<float2 *>(arow + b * K + j) = make_float2(a0, a1);
+                    }
+                } else {
+                    for (int j = 0; j < K; j += 2) {
+                        const bool two = j + 1 < K;
+                        const uint64_t a2 = f2add(f2pack(pn[j], two ? pn[j + 1] : 0.f), dv2);
+                        float a0, a1;
+                        f2unpack(a2, a0, a1);
+                        uint64_t ps2, th2, g2;
+                        elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                        float p0, p1, t0, t1, g0, g1;
+                        f2unpack(ps2, p0, p1);
+                        f2unpack(th2, t0, t1);
+                        f2unpack(g2, g0, g1);
+                        sp += (double)p0 + (two ? (double)p1 : 0.0);
+                        hg2 = f2add(hg2, f2pack(g0, two ? g1 : 0.f));
+                        pn[j] = t0;
+                        if (two) pn[j + 1] = t1;
+                        if (want_a) {
+                            arow[b * K + j] = a0;
+                            if (two) arow[b * K + j + 1] = a1;
+                        }
                     }
                 }
                 sps[b] = sp;
@@ -336,13 +365,15 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs 
         }
         __syncwarp();
         float4 *trow = reinterpret_cast<float4 *>(p.theta + (size_t)f * p.ld);
-        for (int q = lane; q < Kt4; q += 32) {
-            float4 tv = reinterpret_cast<const float4 *>(nbuf)[q];
-            const int k = 4 * q;
-            if (k + 1 >= Kt) tv.y = 0.f;   // (the row padding past Kt stays zero)
+        const int Ktf = Kt >> 2;   // whole float4s; a partial last one keeps the row padding zero
+        for (int q = lane; q < Ktf; q += 32) trow[q] = reinterpret_cast<const float4 *>(nbuf)[q];
+        if (Ktf < Kt4 && lane == 0) {
+            float4 tv = reinterpret_cast<const float4 *>(nbuf)[Ktf];
+            const int k = 4 * Ktf;
+            if (k + 1 >= Kt) tv.y = 0.f;
             if (k + 2 >= Kt) tv.z = 0.f;
             if (k + 3 >= Kt) tv.w = 0.f;
-            trow[q] = tv;
+            trow[Ktf] = tv;
         }
         float hg;
         {
@@ -383,25 +414,28 @@ cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
     const PipeLayout L(a.S, a.N, a.Kt);
     if (L.total <= 12 * 1024) {   // pipelined variant (configs 0-3); config 4's 32 KB rows use the other
         const size_t smem = L.total * WPB;
-        static size_t attr_p = 0;
-        if (smem > 48 * 1024 && attr_p < smem) {
-            cudaError_t e = cudaFuncSetAttribute(dirichlet_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const bool even = (a.K & 1) == 0;
+        auto kern = even ? dirichlet_pipe_kernel<true> : dirichlet_pipe_kernel<false>;
+        static size_t attr_p[2] = {0, 0};
+        if (smem > 48 * 1024 && attr_p[even] < smem) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            attr_p = smem;
+            attr_p[even] = smem;
         }
-        static int sms = 0, per_sm = 0;
-        static size_t per_sm_smem = 0;
-        if (!sms || per_sm_smem != smem) {
+        static int sms = 0, per_sm[2] = {0, 0};
+        static size_t per_sm_smem[2] = {0, 0};
+        if (!sms || per_sm_smem[even] != smem) {
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dirichlet_pipe_kernel, WPB * 32, smem);
-            if (per_sm < 1) per_sm = 1;
-            per_sm_smem = smem;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[even], kern, WPB * 32, smem);
+            if (per_sm[even] < 1) per_sm[even] = 1;
+            per_sm_smem[even] = smem;
         }
         const long long need = (a.frames + WPB - 1) / WPB;
-        const int grid = (int)(need < (long long)sms * per_sm ? need : (long long)sms * per_sm);
-        dirichlet_pipe_kernel<<<grid, WPB * 32, smem, st>>>(a);
+        const long long cap = (long long)sms * per_sm[even];
+        const int grid = (int)(need < cap ? need : cap);
+        kern<<<grid, WPB * 32, smem, st>>>(a);
         return cudaGetLastError();
     }
     const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15));

@@ -47,7 +47,8 @@ def test_psi_float32_accuracy(lo, hi, tol):
 
 
 def test_lngamma_remainder_and_gtilde():
-    """lnGamma(x) = (x - 1/2) ln x - x + ln(2 pi)/2 + u H(2u-1); g~(x) = lnG(x) - (x-1) psi(x) + x is then
+    """lnGamma(x) = (x - 1/2) ln x - x + ln(2 pi)/2 + u H(2u-1) (degree-3 H: ~3e-7, enough for the bound
+    term, whose tolerance is ~1e-3 per element); g~(x) = lnG(x) - (x-1) psi(x) + x is then
     ln(x)/2 + ln(2 pi)/2 + 1/2 + u (H - 1/2) + (u - u^2) G (the identity the Dirichlet kernel uses)."""
     txt = open(HDR).read()
     G, H = _coeffs("dig_G", txt).astype(np.float64), _coeffs("lng_H", txt).astype(np.float64)
@@ -57,7 +58,7 @@ def test_lngamma_remainder_and_gtilde():
     Gv = np.polynomial.polynomial.polyval(t, G)
     Hv = np.polynomial.polynomial.polyval(t, H)
     lng = (x - 0.5) * np.log(x) - x + 0.5 * np.log(2 * np.pi) + u * Hv
-    assert np.max(np.abs(lng - gammaln(x)) / np.maximum(1, np.abs(gammaln(x)))) < 2e-8
+    assert np.max(np.abs(lng - gammaln(x)) / np.maximum(1, np.abs(gammaln(x)))) < 5e-7
     gt = 0.5 * np.log(x) + 0.5 * np.log(2 * np.pi) + 0.5 + u * (Hv - 0.5) + (u - u * u) * Gv
     ref = gammaln(x) - (x - 1) * digamma(x) + x
     assert np.max(np.abs(gt - ref)) < 1e-6
