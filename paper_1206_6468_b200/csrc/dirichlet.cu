@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs 
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, o);
             if (!(qs > 0.f) || !(qs < INFINITY)) bad |= FLAG_NONFINITE;
-            const float gq = gamma / qs;
+            const float gq = gamma * __frcp_rn(qs);
             __syncwarp();
             for (int n = lane; n < p.N; n += 32) dvs[s * p.N + n] = fmaf(gq, dvs[s * p.N + n], 1.f);
         }
@@ -389,7 +389,10 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs 
             for (int o = 16; o > 0; o >>= 1) mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
             const double mx = (double)mxf;
             float *dst = p.ec + ((size_t)(m * p.S + s) * p.T + t) * p.N;
-            for (int n = lane; n < p.N; n += 32) dst[n] = expf((float)((double)gamma * (sps[s * p.N + n] - mx)));
+            // e = exp(gamma (phi - max)) <= 1: the difference in FP64, then one SFU exp2 (relative error of
+            // e ~ 6e-8 |gamma (phi - max)|, i.e. < 1e-6 wherever e is not negligible)
+            for (int n = lane; n < p.N; n += 32)
+                dst[n] = ex2_sfu((float)((double)gamma * (sps[s * p.N + n] - mx)) * 1.44269504088896341f);
             if (lane == 0) {
                 const double off = (double)gamma * (mx - (double)K * psi0);
                 p.eoff[(size_t)(m * p.S + s) * p.T + t] = off;
