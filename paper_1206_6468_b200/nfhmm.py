@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libnfhmm.so")
+LIB_PATH = os.environ.get("NFHMM_LIB") or os.path.join(_HERE, "lib", "libnfhmm.so")   # (override: A/B experiments)
 
 NFHMM_OK, NFHMM_EINVAL, NFHMM_ESTATE, NFHMM_ECUDA = 0, -1, -2, -3
 NFHMM_ENOMEM, NFHMM_EZEROSUPPORT, NFHMM_ENUMERIC = -4, -5, -6
