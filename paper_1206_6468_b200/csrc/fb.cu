@@ -123,7 +123,10 @@ __device__ __forceinline__ void step_products(float (&out)[FBCfg<NMAX>::NQ], flo
     xsum = hsum2(s2[0]);
 }
 
-template <int NMAX>
+// CHUNKED = false: one sequential pass over [0, T) per chain (compiled exactly for that case);
+// CHUNKED = true: phase 3 of the parallel-in-time path -- one unit per (chain, time chunk), started from
+// the exact chunk-start messages of fbp_scan_kernel.
+template <int NMAX, bool CHUNKED>
 __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
     using C = FBCfg<NMAX>;
     constexpr int CPB = C::CPB, NQ = C::NQ, CH = C::CH;
@@ -141,7 +144,11 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
     float *ech = ubuf + 2 * NMAX;
 
     const int s = blockIdx.y;
-    const int m = blockIdx.x * CPB + (warp >> 1);
+    // unit = (mixture, chunk of the time axis); one chunk [0, T) unless the parallel-in-time path
+    // (fbp_* kernels) supplies exact chunk-start messages
+    const int unit = blockIdx.x * CPB + (warp >> 1);
+    const int nchunk = CHUNKED ? p.nchunk : 1;
+    const int m = CHUNKED ? unit / nchunk : unit, chunk = CHUNKED ? unit - m * nchunk : 0;
     const float *Ag = p.trans + (size_t)s * N * N;
     for (int idx = threadIdx.x; idx < NMAX * NMAX; idx += blockDim.x) {
         const int r = idx / NMAX, c = idx - r * NMAX;
@@ -151,9 +158,10 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
     }
     for (int idx = lane; idx < 2 * NMAX; idx += 32) ubuf[idx] = 0.f;
     __syncthreads();
-    if (m >= p.M) return;
+    if (m >= p.M) return;   // (unit beyond M * nchunk)
 
     const int T = p.T;
+    const int ta = CHUNKED ? chunk * p.chunk_len : 0, tb = CHUNKED ? min(T, ta + p.chunk_len) : T;   // [ta, tb)
     const size_t chain = (size_t)m * p.S + s;
     const float *em = p.ec + chain * T * N;     // emissions e_t(n)
     unsigned bad = 0;
@@ -172,26 +180,32 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
                 Mr[REG ? q : 0][REG ? i / 2 : 0] =
                     32 * q + lane < NMAX ? pk2(M[i * NMAX + 32 * q + lane], M[(i + 1) * NMAX + 32 * q + lane]) : 0ull;
     }
-    const int nch = (T + CH - 1) / CH;
+    const int nch = (tb - ta + CH - 1) / CH;
 
     if (!backward) {
         // ---------------- forward: u_t -> p.fwd, log Z ----------------
         float *fwd = p.fwd + chain * T * N;
-        stage_rows(ech, em, N, 0, min(CH, T), lane);
+        stage_rows(ech, em, N, ta, min(CH, tb - ta), lane);
         float u[NQ];
         int esum = 0;            // sum of the power-of-two scale exponents applied
         for (int c = 0; c < nch; ++c) {
-            const int t0 = c * CH, n = min(CH, T - t0);
+            const int t0 = ta + c * CH, n = min(CH, tb - t0);
             const float *ecur = ech + (c & 1) * CH * N;
             cp_async_wait_all();
             __syncwarp();
-            if (c + 1 < nch) stage_rows(ech + ((c + 1) & 1) * CH * N, em, N, t0 + CH, min(CH, T - t0 - CH), lane);
+            if (c + 1 < nch) stage_rows(ech + ((c + 1) & 1) * CH * N, em, N, t0 + CH, min(CH, tb - t0 - CH), lane);
             for (int tt = 0; tt < n; ++tt) {
                 const int t = t0 + tt;
                 const float *et = ecur + tt * N;
-                if (t == 0) {
+                if (t == ta) {
+                    if (CHUNKED) {   // exact chunk-start message u_ta from the scan (fbp_scan_kernel)
+                        const float *f0 = p.fstart + (chain * nchunk + chunk) * NMAX;
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * et[32 * q + lane] : 0.f;
+                        for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? f0[32 * q + lane] : 0.f;
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < NQ; ++q) u[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * et[32 * q + lane] : 0.f;
+                    }
                 } else {
                     float acc[NQ], usum;
                     step_products<NMAX>(acc, usum, ubuf + ((t - 1) & 1) * NMAX, Mr, M, lane);
@@ -213,6 +227,7 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
                 __syncwarp();
             }
         }
+        if (CHUNKED) goto done;   // log Z comes from the scan (fbp_scan_kernel)
         float part = 0.f;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) part += u[q];
@@ -231,20 +246,22 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
         // ---------------- backward: b_t -> p.bwd ----------------
         float *bwd = p.bwd + chain * T * N;
         float b[NQ];
+        // b_{tb-1}: 1 at the end of the sequence, else the exact message from the scan
+        const float *b0 = CHUNKED ? p.bstart + (chain * nchunk + chunk) * NMAX : nullptr;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            b[q] = jv[q] ? 1.f : 0.f;
-            if (jv[q]) bwd[(size_t)(T - 1) * N + 32 * q + lane] = 1.f;
+            b[q] = jv[q] ? (b0 ? b0[32 * q + lane] : 1.f) : 0.f;
+            if (jv[q]) bwd[(size_t)(tb - 1) * N + 32 * q + lane] = b[q];
         }
-        // chunk c covers x_t for t in [t0, t0 + n) in descending t: needs e_{t+1}, rows t0+1 .. t0+n
+        // staging chunk c covers x_t for t in [t0, t0 + n) in descending t: needs e_{t+1}, rows t0+1 .. t0+n
         auto stage_back = [&](int cc, int buf) {
-            const int t0 = cc * CH, ne = min(CH, T - 1 - t0);
+            const int t0 = ta + cc * CH, ne = min(CH, tb - 1 - t0);
             stage_rows(ech + buf * CH * N, em, N, t0 + 1, ne, lane);
         };
-        const int ncb = (T - 1 + CH - 1) / CH;   // chunks of t in [0, T-1)
+        const int ncb = (tb - 1 - ta + CH - 1) / CH;   // staging chunks of t in [ta, tb-1)
         if (ncb > 0) stage_back(ncb - 1, (ncb - 1) & 1);
         for (int c = ncb - 1; c >= 0; --c) {
-            const int t0 = c * CH, n = min(CH, T - 1 - t0);
+            const int t0 = ta + c * CH, n = min(CH, tb - 1 - t0);
             const int buf = c & 1;
             const float *ecur = ech + buf * CH * N;   // row r holds e_{t0 + 1 + r}
             cp_async_wait_all();
@@ -270,6 +287,271 @@ __global__ void __launch_bounds__(FBCfg<NMAX>::WPB * 32) fb_kernel(FBArgs p) {
             }
         }
     }
+done:
+    if (bad) atomicOr(p.flags, bad);
+}
+
+// ---------------------------------------------------------------------------------------------------
+// Parallel-in-time forward-backward, for few chains (single-mixture configurations):
+// the time axis is cut into chunks [t0, t1) of L steps and ONE transfer matrix per chunk serves both
+// directions,  P_c = prod_{t = t0+1}^{t1-1} A diag(e_t)  (empty product = I):
+//   forward   u_{t1-1} = u_{t0} P_c,        next chunk   u_{t1} = (u_{t1-1} A) .* e_{t1};
+//   backward  b_{t0}   = P_c b_{t1-1},      previous     b_{t0-1} = A (e_{t0} .* b_{t0}).
+// Phase 1 (fbp_transfer_kernel) forms every P_c in parallel (a 128-thread CTA per chunk, 4 x 4 register
+// tiles, packed FFMA2, power-of-two rescaling by the CTA max each step, exponent kept); phase 2
+// (fbp_scan_kernel) walks the chunks once per chain and direction -- C vector-matrix products instead of
+// T dependent steps -- giving the exact chunk-start messages and log Z; phase 3 re-runs each chunk from
+// its start message in parallel (fb_kernel<NMAX, true>).  Exact up to FP32 rounding: the same products
+// in a different association order.
+constexpr int FBP_THREADS = 128;
+
+template <int NMAX>
+__global__ void __launch_bounds__(FBP_THREADS) fbp_transfer_kernel(FBArgs p, float *P, float *PT, int *PE) {
+    constexpr int NT = NMAX / 4;                      // 4 x 4 tiles per dimension
+    extern __shared__ __align__(16) float sm[];
+    float *As = sm;                                   // [NMAX][NMAX]  A[k][j]
+    float *Q[2] = {As + NMAX * NMAX, As + 2 * NMAX * NMAX};   // transposed products QT[j][i] (double buffer)
+    float *es = As + 3 * NMAX * NMAX;                 // [L][NMAX] emissions of the chunk
+    float *wmax = es + p.chunk_len * NMAX;            // [4] warp maxima
+    const int N = p.N, T = p.T, L = p.chunk_len;
+    const int c = blockIdx.x, chain = blockIdx.y, s = chain % p.S;
+    const int t0 = c * L, t1 = min(T, t0 + L);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float *Ag = p.trans + (size_t)s * N * N;
+    for (int idx = tid; idx < NMAX * NMAX; idx += FBP_THREADS) {
+        const int r = idx / NMAX, cc = idx - r * NMAX;
+        As[idx] = (r < N && cc < N) ? Ag[r * N + cc] : 0.f;
+        Q[0][idx] = (r == cc && r < N) ? 1.f : 0.f;   // I (symmetric: QT = Q)
+    }
+    const float *em = p.ec + (size_t)chain * T * N;
+    for (int idx = tid; idx < (t1 - t0) * NMAX; idx += FBP_THREADS) {
+        const int r = idx / NMAX, cc = idx - r * NMAX;
+        es[idx] = (cc < N) ? em[(size_t)(t0 + r) * N + cc] : 0.f;
+    }
+    __syncthreads();
+    int etot = 0;          // sum of the power-of-two exponents divided out
+    float pend = 1.f;      // scale still to apply to the current product (the previous step's 2^-E)
+    int cur = 0;
+    for (int t = t0 + 1; t < t1; ++t) {
+        const float *qt = Q[cur];
+        float *qn = Q[cur ^ 1];
+        const float *et = es + (t - t0) * NMAX;
+        float tmax = 0.f;
+        for (int tile = tid; tile < NT * NT; tile += FBP_THREADS) {
+            const int i0 = 4 * (tile / NT), j0 = 4 * (tile % NT);
+            uint64_t acc[4][2];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = 0ull;
+#pragma unroll 4
+            for (int k = 0; k < NMAX; ++k) {
+                const float4 qv = *reinterpret_cast<const float4 *>(qt + k * NMAX + i0);   // Q[i0..i0+3][k]
+                const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(As + k * NMAX + j0);   // A[k][j0..j0+3]
+                const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint64_t q2 = pk2(qa[r], qa[r]);
+                    fma2(acc[r][0], q2, av.x);
+                    fma2(acc[r][1], q2, av.y);
+                }
+            }
+            // Q'[i][j] = e_t[j] pend * sum_k Q[i][k] A[k][j], stored transposed
+            float o[4][4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                float a0, a1, a2, a3;
+                asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc[r][0]));
+                asm("mov.b64 {%0, %1}, %2;" : "=f"(a2), "=f"(a3) : "l"(acc[r][1]));
+                o[r][0] = a0 * et[j0 + 0] * pend;
+                o[r][1] = a1 * et[j0 + 1] * pend;
+                o[r][2] = a2 * et[j0 + 2] * pend;
+                o[r][3] = a3 * et[j0 + 3] * pend;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) tmax = fmaxf(tmax, o[r][cc]);
+            }
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc)
+                *reinterpret_cast<float4 *>(qn + (j0 + cc) * NMAX + i0) = make_float4(o[0][cc], o[1][cc], o[2][cc], o[3][cc]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        if (lane == 0) wmax[warp] = tmax;
+        __syncthreads();
+        const float mx = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]));
+        const int E = mx > 0.f ? exponent_of(mx) : 0;
+        pend = pow2_neg(E);
+        etot += E;
+        cur ^= 1;
+        __syncthreads();   // wmax is rewritten next step
+    }
+    // out: P (row-major) and PT, with the pending scale applied; exponent etot
+    const float *qt = Q[cur];
+    float *Pc = P + ((size_t)chain * p.nchunk + c) * NMAX * NMAX;
+    float *PTc = PT + ((size_t)chain * p.nchunk + c) * NMAX * NMAX;
+    for (int idx = tid; idx < NMAX * NMAX; idx += FBP_THREADS) {
+        const int j = idx / NMAX, i = idx - j * NMAX;          // qt[j][i] = P[i][j]
+        const float v = qt[idx] * pend;
+        PTc[idx] = v;
+        Pc[(size_t)i * NMAX + j] = v;
+    }
+    if (tid == 0) PE[(size_t)chain * p.nchunk + c] = etot;
+}
+
+// Phase 2: warp 0 = forward scan (chunk-start u, log Z), warp 1 = backward scan (chunk-end b).
+template <int NMAX>
+__global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, const float *PT, const int *PE,
+                                                      float *fstart, float *bstart) {
+    using C = FBCfg<NMAX>;
+    constexpr int NQ = C::NQ;
+    extern __shared__ __align__(16) float sm[];
+    float *As = sm;                                   // [NMAX][NMAX] A[i][j]
+    float *AT = As + NMAX * NMAX;                     // [NMAX][NMAX] AT[j][i]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *Pbuf = AT + NMAX * NMAX + warp * (2 * NMAX * NMAX + 2 * NMAX);   // [2][NMAX][NMAX] | x[2][NMAX]
+    float *xb = Pbuf + 2 * NMAX * NMAX;
+    const int N = p.N, T = p.T, L = p.chunk_len, nc = p.nchunk;
+    const int chain = blockIdx.x, s = chain % p.S;
+    const float *Ag = p.trans + (size_t)s * N * N;
+    for (int idx = threadIdx.x; idx < NMAX * NMAX; idx += blockDim.x) {
+        const int r = idx / NMAX, cc = idx - r * NMAX;
+        const float v = (r < N && cc < N) ? Ag[r * N + cc] : 0.f;
+        As[idx] = v;
+        AT[cc * NMAX + r] = v;
+    }
+    for (int idx = lane; idx < 2 * NMAX; idx += 32) xb[idx] = 0.f;
+    __syncthreads();
+    const float *em = p.ec + (size_t)chain * T * N;
+    bool jv[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) jv[q] = 32 * q + lane < N;
+    unsigned bad = 0;
+    // stage matrix `src` ([NMAX][NMAX]) into buffer b with 16-byte cp.async
+    auto stage = [&](const float *src, int b) {
+        float *dst = Pbuf + b * NMAX * NMAX;
+        for (int i = lane; i < NMAX * NMAX / 4; i += 32) {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 4 * i);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 4 * i));
+        }
+        cp_async_commit();
+    };
+    // x (broadcast in smem) times a column-major-by-lane matrix M(i, j) = Ms[i * NMAX + j]
+    auto vecmat = [&](const float *x, const float *Ms, float (&out)[NQ], float &xsum) {
+        uint64_t acc[NQ][2];
+        uint64_t s2[2] = {0ull, 0ull};
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q][0] = acc[q][1] = 0ull;
+        const ulonglong2 *x4 = reinterpret_cast<const ulonglong2 *>(x);
+#pragma unroll 2
+        for (int i4 = 0; i4 < NMAX / 4; ++i4) {
+            const ulonglong2 v = x4[i4];
+            add2(s2[0], v.x);
+            add2(s2[1], v.y);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int j = min(32 * q + lane, NMAX - 1), i = 4 * i4;
+                fma2(acc[q][0], v.x, pk2(Ms[i * NMAX + j], Ms[(i + 1) * NMAX + j]));
+                fma2(acc[q][1], v.y, pk2(Ms[(i + 2) * NMAX + j], Ms[(i + 3) * NMAX + j]));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            add2(acc[q][0], acc[q][1]);
+            out[q] = hsum2(acc[q][0]);
+        }
+        add2(s2[0], s2[1]);
+        xsum = hsum2(s2[0]);
+    };
+    auto put = [&](const float (&v)[NQ], int b) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if (jv[q]) xb[b * NMAX + 32 * q + lane] = v[q];
+        __syncwarp();
+    };
+    auto norm = [&](float (&v)[NQ], long long &ls) {   // rescale by 2^-E(sum v) (exact), ls += E
+        float part = 0.f;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) part += v[q];
+        const float sm_ = warp_sum(part);
+        if (!(sm_ > 0.f) || !(sm_ < INFINITY)) bad |= FLAG_NONFINITE;
+        const int E = exponent_of(sm_);
+        const float sc = pow2_neg(E);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v[q] *= sc;
+        ls += E;
+    };
+    float v[NQ];
+    long long ls = 0;
+    if (warp == 0) {
+        // forward: v = u_{t0} of chunk c
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * em[32 * q + lane] : 0.f;
+        norm(v, ls);
+        stage(P + (size_t)chain * nc * NMAX * NMAX, 0);
+        for (int c = 0; c < nc; ++c) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                if (jv[q]) fstart[((size_t)chain * nc + c) * NMAX + 32 * q + lane] = v[q];
+            cp_async_wait_all();
+            __syncwarp();
+            if (c + 1 < nc) stage(P + ((size_t)chain * nc + c + 1) * NMAX * NMAX, (c + 1) & 1);
+            float ul[NQ], xs;
+            put(v, 0);
+            vecmat(xb, Pbuf + (c & 1) * NMAX * NMAX, ul, xs);       // u_{t1-1} = u_{t0} P_c
+            ls += PE[(size_t)chain * nc + c];
+            __syncwarp();
+            if (c + 1 < nc) {
+                const int t1 = (c + 1) * L;
+                put(ul, 1);
+                float an[NQ];
+                vecmat(xb + NMAX, As, an, xs);                       // u_{t1} = (u_{t1-1} A) .* e_{t1}
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? an[q] * em[(size_t)t1 * N + 32 * q + lane] : 0.f;
+                __syncwarp();
+                norm(v, ls);
+            } else {
+                float part = 0.f;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) part += jv[q] ? ul[q] : 0.f;
+                const float us = warp_sum(part);
+                if (!(us > 0.f) || !(us < INFINITY)) bad |= FLAG_NONFINITE;
+                double offsum = 0.0;
+                for (int t = lane; t < T; t += 32) offsum += p.eoff[(size_t)chain * T + t];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) offsum += __shfl_xor_sync(0xffffffffu, offsum, o);
+                if (lane == 0) {
+                    const double lz = log((double)us) + (double)ls * 0.69314718055994530942 + offsum;
+                    p.logZ[chain] = lz;
+                    if (!isfinite(lz)) bad |= FLAG_NONFINITE;
+                }
+            }
+        }
+    } else {
+        // backward: v = b_{t1-1} of chunk c
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? 1.f : 0.f;
+        stage(PT + ((size_t)chain * nc + nc - 1) * NMAX * NMAX, (nc - 1) & 1);
+        for (int c = nc - 1; c >= 0; --c) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                if (jv[q]) bstart[((size_t)chain * nc + c) * NMAX + 32 * q + lane] = v[q];
+            if (c == 0) break;
+            cp_async_wait_all();
+            __syncwarp();
+            if (c - 1 >= 1) stage(PT + ((size_t)chain * nc + c - 1) * NMAX * NMAX, (c - 1) & 1);
+            float bf[NQ], xs;
+            put(v, 0);
+            vecmat(xb, Pbuf + (c & 1) * NMAX * NMAX, bf, xs);       // b_{t0} = P_c b_{t1-1}: (P^T)(j,i) by lane i
+            __syncwarp();
+            const int t0 = c * L;
+            float xe[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) xe[q] = jv[q] ? em[(size_t)t0 * N + 32 * q + lane] * bf[q] : 0.f;
+            put(xe, 1);
+            vecmat(xb + NMAX, AT, v, xs);                            // b_{t0-1} = A (e_{t0} .* b_{t0})
+            __syncwarp();
+            norm(v, ls);
+        }
+    }
+    cp_async_wait_all();
     if (bad) atomicOr(p.flags, bad);
 }
 
@@ -278,18 +560,54 @@ cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
     using C = FBCfg<NMAX>;
     const int N = a.N;
     const size_t smem = ((size_t)2 * NMAX * NMAX + (size_t)C::WPB * (2 * NMAX + 2 * C::CH * N)) * sizeof(float);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && attr < smem) {
-        cudaError_t e = cudaFuncSetAttribute(fb_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool chunked = a.nchunk > 1;
+    auto kern = chunked ? fb_kernel<NMAX, true> : fb_kernel<NMAX, false>;
+    static size_t attr[2] = {0, 0};
+    if (smem > 48 * 1024 && attr[chunked] < smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = smem;
+        attr[chunked] = smem;
     }
-    dim3 grid((a.M + C::CPB - 1) / C::CPB, a.S);
-    fb_kernel<NMAX><<<grid, C::WPB * 32, smem, st>>>(a);
+    if (chunked) {   // phases 1 and 2 of the parallel-in-time path (NMAX <= 64)
+        if (NMAX > 64 || !a.P || !a.PT || !a.PE) return cudaErrorInvalidValue;
+        const size_t sm1 = ((size_t)3 * NMAX * NMAX + (size_t)a.chunk_len * NMAX + 4) * sizeof(float);
+        const size_t sm2 = ((size_t)2 * NMAX * NMAX + 2 * (2 * NMAX * NMAX + 2 * NMAX)) * sizeof(float);
+        static size_t attr1 = 0, attr2 = 0;
+        if (sm1 > 48 * 1024 && attr1 < sm1) {
+            cudaError_t e = cudaFuncSetAttribute(fbp_transfer_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+            if (e != cudaSuccess) return e;
+            attr1 = sm1;
+        }
+        if (sm2 > 48 * 1024 && attr2 < sm2) {
+            cudaError_t e = cudaFuncSetAttribute(fbp_scan_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+            if (e != cudaSuccess) return e;
+            attr2 = sm2;
+        }
+        fbp_transfer_kernel<NMAX><<<dim3(a.nchunk, a.M * a.S), FBP_THREADS, sm1, st>>>(a, a.P, a.PT, a.PE);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        fbp_scan_kernel<NMAX><<<a.M * a.S, 64, sm2, st>>>(a, a.P, a.PT, a.PE, a.fstart, a.bstart);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const int units = a.M * (chunked ? a.nchunk : 1);
+    dim3 grid((units + C::CPB - 1) / C::CPB, a.S);
+    kern<<<grid, C::WPB * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 }  // namespace
+
+int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len) {
+    // Parallel in time only while the sequential recursion would leave most of the GPU idle (at most
+    // 32 chains -- e.g. single-mixture configurations), for N <= 64 (phase-2 smem) and long enough sequences.  Chunk length ~ sqrt(T): phase 1
+    // costs ~L matrix products per chunk, phase 2 ~T/L vector-matrix products per chain.
+    if (chains > 32 || N > 64 || T < 96) return 0;
+    int L = 32;
+    while (L * L < T / 2 && L < 128) L *= 2;
+    *chunk_len = L;
+    return (int)((T + L - 1) / L);
+}
 
 cudaError_t launch_fb(const FBArgs &a, cudaStream_t st) {
     const int N = a.N;

@@ -34,6 +34,10 @@ struct nfhmm {
     float *bs_a = nullptr, *bs_b = nullptr;   // tensor-core path: pre-split beta for (a) and betaT for (b)
     double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
     double *fconst = nullptr;   // per-frame alpha_0, psi(alpha_0), bound constant (set_observations)
+    // parallel-in-time forward-backward (few chains): chunks, their transfer matrices and start messages
+    int fb_nchunk = 0, fb_len = 0;
+    float *fbP = nullptr, *fbPT = nullptr, *fbF = nullptr, *fbB = nullptr;
+    int *fbE = nullptr;
     unsigned *flags = nullptr;
 
     bool have_model = false, have_obs = false, R_valid = false;
@@ -148,6 +152,14 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take(fr * (size_t)(h->nt_a > h->nt_tc_a ? h->nt_a : h->nt_tc_a) * 8); h->data_part = (double *)p;
     p = take(fr * 8);                            h->hdir = (double *)p;
     p = take(fr * 4 * 8);                        h->fconst = (double *)p;
+    {   // parallel-in-time FB scratch (NMAX <= 64 on that path)
+        const size_t units = (size_t)h->M * h->S * (size_t)h->fb_nchunk;
+        p = take(units * 64 * 64 * 4);           h->fbP = (float *)p;
+        p = take(units * 64 * 64 * 4);           h->fbPT = (float *)p;
+        p = take(units * 64 * 4);                h->fbF = (float *)p;
+        p = take(units * 64 * 4);                h->fbB = (float *)p;
+        p = take(units * 4);                     h->fbE = (int *)p;
+    }
     p = take((size_t)h->M * h->max_iters * 8);   h->fe = (double *)p;
     p = take(fr * 4);                            h->vt = (float *)p;
     p = take(fr * 4);                            h->scale = (float *)p;
@@ -273,6 +285,13 @@ int step_fb(nfhmm_t *h) {
     f.prior = h->prior;
     f.fwd = h->fwd;
     f.bwd = h->bwd;
+    f.nchunk = h->fb_nchunk;
+    f.chunk_len = h->fb_len;
+    f.P = h->fbP;
+    f.PT = h->fbPT;
+    f.PE = h->fbE;
+    f.fstart = h->fbF;
+    f.bstart = h->fbB;
     f.logZ = h->logZ;
     f.flags = h->flags;
     LAUNCH(h, NFHMM_K_FB, launch_fb(f, h->st));
@@ -370,6 +389,13 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
     h->Kb = (int)((Kt + h->bn_b - 1) / h->bn_b * h->bn_b);
     h->nt_a = h->Fa / h->bn_a;
     h->math = o.math == NFHMM_MATH_SIMT ? NFHMM_MATH_SIMT : NFHMM_MATH_TC;
+    {   // parallel-in-time forward-backward for few chains (NFHMM_FB_PARALLEL=0 disables)
+        const char *e = getenv("NFHMM_FB_PARALLEL");
+        int L = 0;
+        const int nc = (e && atoi(e) == 0) ? 0 : fb_pick_chunks(h->M * h->S, h->T, h->N, &L);
+        h->fb_nchunk = nc > 1 ? nc : 0;
+        h->fb_len = nc > 1 ? L : 0;
+    }
     h->bn_tc_a = tc_pick_bn(F);
     h->bn_tc_b = tc_pick_bn(Kt);
     h->nt_tc_a = (int)((F + h->bn_tc_a - 1) / h->bn_tc_a);

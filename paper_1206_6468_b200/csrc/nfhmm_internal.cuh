@@ -97,7 +97,16 @@ struct FBArgs {
     float *bwd;               // [M][S][T][N] out: scaled backward messages b_t (d_t = u_t .* b_t / sum)
     double *logZ;             // [M][S] out
     unsigned *flags;
+    // parallel-in-time path (fbp_*): nchunk chunks of chunk_len steps; exact chunk-start messages
+    int nchunk, chunk_len;    // nchunk <= 1: one sequential pass over [0, T)
+    float *fstart;            // [M*S][nchunk][NMAX]  u_{t0} of each chunk (scratch)
+    float *bstart;            // [M*S][nchunk][NMAX]  b_{t1-1} of each chunk (scratch)
+    float *P, *PT;            // [M*S][nchunk][NMAX][NMAX] chunk transfer matrices and transposes (scratch)
+    int *PE;                  // [M*S][nchunk] their power-of-two exponents
 };
+// Chunking of the parallel-in-time FB for a handle (0 = sequential): used when few chains would leave
+// the GPU idle during the 2T dependent steps.
+int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len);
 cudaError_t launch_fb(const FBArgs &a, cudaStream_t st);
 
 struct ElboArgs {
