@@ -22,6 +22,7 @@
 // are their FP64 per-frame offsets.  The emissions of the next CH steps are staged into shared memory
 // with cp.async (double-buffered chunks).
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <math.h>
 
 #include "nfhmm_internal.cuh"
@@ -297,117 +298,126 @@ done:
 // directions,  P_c = prod_{t = t0+1}^{t1-1} A diag(e_t)  (empty product = I):
 //   forward   u_{t1-1} = u_{t0} P_c,        next chunk   u_{t1} = (u_{t1-1} A) .* e_{t1};
 //   backward  b_{t0}   = P_c b_{t1-1},      previous     b_{t0-1} = A (e_{t0} .* b_{t0}).
-// Phase 1 (fbp_transfer_kernel) forms every P_c in parallel (a 128-thread CTA per chunk, 4 x 4 register
-// tiles, packed FFMA2, power-of-two rescaling by the CTA max each step, exponent kept); phase 2
+// Phase 1 (fbp_transfer_kernel) forms every P_c in parallel -- its rows are independent vector
+// recursions of the basis vectors, one warp each, with per-row power-of-two exponents; phase 2
 // (fbp_scan_kernel) walks the chunks once per chain and direction -- C vector-matrix products instead of
 // T dependent steps -- giving the exact chunk-start messages and log Z; phase 3 re-runs each chunk from
 // its start message in parallel (fb_kernel<NMAX, true>).  Exact up to FP32 rounding: the same products
 // in a different association order.
-constexpr int FBP_THREADS = 128;
+
+// Phase 1: row i of P_c is the forward recursion of the basis vector e_i through the chunk
+// (P'[i][:] = P[i][:] A diag(e_t)), so every row is an independent warp running the same vector step as
+// the sequential kernel (A columns in registers, broadcast through shared memory, power-of-two rescale).
+// Rows carry their own exponents PE[row] (the scan folds them in exactly); P is written row-major and
+// transposed.  Block = FBP_ROWS warps (rows) of one (chain, chunk).
+constexpr int FBP_ROWS = 4;
 
 template <int NMAX>
-__global__ void __launch_bounds__(FBP_THREADS) fbp_transfer_kernel(FBArgs p, float *P, float *PT, int *PE) {
-    constexpr int NT = NMAX / 4;                      // 4 x 4 tiles per dimension
+__global__ void __launch_bounds__(FBP_ROWS * 32) fbp_transfer_kernel(FBArgs p, float *P, float *PT, int *PE) {
+    using C = FBCfg<NMAX>;
+    constexpr int NQ = C::NQ;
     extern __shared__ __align__(16) float sm[];
-    float *As = sm;                                   // [NMAX][NMAX]  A[k][j]
-    float *Q[2] = {As + NMAX * NMAX, As + 2 * NMAX * NMAX};   // transposed products QT[j][i] (double buffer)
-    float *es = As + 3 * NMAX * NMAX;                 // [L][NMAX] emissions of the chunk
-    float *wmax = es + p.chunk_len * NMAX;            // [4] warp maxima
+    float *As = sm;                                   // [NMAX][NMAX]  A[i][j]
+    float *es = As + NMAX * NMAX;                     // [L][NMAX] emissions of the chunk
+    float *xb = es + p.chunk_len * NMAX;              // [FBP_ROWS][2][NMAX] broadcast buffers
     const int N = p.N, T = p.T, L = p.chunk_len;
-    const int c = blockIdx.x, chain = blockIdx.y, s = chain % p.S;
+    const int rows_blocks = (NMAX + FBP_ROWS - 1) / FBP_ROWS;
+    const int c = blockIdx.x / rows_blocks, rb = blockIdx.x - c * rows_blocks;
+    const int chain = blockIdx.y, s = chain % p.S;
     const int t0 = c * L, t1 = min(T, t0 + L);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = rb * FBP_ROWS + warp;
     const float *Ag = p.trans + (size_t)s * N * N;
-    for (int idx = tid; idx < NMAX * NMAX; idx += FBP_THREADS) {
+    for (int idx = threadIdx.x; idx < NMAX * NMAX; idx += blockDim.x) {
         const int r = idx / NMAX, cc = idx - r * NMAX;
         As[idx] = (r < N && cc < N) ? Ag[r * N + cc] : 0.f;
-        Q[0][idx] = (r == cc && r < N) ? 1.f : 0.f;   // I (symmetric: QT = Q)
     }
     const float *em = p.ec + (size_t)chain * T * N;
-    for (int idx = tid; idx < (t1 - t0) * NMAX; idx += FBP_THREADS) {
+    for (int idx = threadIdx.x; idx < (t1 - t0) * NMAX; idx += blockDim.x) {
         const int r = idx / NMAX, cc = idx - r * NMAX;
         es[idx] = (cc < N) ? em[(size_t)(t0 + r) * N + cc] : 0.f;
     }
+    float *bx = xb + warp * 2 * NMAX;
+    for (int idx = lane; idx < 2 * NMAX; idx += 32) bx[idx] = 0.f;
     __syncthreads();
-    int etot = 0;          // sum of the power-of-two exponents divided out
-    float pend = 1.f;      // scale still to apply to the current product (the previous step's 2^-E)
-    int cur = 0;
-    for (int t = t0 + 1; t < t1; ++t) {
-        const float *qt = Q[cur];
-        float *qn = Q[cur ^ 1];
-        const float *et = es + (t - t0) * NMAX;
-        float tmax = 0.f;
-        for (int tile = tid; tile < NT * NT; tile += FBP_THREADS) {
-            const int i0 = 4 * (tile / NT), j0 = 4 * (tile % NT);
-            uint64_t acc[4][2];
+    if (row >= NMAX) return;
+    bool jv[NQ];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) acc[r][0] = acc[r][1] = 0ull;
-#pragma unroll 4
-            for (int k = 0; k < NMAX; ++k) {
-                const float4 qv = *reinterpret_cast<const float4 *>(qt + k * NMAX + i0);   // Q[i0..i0+3][k]
-                const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(As + k * NMAX + j0);   // A[k][j0..j0+3]
-                const float qa[4] = {qv.x, qv.y, qv.z, qv.w};
+    for (int q = 0; q < NQ; ++q) jv[q] = 32 * q + lane < N;
+    uint64_t Mr[C::REG ? NQ : 1][C::REG ? NMAX / 2 : 1];
+    if (C::REG) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const uint64_t q2 = pk2(qa[r], qa[r]);
-                    fma2(acc[r][0], q2, av.x);
-                    fma2(acc[r][1], q2, av.y);
-                }
-            }
-            // Q'[i][j] = e_t[j] pend * sum_k Q[i][k] A[k][j], stored transposed
-            float o[4][4];
+        for (int q = 0; q < NQ; ++q)
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                float a0, a1, a2, a3;
-                asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc[r][0]));
-                asm("mov.b64 {%0, %1}, %2;" : "=f"(a2), "=f"(a3) : "l"(acc[r][1]));
-                o[r][0] = a0 * et[j0 + 0] * pend;
-                o[r][1] = a1 * et[j0 + 1] * pend;
-                o[r][2] = a2 * et[j0 + 2] * pend;
-                o[r][3] = a3 * et[j0 + 3] * pend;
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) tmax = fmaxf(tmax, o[r][cc]);
-            }
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc)
-                *reinterpret_cast<float4 *>(qn + (j0 + cc) * NMAX + i0) = make_float4(o[0][cc], o[1][cc], o[2][cc], o[3][cc]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-        if (lane == 0) wmax[warp] = tmax;
-        __syncthreads();
-        const float mx = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]));
-        const int E = mx > 0.f ? exponent_of(mx) : 0;
-        pend = pow2_neg(E);
-        etot += E;
-        cur ^= 1;
-        __syncthreads();   // wmax is rewritten next step
+            for (int i = 0; i < NMAX; i += 2)
+                Mr[C::REG ? q : 0][C::REG ? i / 2 : 0] =
+                    32 * q + lane < NMAX ? pk2(As[i * NMAX + 32 * q + lane], As[(i + 1) * NMAX + 32 * q + lane]) : 0ull;
     }
-    // out: P (row-major) and PT, with the pending scale applied; exponent etot
-    const float *qt = Q[cur];
+    float v[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = (32 * q + lane == row && row < N) ? 1.f : 0.f;
+    int etot = 0;
+    for (int t = t0 + 1; t < t1; ++t) {
+        float *un = bx + ((t - t0) & 1) * NMAX;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if (jv[q]) un[32 * q + lane] = v[q];
+        __syncwarp();
+        float acc[NQ], xs;
+        step_products<NMAX>(acc, xs, un, Mr, As, lane);
+        // row of a state no path leaves (or a padded row): stays zero, no rescale
+        const int E = xs > 0.f ? exponent_of(xs) : 0;
+        const float sc = pow2_neg(E);
+        etot += E;
+        const float *et = es + (t - t0) * NMAX;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? acc[q] * et[32 * q + lane] * sc : 0.f;
+    }
+    // the exponents of the first step's input were 0 (a basis vector); the last step's output carries
+    // the scale of its input sum only: fold the row's remaining magnitude into etot via one more rescale
+    float part = 0.f;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) part += v[q];
+    const float rs = warp_sum(part);
+    const int E = rs > 0.f ? exponent_of(rs) : 0;
+    const float sc = pow2_neg(E);
+    etot += E;
     float *Pc = P + ((size_t)chain * p.nchunk + c) * NMAX * NMAX;
     float *PTc = PT + ((size_t)chain * p.nchunk + c) * NMAX * NMAX;
-    for (int idx = tid; idx < NMAX * NMAX; idx += FBP_THREADS) {
-        const int j = idx / NMAX, i = idx - j * NMAX;          // qt[j][i] = P[i][j]
-        const float v = qt[idx] * pend;
-        PTc[idx] = v;
-        Pc[(size_t)i * NMAX + j] = v;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int j = 32 * q + lane;
+        if (j < NMAX) {
+            const float x = jv[q] ? v[q] * sc : 0.f;
+            Pc[(size_t)row * NMAX + j] = x;
+            PTc[(size_t)j * NMAX + row] = x;
+        }
     }
-    if (tid == 0) PE[(size_t)chain * p.nchunk + c] = etot;
+    if (lane == 0) PE[((size_t)chain * p.nchunk + c) * NMAX + row] = etot;
 }
 
-// Phase 2: warp 0 = forward scan (chunk-start u, log Z), warp 1 = backward scan (chunk-end b).
+// Phase 2: warp 0 = forward scan (chunk-start u, log Z), warp 1 = backward scan (chunk-end b).  Each
+// chunk's inputs -- P_c (forward) or P_c^T (backward), its row exponents and the emission row that links
+// to the neighbouring chunk -- arrive together in a FBP_RING-deep cp.async ring, so the walk over the
+// chunks is bound by its own arithmetic rather than by one L2 round trip per chunk.
+constexpr int FBP_RING = 4;
+
+template <int NMAX>
+struct ScanSlot {   // floats: P [NMAX][NMAX] | exponents [NMAX] (int bits) | emission row [NMAX]
+    static constexpr int FLOATS = NMAX * NMAX + 2 * NMAX;
+};
+
 template <int NMAX>
 __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, const float *PT, const int *PE,
                                                       float *fstart, float *bstart) {
     using C = FBCfg<NMAX>;
-    constexpr int NQ = C::NQ;
+    constexpr int NQ = C::NQ, SLOT = ScanSlot<NMAX>::FLOATS;
     extern __shared__ __align__(16) float sm[];
     float *As = sm;                                   // [NMAX][NMAX] A[i][j]
     float *AT = As + NMAX * NMAX;                     // [NMAX][NMAX] AT[j][i]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float *Pbuf = AT + NMAX * NMAX + warp * (2 * NMAX * NMAX + 2 * NMAX);   // [2][NMAX][NMAX] | x[2][NMAX]
-    float *xb = Pbuf + 2 * NMAX * NMAX;
+    float *ring = AT + NMAX * NMAX + warp * (FBP_RING * SLOT + 2 * NMAX);
+    float *xb = ring + FBP_RING * SLOT;               // broadcast buffers [2][NMAX]
     const int N = p.N, T = p.T, L = p.chunk_len, nc = p.nchunk;
     const int chain = blockIdx.x, s = chain % p.S;
     const float *Ag = p.trans + (size_t)s * N * N;
@@ -418,33 +428,38 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
         AT[cc * NMAX + r] = v;
     }
     for (int idx = lane; idx < 2 * NMAX; idx += 32) xb[idx] = 0.f;
+    for (int idx = lane; idx < FBP_RING * SLOT; idx += 32) ring[idx] = 0.f;   // (padded emission entries)
     __syncthreads();
     const float *em = p.ec + (size_t)chain * T * N;
     bool jv[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) jv[q] = 32 * q + lane < N;
     unsigned bad = 0;
-    // stage matrix `src` ([NMAX][NMAX]) into buffer b with 16-byte cp.async
-    auto stage = [&](const float *src, int b) {
-        float *dst = Pbuf + b * NMAX * NMAX;
+    const bool fwd = warp == 0;
+    // slot for chunk c: matrix, row exponents, linking emission row (forward: e_{t1}; backward: e_{t0})
+    auto stage = [&](int c) {
+        float *dst = ring + (c % FBP_RING) * SLOT;
+        const float *src = (fwd ? P : PT) + ((size_t)chain * nc + c) * NMAX * NMAX;
         for (int i = lane; i < NMAX * NMAX / 4; i += 32) {
             const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 4 * i);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 4 * i));
         }
+        const int *pe = PE + ((size_t)chain * nc + c) * NMAX;
+        for (int i = lane; i < NMAX; i += 32) cp_async4(dst + NMAX * NMAX + i, reinterpret_cast<const float *>(pe + i));
+        const int te = fwd ? (c + 1) * L : c * L;
+        if (te < T)
+            for (int i = lane; i < N; i += 32) cp_async4(dst + NMAX * NMAX + NMAX + i, em + (size_t)te * N + i);
         cp_async_commit();
     };
-    // x (broadcast in smem) times a column-major-by-lane matrix M(i, j) = Ms[i * NMAX + j]
-    auto vecmat = [&](const float *x, const float *Ms, float (&out)[NQ], float &xsum) {
+    // x (broadcast in smem) times M(i, j) = Ms[i * NMAX + j], lane-owned columns j
+    auto vecmat = [&](const float *x, const float *Ms, float (&out)[NQ]) {
         uint64_t acc[NQ][2];
-        uint64_t s2[2] = {0ull, 0ull};
 #pragma unroll
         for (int q = 0; q < NQ; ++q) acc[q][0] = acc[q][1] = 0ull;
         const ulonglong2 *x4 = reinterpret_cast<const ulonglong2 *>(x);
 #pragma unroll 2
         for (int i4 = 0; i4 < NMAX / 4; ++i4) {
             const ulonglong2 v = x4[i4];
-            add2(s2[0], v.x);
-            add2(s2[1], v.y);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const int j = min(32 * q + lane, NMAX - 1), i = 4 * i4;
@@ -457,10 +472,9 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
             add2(acc[q][0], acc[q][1]);
             out[q] = hsum2(acc[q][0]);
         }
-        add2(s2[0], s2[1]);
-        xsum = hsum2(s2[0]);
     };
     auto put = [&](const float (&v)[NQ], int b) {
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < NQ; ++q)
             if (jv[q]) xb[b * NMAX + 32 * q + lane] = v[q];
@@ -478,39 +492,59 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
         for (int q = 0; q < NQ; ++q) v[q] *= sc;
         ls += E;
     };
-    float v[NQ];
+    // per-row exponents of the slot's matrix (row i stored as P~[i][:] 2^-E_i): w = 2^(E_i - Emax), Emax
+    auto row_scales = [&](const float *slot, float (&w)[NQ]) {
+        const int *pe = reinterpret_cast<const int *>(slot + NMAX * NMAX);
+        int e[NQ], emax = INT_MIN;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            e[q] = jv[q] ? pe[32 * q + lane] : INT_MIN;
+            emax = max(emax, e[q]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int d = jv[q] ? e[q] - emax : -1000;
+            w[q] = d < -126 ? 0.f : __uint_as_float((uint32_t)(127 + d) << 23);
+        }
+        return emax;
+    };
+    float v[NQ], w[NQ], y[NQ];
     long long ls = 0;
-    if (warp == 0) {
-        // forward: v = u_{t0} of chunk c
+    const int npre = min(FBP_RING - 1, nc);
+    if (fwd) {
+        for (int c = 0; c < npre; ++c) stage(c);
 #pragma unroll
         for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * em[32 * q + lane] : 0.f;
         norm(v, ls);
-        stage(P + (size_t)chain * nc * NMAX * NMAX, 0);
         for (int c = 0; c < nc; ++c) {
+            // v = u_{t0} of chunk c
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
                 if (jv[q]) fstart[((size_t)chain * nc + c) * NMAX + 32 * q + lane] = v[q];
-            cp_async_wait_all();
+            if (c + FBP_RING - 1 < nc) stage(c + FBP_RING - 1);
+            else cp_async_commit();
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(FBP_RING - 1));
             __syncwarp();
-            if (c + 1 < nc) stage(P + ((size_t)chain * nc + c + 1) * NMAX * NMAX, (c + 1) & 1);
-            float ul[NQ], xs;
-            put(v, 0);
-            vecmat(xb, Pbuf + (c & 1) * NMAX * NMAX, ul, xs);       // u_{t1-1} = u_{t0} P_c
-            ls += PE[(size_t)chain * nc + c];
-            __syncwarp();
-            if (c + 1 < nc) {
-                const int t1 = (c + 1) * L;
-                put(ul, 1);
-                float an[NQ];
-                vecmat(xb + NMAX, As, an, xs);                       // u_{t1} = (u_{t1-1} A) .* e_{t1}
+            const float *slot = ring + (c % FBP_RING) * SLOT;
+            ls += row_scales(slot, w);
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? an[q] * em[(size_t)t1 * N + 32 * q + lane] : 0.f;
-                __syncwarp();
+            for (int q = 0; q < NQ; ++q) w[q] *= v[q];
+            put(w, 0);
+            vecmat(xb, slot, y);                                    // u_{t1-1} = u_{t0} P_c
+            if (c + 1 < nc) {
+                put(y, 1);
+                float an[NQ];
+                vecmat(xb + NMAX, As, an);                          // u_{t1} = (u_{t1-1} A) .* e_{t1}
+                const float *e1 = slot + NMAX * NMAX + NMAX;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? an[q] * e1[32 * q + lane] : 0.f;
                 norm(v, ls);
             } else {
                 float part = 0.f;
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) part += jv[q] ? ul[q] : 0.f;
+                for (int q = 0; q < NQ; ++q) part += jv[q] ? y[q] : 0.f;
                 const float us = warp_sum(part);
                 if (!(us > 0.f) || !(us < INFINITY)) bad |= FLAG_NONFINITE;
                 double offsum = 0.0;
@@ -525,29 +559,31 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
             }
         }
     } else {
-        // backward: v = b_{t1-1} of chunk c
+        // chunks in descending order: ring position k holds chunk nc - 1 - k
+        auto cid = [&](int k) { return nc - 1 - k; };
+        for (int k = 0; k < npre; ++k) stage(cid(k));
 #pragma unroll
         for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? 1.f : 0.f;
-        stage(PT + ((size_t)chain * nc + nc - 1) * NMAX * NMAX, (nc - 1) & 1);
-        for (int c = nc - 1; c >= 0; --c) {
+        for (int k = 0; k < nc; ++k) {
+            const int c = cid(k);
+            // v = b_{t1-1} of chunk c
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
                 if (jv[q]) bstart[((size_t)chain * nc + c) * NMAX + 32 * q + lane] = v[q];
+            if (k + FBP_RING - 1 < nc) stage(cid(k + FBP_RING - 1));
+            else cp_async_commit();
             if (c == 0) break;
-            cp_async_wait_all();
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(FBP_RING - 1));
             __syncwarp();
-            if (c - 1 >= 1) stage(PT + ((size_t)chain * nc + c - 1) * NMAX * NMAX, (c - 1) & 1);
-            float bf[NQ], xs;
+            const float *slot = ring + (c % FBP_RING) * SLOT;
             put(v, 0);
-            vecmat(xb, Pbuf + (c & 1) * NMAX * NMAX, bf, xs);       // b_{t0} = P_c b_{t1-1}: (P^T)(j,i) by lane i
-            __syncwarp();
-            const int t0 = c * L;
-            float xe[NQ];
+            vecmat(xb, slot, y);                                    // b_{t0} = P_c b_{t1-1} (slot holds P^T)
+            ls += row_scales(slot, w);
+            const float *e0 = slot + NMAX * NMAX + NMAX;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) xe[q] = jv[q] ? em[(size_t)t0 * N + 32 * q + lane] * bf[q] : 0.f;
-            put(xe, 1);
-            vecmat(xb + NMAX, AT, v, xs);                            // b_{t0-1} = A (e_{t0} .* b_{t0})
-            __syncwarp();
+            for (int q = 0; q < NQ; ++q) y[q] = jv[q] ? y[q] * w[q] * e0[32 * q + lane] : 0.f;
+            put(y, 1);
+            vecmat(xb + NMAX, AT, v);                               // b_{t0-1} = A (e_{t0} .* b_{t0})
             norm(v, ls);
         }
     }
@@ -570,8 +606,8 @@ cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
     }
     if (chunked) {   // phases 1 and 2 of the parallel-in-time path (NMAX <= 64)
         if (NMAX > 64 || !a.P || !a.PT || !a.PE) return cudaErrorInvalidValue;
-        const size_t sm1 = ((size_t)3 * NMAX * NMAX + (size_t)a.chunk_len * NMAX + 4) * sizeof(float);
-        const size_t sm2 = ((size_t)2 * NMAX * NMAX + 2 * (2 * NMAX * NMAX + 2 * NMAX)) * sizeof(float);
+        const size_t sm1 = ((size_t)NMAX * NMAX + (size_t)a.chunk_len * NMAX + FBP_ROWS * 2 * NMAX) * sizeof(float);
+        const size_t sm2 = ((size_t)2 * NMAX * NMAX + 2 * ((size_t)FBP_RING * ScanSlot<NMAX>::FLOATS + 2 * NMAX)) * sizeof(float);
         static size_t attr1 = 0, attr2 = 0;
         if (sm1 > 48 * 1024 && attr1 < sm1) {
             cudaError_t e = cudaFuncSetAttribute(fbp_transfer_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
@@ -583,7 +619,8 @@ cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
             if (e != cudaSuccess) return e;
             attr2 = sm2;
         }
-        fbp_transfer_kernel<NMAX><<<dim3(a.nchunk, a.M * a.S), FBP_THREADS, sm1, st>>>(a, a.P, a.PT, a.PE);
+        const int rows_blocks = (NMAX + FBP_ROWS - 1) / FBP_ROWS;
+        fbp_transfer_kernel<NMAX><<<dim3(a.nchunk * rows_blocks, a.M * a.S), FBP_ROWS * 32, sm1, st>>>(a, a.P, a.PT, a.PE);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         fbp_scan_kernel<NMAX><<<a.M * a.S, 64, sm2, st>>>(a, a.P, a.PT, a.PE, a.fstart, a.bstart);

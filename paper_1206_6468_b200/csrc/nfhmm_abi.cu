@@ -158,7 +158,7 @@ size_t carve(nfhmm_t *h, char *base) {
         p = take(units * 64 * 64 * 4);           h->fbPT = (float *)p;
         p = take(units * 64 * 4);                h->fbF = (float *)p;
         p = take(units * 64 * 4);                h->fbB = (float *)p;
-        p = take(units * 4);                     h->fbE = (int *)p;
+        p = take(units * 64 * 4);                h->fbE = (int *)p;
     }
     p = take((size_t)h->M * h->max_iters * 8);   h->fe = (double *)p;
     p = take(fr * 4);                            h->vt = (float *)p;

@@ -102,7 +102,7 @@ struct FBArgs {
     float *fstart;            // [M*S][nchunk][NMAX]  u_{t0} of each chunk (scratch)
     float *bstart;            // [M*S][nchunk][NMAX]  b_{t1-1} of each chunk (scratch)
     float *P, *PT;            // [M*S][nchunk][NMAX][NMAX] chunk transfer matrices and transposes (scratch)
-    int *PE;                  // [M*S][nchunk] their power-of-two exponents
+    int *PE;                  // [M*S][nchunk][NMAX] per-row power-of-two exponents of P
 };
 // Chunking of the parallel-in-time FB for a handle (0 = sequential): used when few chains would leave
 // the GPU idle during the 2T dependent steps.
