@@ -416,9 +416,11 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
     float *As = sm;                                   // [NMAX][NMAX] A[i][j]
     float *AT = As + NMAX * NMAX;                     // [NMAX][NMAX] AT[j][i]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float *ring = AT + NMAX * NMAX + warp * (FBP_RING * SLOT + 2 * NMAX);
+    const int nc = p.nchunk;
+    float *wall = AT + NMAX * NMAX + warp * ((size_t)nc * NMAX + FBP_RING * SLOT + 2 * NMAX);   // [nc][NMAX]
+    float *ring = wall + (size_t)nc * NMAX;
     float *xb = ring + FBP_RING * SLOT;               // broadcast buffers [2][NMAX]
-    const int N = p.N, T = p.T, L = p.chunk_len, nc = p.nchunk;
+    const int N = p.N, T = p.T, L = p.chunk_len;
     const int chain = blockIdx.x, s = chain % p.S;
     const float *Ag = p.trans + (size_t)s * N * N;
     for (int idx = threadIdx.x; idx < NMAX * NMAX; idx += blockDim.x) {
@@ -436,7 +438,37 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
     for (int q = 0; q < NQ; ++q) jv[q] = 32 * q + lane < N;
     unsigned bad = 0;
     const bool fwd = warp == 0;
-    // slot for chunk c: matrix, row exponents, linking emission row (forward: e_{t1}; backward: e_{t0})
+    const float *M = fwd ? As : AT;                   // the linking step: u A (forward), A x (backward)
+    uint64_t Mr[C::REG ? NQ : 1][C::REG ? NMAX / 2 : 1];
+    if (C::REG) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int i = 0; i < NMAX; i += 2)
+                Mr[C::REG ? q : 0][C::REG ? i / 2 : 0] =
+                    32 * q + lane < NMAX ? pk2(M[i * NMAX + 32 * q + lane], M[(i + 1) * NMAX + 32 * q + lane]) : 0ull;
+    }
+    // every chunk's row scales w[c][i] = 2^(E_i - Emax_c) up front (independent of the messages), with the
+    // total of the Emax_c (forward: chunks 0..nc-1; backward: nc-1..1) kept for log Z
+    long long ls = 0;
+    for (int c = 0; c < nc; ++c) {
+        const int *pe = PE + ((size_t)chain * nc + c) * NMAX;
+        int e[NQ], emax = INT_MIN;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            e[q] = jv[q] ? pe[32 * q + lane] : INT_MIN;
+            emax = max(emax, e[q]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int d = jv[q] ? e[q] - emax : -1000;
+            if (32 * q + lane < NMAX) wall[c * NMAX + 32 * q + lane] = d < -126 ? 0.f : __uint_as_float((uint32_t)(127 + d) << 23);
+        }
+        if (fwd || c > 0) ls += emax;
+    }
+    // slot for chunk c: matrix, (unused exponent row), linking emission row (forward e_{t1}; backward e_{t0})
     auto stage = [&](int c) {
         float *dst = ring + (c % FBP_RING) * SLOT;
         const float *src = (fwd ? P : PT) + ((size_t)chain * nc + c) * NMAX * NMAX;
@@ -444,22 +476,23 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
             const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 4 * i);
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + 4 * i));
         }
-        const int *pe = PE + ((size_t)chain * nc + c) * NMAX;
-        for (int i = lane; i < NMAX; i += 32) cp_async4(dst + NMAX * NMAX + i, reinterpret_cast<const float *>(pe + i));
         const int te = fwd ? (c + 1) * L : c * L;
         if (te < T)
             for (int i = lane; i < N; i += 32) cp_async4(dst + NMAX * NMAX + NMAX + i, em + (size_t)te * N + i);
         cp_async_commit();
     };
-    // x (broadcast in smem) times M(i, j) = Ms[i * NMAX + j], lane-owned columns j
-    auto vecmat = [&](const float *x, const float *Ms, float (&out)[NQ]) {
+    // x (broadcast in smem) times the slot matrix Ms (lane-owned columns); xsum = sum of x
+    auto vecmat = [&](const float *x, const float *Ms, float (&out)[NQ], float &xsum) {
         uint64_t acc[NQ][2];
+        uint64_t s2[2] = {0ull, 0ull};
 #pragma unroll
         for (int q = 0; q < NQ; ++q) acc[q][0] = acc[q][1] = 0ull;
         const ulonglong2 *x4 = reinterpret_cast<const ulonglong2 *>(x);
 #pragma unroll 2
         for (int i4 = 0; i4 < NMAX / 4; ++i4) {
             const ulonglong2 v = x4[i4];
+            add2(s2[0], v.x);
+            add2(s2[1], v.y);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const int j = min(32 * q + lane, NMAX - 1), i = 4 * i4;
@@ -472,6 +505,8 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
             add2(acc[q][0], acc[q][1]);
             out[q] = hsum2(acc[q][0]);
         }
+        add2(s2[0], s2[1]);
+        xsum = hsum2(s2[0]);
     };
     auto put = [&](const float (&v)[NQ], int b) {
         __syncwarp();
@@ -480,46 +515,26 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
             if (jv[q]) xb[b * NMAX + 32 * q + lane] = v[q];
         __syncwarp();
     };
-    auto norm = [&](float (&v)[NQ], long long &ls) {   // rescale by 2^-E(sum v) (exact), ls += E
-        float part = 0.f;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) part += v[q];
-        const float sm_ = warp_sum(part);
-        if (!(sm_ > 0.f) || !(sm_ < INFINITY)) bad |= FLAG_NONFINITE;
-        const int E = exponent_of(sm_);
-        const float sc = pow2_neg(E);
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) v[q] *= sc;
-        ls += E;
-    };
-    // per-row exponents of the slot's matrix (row i stored as P~[i][:] 2^-E_i): w = 2^(E_i - Emax), Emax
-    auto row_scales = [&](const float *slot, float (&w)[NQ]) {
-        const int *pe = reinterpret_cast<const int *>(slot + NMAX * NMAX);
-        int e[NQ], emax = INT_MIN;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            e[q] = jv[q] ? pe[32 * q + lane] : INT_MIN;
-            emax = max(emax, e[q]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const int d = jv[q] ? e[q] - emax : -1000;
-            w[q] = d < -126 ? 0.f : __uint_as_float((uint32_t)(127 + d) << 23);
-        }
-        return emax;
-    };
-    float v[NQ], w[NQ], y[NQ];
-    long long ls = 0;
+    float v[NQ], y[NQ];
     const int npre = min(FBP_RING - 1, nc);
     if (fwd) {
         for (int c = 0; c < npre; ++c) stage(c);
+        float part = 0.f;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * em[32 * q + lane] : 0.f;
-        norm(v, ls);
+        for (int q = 0; q < NQ; ++q) {
+            v[q] = jv[q] ? p.prior[s * N + 32 * q + lane] * em[32 * q + lane] : 0.f;
+            part += v[q];
+        }
+        {   // u_0 normalised exactly once; later rescales come from the lane-local input sums
+            const float s0 = warp_sum(part);
+            const int E = exponent_of(s0);
+            const float sc = pow2_neg(E);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) v[q] *= sc;
+            ls += E;
+        }
         for (int c = 0; c < nc; ++c) {
-            // v = u_{t0} of chunk c
+            // v = u_{t0} of chunk c (scaled)
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
                 if (jv[q]) fstart[((size_t)chain * nc + c) * NMAX + 32 * q + lane] = v[q];
@@ -528,24 +543,27 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
             asm volatile("cp.async.wait_group %0;\n" ::"n"(FBP_RING - 1));
             __syncwarp();
             const float *slot = ring + (c % FBP_RING) * SLOT;
-            ls += row_scales(slot, w);
+            float w[NQ], xs;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) w[q] *= v[q];
+            for (int q = 0; q < NQ; ++q) w[q] = jv[q] ? v[q] * wall[c * NMAX + 32 * q + lane] : 0.f;
             put(w, 0);
-            vecmat(xb, slot, y);                                    // u_{t1-1} = u_{t0} P_c
+            vecmat(xb, slot, y, xs);                               // u_{t1-1} = u_{t0} P_c (row-scaled)
             if (c + 1 < nc) {
                 put(y, 1);
-                float an[NQ];
-                vecmat(xb + NMAX, As, an);                          // u_{t1} = (u_{t1-1} A) .* e_{t1}
+                float an[NQ], ys;
+                step_products<NMAX>(an, ys, xb + NMAX, Mr, M, lane);   // u_{t1} = (u_{t1-1} A) .* e_{t1}
+                const int E = exponent_of(ys);                     // rescale by the input's sum
+                const float sc = pow2_neg(E);
+                ls += E;
                 const float *e1 = slot + NMAX * NMAX + NMAX;
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? an[q] * e1[32 * q + lane] : 0.f;
-                norm(v, ls);
+                for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? an[q] * e1[32 * q + lane] * sc : 0.f;
+                if (!(ys > 0.f) || !(ys < INFINITY)) bad |= FLAG_NONFINITE;
             } else {
-                float part = 0.f;
+                float part2 = 0.f;
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) part += jv[q] ? y[q] : 0.f;
-                const float us = warp_sum(part);
+                for (int q = 0; q < NQ; ++q) part2 += jv[q] ? y[q] : 0.f;
+                const float us = warp_sum(part2);
                 if (!(us > 0.f) || !(us < INFINITY)) bad |= FLAG_NONFINITE;
                 double offsum = 0.0;
                 for (int t = lane; t < T; t += 32) offsum += p.eoff[(size_t)chain * T + t];
@@ -566,7 +584,7 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
         for (int q = 0; q < NQ; ++q) v[q] = jv[q] ? 1.f : 0.f;
         for (int k = 0; k < nc; ++k) {
             const int c = cid(k);
-            // v = b_{t1-1} of chunk c
+            // v = b_{t1-1} of chunk c (scaled)
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
                 if (jv[q]) bstart[((size_t)chain * nc + c) * NMAX + 32 * q + lane] = v[q];
@@ -576,15 +594,18 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
             asm volatile("cp.async.wait_group %0;\n" ::"n"(FBP_RING - 1));
             __syncwarp();
             const float *slot = ring + (c % FBP_RING) * SLOT;
+            float xs;
             put(v, 0);
-            vecmat(xb, slot, y);                                    // b_{t0} = P_c b_{t1-1} (slot holds P^T)
-            ls += row_scales(slot, w);
+            vecmat(xb, slot, y, xs);                               // b_{t0} = P_c b_{t1-1} (slot holds P^T)
+            const int E = exponent_of(xs);                         // rescale by the input's sum
+            const float sc = pow2_neg(E);
+            if (!(xs > 0.f) || !(xs < INFINITY)) bad |= FLAG_NONFINITE;
             const float *e0 = slot + NMAX * NMAX + NMAX;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) y[q] = jv[q] ? y[q] * w[q] * e0[32 * q + lane] : 0.f;
+            for (int q = 0; q < NQ; ++q) y[q] = jv[q] ? y[q] * wall[c * NMAX + 32 * q + lane] * e0[32 * q + lane] * sc : 0.f;
             put(y, 1);
-            vecmat(xb + NMAX, AT, v);                               // b_{t0-1} = A (e_{t0} .* b_{t0})
-            norm(v, ls);
+            float ys;
+            step_products<NMAX>(v, ys, xb + NMAX, Mr, M, lane);   // b_{t0-1} = A (e_{t0} .* b_{t0})
         }
     }
     cp_async_wait_all();
@@ -607,7 +628,8 @@ cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
     if (chunked) {   // phases 1 and 2 of the parallel-in-time path (NMAX <= 64)
         if (NMAX > 64 || !a.P || !a.PT || !a.PE) return cudaErrorInvalidValue;
         const size_t sm1 = ((size_t)NMAX * NMAX + (size_t)a.chunk_len * NMAX + FBP_ROWS * 2 * NMAX) * sizeof(float);
-        const size_t sm2 = ((size_t)2 * NMAX * NMAX + 2 * ((size_t)FBP_RING * ScanSlot<NMAX>::FLOATS + 2 * NMAX)) * sizeof(float);
+        const size_t sm2 = ((size_t)2 * NMAX * NMAX +
+                            2 * ((size_t)a.nchunk * NMAX + (size_t)FBP_RING * ScanSlot<NMAX>::FLOATS + 2 * NMAX)) * sizeof(float);
         static size_t attr1 = 0, attr2 = 0;
         if (sm1 > 48 * 1024 && attr1 < sm1) {
             cudaError_t e = cudaFuncSetAttribute(fbp_transfer_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
