@@ -181,3 +181,19 @@ def test_bench_kernel_instrumentation_resets_state():
     h.close()
     for key in ("d_hat", "alpha_hat", "V_hat", "free_energy"):
         np.testing.assert_array_equal(out[key], ref[key], err_msg=key)
+
+
+@pytest.mark.parametrize("c,over", [(1, dict(T=400)), (2, dict(T=333)), (3, dict(T=250, M=2))])
+def test_parallel_in_time_fb_matches_sequential(c, over, monkeypatch):
+    """the chunked (parallel-in-time) forward-backward that few-chain handles use agrees with
+    the sequential recursion (same products, another association order) and with the oracle."""
+    cfg, model, V = make_inputs(c, **over)
+    par = run_gpu(cfg, model, V, 6)
+    monkeypatch.setenv("NFHMM_FB_PARALLEL", "0")
+    seq = run_gpu(cfg, model, V, 6)
+    for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
+        assert rel_l2(par[key], seq[key]) <= 2e-6, key
+    assert np.all(np.abs(par["free_energy"] - seq["free_energy"]) <= 1e-7 * np.abs(seq["free_energy"]))
+    o = run_oracle(cfg, model, V[0], 6)
+    assert rel_l2(par["V_star"][0], o["V_star"]) <= TOL_VSTAR
+    assert np.all(np.abs(par["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
