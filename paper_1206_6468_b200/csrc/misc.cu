@@ -17,9 +17,13 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // (g) L_i[m] = sum_t (sum_tiles data_part[t] + hdir[t]) + sum_s log Z[m][s] + T c_prior   (DESIGN R8)
 // One CTA per mixture, fixed-order FP64 reduction: bitwise independent of how mixtures are sharded.
+// The sweep index comes from a device counter (so that a CUDA graph of one sweep can be replayed): every
+// block reads it, and the last block to finish advances it.
 __global__ void __launch_bounds__(256) elbo_kernel(ElboArgs p) {
     __shared__ double scratch[8];
+    __shared__ bool last;
     const int m = blockIdx.x;
+    const int iter = *p.iter_ctr;
     double acc = 0.0;
     for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
         const size_t f = (size_t)m * p.T + t;
@@ -35,7 +39,14 @@ __global__ void __launch_bounds__(256) elbo_kernel(ElboArgs p) {
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += scratch[w];
         for (int k = 0; k < p.S; ++k) s += p.logZ[(size_t)m * p.S + k];
         s += p.c_prior_T;
-        p.fe[(size_t)m * p.max_iters + p.iter] = s;
+        if (iter < p.max_iters) p.fe[(size_t)m * p.max_iters + iter] = s;
+        __threadfence();
+        last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
+        if (last) {
+            *p.done_ctr = 0u;
+            *p.iter_ctr = iter + 1;
+            __threadfence();
+        }
     }
 }
 

@@ -110,7 +110,9 @@ int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len);
 cudaError_t launch_fb(const FBArgs &a, cudaStream_t st);
 
 struct ElboArgs {
-    int M, T, n_tiles, S, iter, max_iters;
+    int M, T, n_tiles, S, max_iters;
+    int *iter_ctr;            // device sweep counter (row of fe to write; advanced by the kernel)
+    unsigned *done_ctr;       // device: blocks finished (last-block pattern)
     double c_prior_T;         // T * (lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma))
     const double *data_part;  // [M*T][n_tiles]
     const double *hdir;       // [M*T]
