@@ -25,7 +25,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
-#include "digamma_u_poly.cuh"
+#include "dirichlet_math.cuh"
 #include "nfhmm_internal.cuh"
 
 namespace nfk {
@@ -33,50 +33,6 @@ namespace nfk {
 namespace {
 
 constexpr int WPB = 8;   // frames (warps) per CTA
-
-// ln of a pair, both >= 1 (normal): exponent ln 2 + lg2(mantissa) ln 2 (SFU), assembled packed
-__device__ __forceinline__ uint64_t ln_sfu2(float x0, float x1) {
-    const uint32_t b0 = __float_as_uint(x0), b1 = __float_as_uint(x1);
-    float l0, l1;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0) : "f"(__uint_as_float((b0 & 0x007FFFFFu) | 0x3F800000u)));
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1) : "f"(__uint_as_float((b1 & 0x007FFFFFu) | 0x3F800000u)));
-    const uint64_t e = f2pack((float)((int)(b0 >> 23) - 127), (float)((int)(b1 >> 23) - 127));
-    return f2fma(e, f2c(0.693147180559945309f), f2mul(f2pack(l0, l1), f2c(0.693147180559945309f)));
-}
-__device__ __forceinline__ float rcp_sfu(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ float ex2_sfu(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-// Two elements at once (packed FFMA2 pipeline): alpha pair a -> psi, theta, and the running g~ sum
-//   u = 1/a, t = 2u - 1, r = u/2 + u^2 G(t), psi = ln a - r, theta = a e^{-psi_0} exp(-r),
-//   g~ = ln(a)/2 + ln(2 pi)/2 + 1/2 + u (H(t) - 1/2) + (u - u^2) G(t)
-__device__ __forceinline__ void elem_pair(float a0, float a1, uint64_t e0_2, bool want_h, uint64_t &psi2,
-                                          uint64_t &th2, uint64_t &g2t) {
-    const uint64_t a2 = f2pack(a0, a1);
-    const uint64_t u2 = f2pack(rcp_sfu(a0), rcp_sfu(a1));
-    const uint64_t lx2 = ln_sfu2(a0, a1);
-    const uint64_t t2 = f2fma(u2, f2c(2.f), f2c(-1.f));
-    const uint64_t G2 = dig_G2(t2);
-    const uint64_t uu2 = f2mul(u2, u2);
-    const uint64_t r2 = f2fma(uu2, G2, f2mul(u2, f2c(0.5f)));
-    psi2 = f2sub(lx2, r2);
-    float q0, q1;
-    f2unpack(f2mul(r2, f2c(-1.44269504088896341f)), q0, q1);
-    th2 = f2mul(f2mul(a2, e0_2), f2pack(ex2_sfu(q0), ex2_sfu(q1)));
-    if (want_h) {
-        const uint64_t H2 = lng_H2(t2);
-        const uint64_t g2 = f2fma(f2c(0.5f), lx2, f2c(1.41893853320467274f));
-        g2t = f2add(g2, f2fma(u2, f2sub(H2, f2c(0.5f)), f2mul(f2sub(u2, uu2), G2)));
-    } else {
-        g2t = 0ull;
-    }
-}
 
 __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -410,7 +366,142 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs 
     if (bad) atomicOr(p.flags, bad);
 }
 
+// ---------------------------------------------------------------------------------------------------
+// Fused path (the element work of (c)+(d) runs in the back-projection GEMM's epilogue, gemm_tc.cu):
+//   dv_kernel   (before the GEMM)  dvT[b][f] = gamma d_{s,t,n} + 1 for block b = s N + n,
+//               d = u .* b / sum_n (u .* b);
+//   eq8_kernel  (after the GEMM)   Eq. 8 block sums of psi (spsT, plus sps2T for the blocks whose K elements
+//               straddle two epilogue warps' 32-column chunks) -> centred emissions e and offsets eoff, and
+//               the frame's bound term H_t from the per-column-tile g~ partial sums hpartT.
+// The per-block arrays are block-major ([block][frame]): in the GEMM epilogue thread = frame row, so
+// a warp's reads of dvT and writes of spsT / hpartT are 128-byte coalesced rows.  Both kernels move them
+// through a [SN][33] shared tile, 32 frames per CTA.
+constexpr int FR = 32;   // frames per CTA of the fused-path kernels
+
+__global__ void __launch_bounds__(WPB * 32) dv_kernel(DirichletArgs p, float *dvT) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float *tl = reinterpret_cast<float *>(smem_raw);   // [SN][FR + 1]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int SN = p.S * p.N, f0 = blockIdx.x * FR;
+    unsigned bad = 0;
+    for (int fl = warp; fl < FR; fl += WPB) {
+        const int f = f0 + fl;
+        if (f >= p.frames) break;
+        const int m = f / p.T, t = f - m * p.T;
+        for (int s = 0; s < p.S; ++s) {
+            const size_t row = ((size_t)(m * p.S + s) * p.T + t) * p.N;
+            float q[4], qs = 0.f;   // N <= 128
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int n = lane + 32 * i;
+                q[i] = n < p.N ? p.u_fwd[row + n] * p.b_bwd[row + n] : 0.f;
+                qs += q[i];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) qs += __shfl_xor_sync(0xffffffffu, qs, o);
+            if (!(qs > 0.f) || !(qs < INFINITY)) bad |= FLAG_NONFINITE;
+            const float gq = p.gamma * __frcp_rn(qs);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int n = lane + 32 * i;
+                if (n < p.N) tl[(s * p.N + n) * (FR + 1) + fl] = fmaf(gq, q[i], 1.f);
+            }
+        }
+    }
+    __syncthreads();
+    if (f0 + lane < p.frames)
+        for (int b = warp; b < SN; b += WPB) dvT[(size_t)b * p.ldf + f0 + lane] = tl[b * (FR + 1) + lane];
+    if (bad) atomicOr(p.flags, bad);
+}
+
+__global__ void __launch_bounds__(WPB * 32) eq8_kernel(DirichletArgs p, const double *spsT, const double *sps2T,
+                                                       const double *hpartT, int n_tiles, int bn) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *tl = reinterpret_cast<double *>(smem_raw);   // [SN][FR + 1]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int SN = p.S * p.N, K = p.K, f0 = blockIdx.x * FR;
+    const bool fok = f0 + lane < p.frames;
+    for (int b = warp; b < SN; b += WPB) {
+        double v = 0.0;
+        if (fok) {
+            const size_t i = (size_t)b * p.ldf + f0 + lane;
+            v = spsT[i];
+            const int ls = (b * K) % bn;   // block start inside its column tile
+            if ((ls >> 5) != ((ls + K - 1) >> 5)) v += sps2T[i];
+        }
+        tl[b * (FR + 1) + lane] = v;
+    }
+    if (p.hdir && warp == 0 && fok) {
+        const int f = f0 + lane;
+        double h = 0.0;
+        for (int c = 0; c < n_tiles; ++c) h += hpartT[(size_t)c * p.ldf + f];
+        p.hdir[f] = h + p.fconst[4 * (size_t)f + 2];
+    }
+    __syncthreads();
+    unsigned bad = 0;
+    for (int fl = warp; fl < FR; fl += WPB) {
+        const int f = f0 + fl;
+        if (f >= p.frames) break;
+        const int m = f / p.T, t = f - m * p.T;
+        const double psi0 = p.fconst[4 * (size_t)f + 1];
+        for (int s = 0; s < p.S; ++s) {
+            double v[4];
+            float mxf = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int n = lane + 32 * i;
+                v[i] = n < p.N ? tl[(s * p.N + n) * (FR + 1) + fl] : 0.0;
+                if (n < p.N) mxf = fmaxf(mxf, (float)v[i]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+            const double mx = (double)mxf;
+            float *dst = p.ec + ((size_t)(m * p.S + s) * p.T + t) * p.N;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int n = lane + 32 * i;
+                if (n < p.N) dst[n] = ex2_sfu((float)((double)p.gamma * (v[i] - mx)) * 1.44269504088896341f);
+            }
+            if (lane == 0) {
+                const double off = (double)p.gamma * (mx - (double)K * psi0);
+                p.eoff[(size_t)(m * p.S + s) * p.T + t] = off;
+                if (!isfinite(off)) bad |= FLAG_NONFINITE;
+            }
+        }
+    }
+    if (bad) atomicOr(p.flags, bad);
+}
+
 }  // namespace
+
+size_t fused_tile_bytes(int SN, int elem) { return (size_t)SN * (FR + 1) * elem; }
+
+cudaError_t launch_dv(const DirichletArgs &a, float *dvT, cudaStream_t st) {
+    const size_t smem = fused_tile_bytes(a.S * a.N, 4);
+    if (a.N > 128 || smem > 200 * 1024) return cudaErrorInvalidValue;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && attr < smem) {
+        cudaError_t e = cudaFuncSetAttribute(dv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    dv_kernel<<<(a.frames + FR - 1) / FR, WPB * 32, smem, st>>>(a, dvT);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eq8(const DirichletArgs &a, const double *spsT, const double *sps2T, const double *hpartT,
+                       int n_tiles, int bn, cudaStream_t st) {
+    const size_t smem = fused_tile_bytes(a.S * a.N, 8);
+    if (a.N > 128 || smem > 200 * 1024) return cudaErrorInvalidValue;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && attr < smem) {
+        cudaError_t e = cudaFuncSetAttribute(eq8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    eq8_kernel<<<(a.frames + FR - 1) / FR, WPB * 32, smem, st>>>(a, spsT, sps2T, hpartT, n_tiles, bn);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
     const int SN = a.S * a.N;

@@ -41,6 +41,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include "dirichlet_math.cuh"
 #include "nfhmm_internal.cuh"
 
 namespace nfk {
@@ -68,7 +69,8 @@ constexpr int MAX_STAGES = 8;
 constexpr int A_PREFETCH = 16;             // stages ahead at which the producer pulls A tiles into L2
 constexpr int XCH_OFF = 1024;                                      // [3][128] FP64 row partials
 constexpr int EPI_OFF = 4096;                                      // epilogue tiles [12][4 KB]
-constexpr int RING_OFF = EPI_OFF + EPI_WARPS * EPI_TILE_BYTES;   // then the stage ring
+constexpr int RING_OFF = EPI_OFF + EPI_WARPS * EPI_TILE_BYTES;   // then the stage ring (DIRICHLET: the
+                                                                   // epilogue warps' dv tiles come first)
 constexpr int SMEM_MAX = 227 * 1024;
 
 // TMEM map (512 columns): accumulation slots at [0, BN) and [BN, 2 BN); A stages from a_col0(BN).
@@ -233,7 +235,7 @@ __device__ __forceinline__ void tmem_add16(uint32_t taddr, float (&acc)[32]) {
     for (int i = 0; i < 16; ++i) acc[i] += __uint_as_float(r[i]);
 }
 
-enum TcMode : int { TC_RATIO = 0, TC_STORE = 1, TC_SEPARATE = 2, TC_BACKPROJ = 3 };
+enum TcMode : int { TC_RATIO = 0, TC_STORE = 1, TC_SEPARATE = 2, TC_BACKPROJ = 3, TC_DIRICHLET = 4 };
 
 struct TcParams {
     int mode;
@@ -255,6 +257,12 @@ struct TcParams {
     float *out_src;
     int T, S, s;
     unsigned *flags;
+    // DIRICHLET (back-projection with the fused Eq. 6-8 element step): see launch_backproj_dirichlet_tc
+    int ring_off;           // byte offset of the stage ring
+    int K, Kt, SN, nbc, ldf;
+    const double *fconst;
+    double *spsT, *sps2T, *hpartT;
+    float *alpha_out;
     int dbg;                // performance experiments only (NFHMM_TC_DEBUG): 1 no A loads, 2 no MMAs, 4 no epilogue
                             // I/O, 8 no A TMEM stores, 32 no B loads, 64 no drains, 128 no converter work
 };
@@ -267,15 +275,17 @@ struct Smem {
 // 16-byte chunk c of row r in a TMA tile with 64-B rows, 64-byte swizzle (bits [4,5] ^= bits [7,8])
 __device__ __forceinline__ uint32_t swz64(int r, int c) { return (uint32_t)r * 64u + (uint32_t)((c ^ (r >> 1)) & 3) * 16u; }
 
+template <bool FUSED>   // FUSED: the DIRICHLET epilogue only (a separate instantiation keeps registers down)
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmIn,
-                   const __grid_constant__ CUtensorMap tmOut, TcParams p) {
+                   const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmDv,
+                   TcParams p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const int BN = p.bn;
     const uint32_t b_bytes = (uint32_t)BN * TC_KB * 4;     // one of hi / lo
     const uint32_t stage_bytes = (uint32_t)stage_bytes_of(BN);
-    unsigned char *ring = smem_raw + RING_OFF;
+    unsigned char *ring = smem_raw + p.ring_off;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mtiles = (p.M + TC_BM - 1) / TC_BM;
@@ -309,6 +319,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmIn) : "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmOut) : "memory");
         }
+        if (p.mode == TC_DIRICHLET) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmDv) : "memory");
     }
     tc_fence_before();
     __syncthreads();
@@ -467,16 +478,106 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             return b;
         };
         // lane 0: fetch chunk j's operand sub-tiles into the warp's buffer (after earlier stores read it)
+        constexpr bool fused = FUSED;
+        float *dvbuf = reinterpret_cast<float *>(smem_raw + RING_OFF + (size_t)ew * p.nbc * 128);   // [nbc][32]
         auto fetch = [&](int j, int n0, int r0) {
             const uint32_t b = chunk_bytes(j);
             if (!b) return;
             bulk_wait_read_all();
-            mbar_arrive_expect_tx(&S.ebar[ew], b);
+            mbar_arrive_expect_tx(&S.ebar[ew], b + (fused ? (uint32_t)p.nbc * 128u : 0u));
+            if (fused) tma_load_2d(dvbuf, &tmDv, r0, (n0 + 32 * (cg + EPI_PER_Q * j)) / p.K, &S.ebar[ew]);
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
                 const int c0 = 32 * (cg + EPI_PER_Q * j) + 16 * hh;
                 if (c0 + 16 <= BN) tma_load_2d(etile + hh * EPI_SUB_BYTES, &tmIn, n0 + c0, r0, &S.ebar[ew]);
             }
+        };
+        // DIRICHLET epilogue of one 32-column chunk (Eqs. 6-8 per element, dirichlet.cu for the
+        // arithmetic): alpha = theta .* C + dv(block), then psi, the new theta (in place of the operand
+        // tile, leaving by the TMA store) and g~.  The columns are K-element blocks (BN % K == 0, K <= 32);
+        // the chunk's block ends are a warp-uniform bit mask, so the per-element bookkeeping is
+        // branch-free: a block's psi sum is stored to spsT when its last element passes (to sps2T if the
+        // block started in the previous chunk, which another warp owns), and a block still open at the
+        // chunk's end is stored to spsT as its first part.
+        auto fused_chunk = [&](int j, int n0, int r0, int row, bool row_ok, float e0f, float(&a32)[32],
+                               uint64_t &hg2) {
+            const int c0 = 32 * (cg + EPI_PER_Q * j), gc = n0 + c0, K = p.K;
+            const int bq = gc / K, off = gc - bq * K, lim = p.Kt - gc;
+            uint32_t endm = 0;   // bit i: column gc + i closes a block
+            for (int i = K - 1 - off; i < 32; i += K) endm |= 1u << i;
+            const uint32_t realm = lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (1u << lim) - 1u);
+            const bool rok = row_ok;
+            const int nb_last = p.SN - 1 - bq;   // relative index of the last real block
+            double *const dst0 = off ? p.sps2T : p.spsT;   // the chunk's first block
+            double *const dstn = p.spsT;
+            const size_t ldf = (size_t)p.ldf;
+            const uint64_t e0_2 = f2c(e0f);
+            const bool want_h = p.hpartT != nullptr, want_a = p.alpha_out != nullptr && row_ok;
+            int rel = 0;
+            double sp = 0.0;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                if (c0 + 16 * hh + 16 > BN) continue;
+                unsigned char *tb = etile + hh * EPI_SUB_BYTES;
+#pragma unroll
+                for (int i4 = 0; i4 < 4; ++i4) {
+                    float4 *px = reinterpret_cast<float4 *>(tb + swz64(lane, i4));
+                    const float4 x = *px;
+                    const float xv[4] = {x.x, x.y, x.z, x.w};
+                    float y[4], av[4];
+#pragma unroll
+                    for (int e = 0; e < 4; e += 2) {
+                        const int cc = 16 * hh + 4 * i4 + e;   // column inside the chunk
+                        const int end0 = (endm >> cc) & 1, end1 = (endm >> (cc + 1)) & 1;
+                        const int relB = rel + end0;
+                        const float dvA = dvbuf[rel * 32 + lane];
+                        const float dvB = dvbuf[min(relB, p.nbc - 1) * 32 + lane];
+                        const float a0 = __fadd_rn(__fmul_rn(xv[e], a32[cc]), dvA);
+                        const float a1 = __fadd_rn(__fmul_rn(xv[e + 1], a32[cc + 1]), dvB);
+                        uint64_t ps2, th2, g2;
+                        elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                        float p0, p1, t0, t1, g0, g1;
+                        f2unpack(ps2, p0, p1);
+                        f2unpack(th2, t0, t1);
+                        f2unpack(g2, g0, g1);
+                        const bool re0 = (realm >> cc) & 1, re1 = (realm >> (cc + 1)) & 1;
+                        y[e] = re0 ? t0 : xv[e];   // padding columns (>= Kt) keep their operand
+                        y[e + 1] = re1 ? t1 : xv[e + 1];
+                        hg2 = f2add(hg2, f2pack(re0 ? g0 : 0.f, re1 ? g1 : 0.f));
+                        sp += (double)p0;
+                        if (end0 && rok && rel <= nb_last) (rel == 0 ? dst0 : dstn)[(size_t)(bq + rel) * ldf + row] = sp;
+                        sp = end0 ? 0.0 : sp;
+                        sp += (double)p1;
+                        if (end1 && rok && relB <= nb_last)
+                            (relB == 0 ? dst0 : dstn)[(size_t)(bq + relB) * ldf + row] = sp;
+                        sp = end1 ? 0.0 : sp;
+                        rel = relB + end1;
+                        av[e] = a0;
+                        av[e + 1] = a1;
+                    }
+                    *px = make_float4(y[0], y[1], y[2], y[3]);
+                    if (want_a) {   // last sweep of a call: alpha for posteriors / separation
+                        const int col = gc + 16 * hh + 4 * i4;
+                        float *dst = p.alpha_out + (size_t)row * p.ldc + col;
+                        if (col + 4 <= p.Kt) {
+                            *reinterpret_cast<float4 *>(dst) = make_float4(av[0], av[1], av[2], av[3]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (col + e < p.Kt) dst[e] = av[e];
+                        }
+                    }
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmOut, gc + 16 * hh, r0, tb);
+                    bulk_commit();
+                }
+            }
+            // a block still open at the chunk's end continues in the next chunk: this is its first part
+            const int w = c0 + 32 <= BN ? 32 : 16;
+            if (!((endm >> (w - 1)) & 1) && rok && rel <= nb_last) (rel == 0 ? dst0 : dstn)[(size_t)(bq + rel) * ldf + row] = sp;
         };
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
             const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
@@ -485,6 +586,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // chunk 0's operand lands while the tile accumulates; chunk 1's is fetched after chunk 0 left
             if (tma_epi && lane == 0) fetch(0, n0, r0);
             __syncwarp();
+            float e0f = 1.f;   // DIRICHLET: e^{-psi(alpha_0)} of this thread's frame
+            if (fused && r0 + lane < p.M) e0f = (float)p.fconst[4 * (size_t)(r0 + lane) + 3];
             float acc[EPI_CH][32];
 #pragma unroll
             for (int j = 0; j < EPI_CH; ++j)
@@ -509,6 +612,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int row = r0 + lane;
             const bool row_ok = row < p.M;
             double part = 0.0;
+            uint64_t hg2 = 0ull;   // DIRICHLET: packed running sum of g~ over this thread's columns
             if (tma_epi) {
 #pragma unroll
                 for (int j = 0; j < EPI_CH; ++j) {
@@ -519,6 +623,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                     mbar_wait_sleep(&S.ebar[ew], e_ph);
                     e_ph ^= 1;
+                    if constexpr (FUSED) {
+                        fused_chunk(j, n0, r0, row, row_ok, e0f, acc[j], hg2);
+                    } else {
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         const int c0 = 32 * (cg + EPI_PER_Q * j) + 16 * hh;
@@ -561,9 +668,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             bulk_commit();
                         }
                     }
+                    }
                 }
                 if (!row_ok) part = 0.0;
-            } else {
+            } else if (!FUSED) {
 #pragma unroll
                 for (int j = 0; j < EPI_CH; ++j) {
                     const int c0 = 32 * (cg + EPI_PER_Q * j);
@@ -586,13 +694,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                 }
             }
-            if (p.mode == TC_RATIO && p.data_part) {
+            if (fused && p.hpartT) {
+                float h0, h1;
+                f2unpack(hg2, h0, h1);
+                part = row_ok ? (double)h0 + (double)h1 : 0.0;
+            }
+            if ((p.mode == TC_RATIO && p.data_part) || (fused && p.hpartT)) {
                 // three warps share each row: combine their partials in a fixed order
                 const int rl = 32 * q + lane;
                 xch[cg * 128 + rl] = part;
                 asm volatile("bar.sync 1, %0;\n" ::"r"(EPI_WARPS * 32) : "memory");
-                if (cg == 0 && row_ok)
-                    p.data_part[(size_t)row * p.n_tiles + nt] = (xch[rl] + xch[128 + rl]) + xch[256 + rl];
+                if (cg == 0 && row_ok) {
+                    const double v = (xch[rl] + xch[128 + rl]) + xch[256 + rl];
+                    if (fused) p.hpartT[(size_t)nt * p.ldf + row] = v;
+                    else p.data_part[(size_t)row * p.n_tiles + nt] = v;
+                }
                 asm volatile("bar.sync 1, %0;\n" ::"r"(EPI_WARPS * 32) : "memory");
             }
         }
@@ -611,8 +727,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 int g_num_sms = 0;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-int stages_for(int bn) {
-    int s = (SMEM_MAX - RING_OFF) / stage_bytes_of(bn);
+int stages_for(int bn, int ring_off = RING_OFF) {
+    int s = (SMEM_MAX - ring_off) / stage_bytes_of(bn);
     if (s > tmem_a_stages(bn)) s = tmem_a_stages(bn);
     return s > MAX_STAGES ? MAX_STAGES : s;
 }
@@ -638,25 +754,35 @@ cudaError_t make_map(CUtensorMap *m, const float *base, int64_t cols, int64_t ro
 }
 
 // A [M][lda] (cols = lda); epilogue in / out [M][ldc]
-cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, float *eout, cudaStream_t st) {
+cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, float *eout, cudaStream_t st,
+                      const float *dvT = nullptr) {
     if (g_num_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     if (p.bn < 16 || p.bn > TC_MAX_BN || p.bn % 16 || p.stages < 2) return cudaErrorInvalidValue;
-    const size_t smem = RING_OFF + (size_t)p.stages * stage_bytes_of(p.bn);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    if (p.ring_off == 0) p.ring_off = RING_OFF;
+    const size_t smem = (size_t)p.ring_off + (size_t)p.stages * stage_bytes_of(p.bn);
+    if (smem > SMEM_MAX) return cudaErrorInvalidValue;
+    const bool fused = p.mode == TC_DIRICHLET;
+    auto kern = fused ? tc_gemm_kernel<true> : tc_gemm_kernel<false>;
+    static bool attr[2] = {false, false};
+    if (!attr[fused]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr[fused] = true;
     }
-    CUtensorMap mA, mIn, mOut;
+    CUtensorMap mA, mIn, mOut, mDv;
     cudaError_t e = make_map(&mA, A, lda, p.M, lda, TC_KB, TC_BM, CU_TENSOR_MAP_SWIZZLE_64B);
     if (e != cudaSuccess) return e;
     mIn = mA;
     mOut = mA;
+    mDv = mA;
+    if (p.mode == TC_DIRICHLET) {   // dvT [SN][ldf]: box = 32 frames x nbc blocks, no swizzle
+        e = make_map(&mDv, dvT, p.ldf, p.SN, p.ldf, 32, p.nbc, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (e != cudaSuccess) return e;
+    }
     if (p.tma_epi) {
         e = make_map(&mIn, ein, p.ldc, p.M, p.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (e == cudaSuccess) e = make_map(&mOut, eout, p.ldc, p.M, p.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -673,17 +799,17 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
     }
     p.dbg = dbg;
     p.chunk_kb = chunk;
-    tc_gemm_kernel<<<grid, TC_THREADS, smem, st>>>(mA, mIn, mOut, p);
+    kern<<<grid, TC_THREADS, smem, st>>>(mA, mIn, mOut, mDv, p);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-int tc_pick_bn(int64_t n) {
-    int best = 16;
+int tc_pick_bn(int64_t n, int mult) {
+    int best = 0;
     int64_t best_pad = INT64_MAX;
     // padded width plus a per-tile cost (each extra column tile re-reads the A rows from L2)
-    for (int bn = 16; bn <= TC_MAX_BN; bn += 16) {
+    for (int bn = mult; bn <= TC_MAX_BN; bn += mult) {
         const int64_t pad = (n + bn - 1) / bn * bn + 24 * ((n + bn - 1) / bn);
         if (pad < best_pad || (pad == best_pad && bn > best)) {
             best_pad = pad;
@@ -760,6 +886,37 @@ cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaS
     p.nkb_total = a.nkb_total;
     p.ldc = a.ldb;
     return launch_tc(p, a.A, a.lda, a.theta, a.n_out, st);
+}
+
+int tc_fused_blocks_per_chunk(int K) { return (2 * K - 2 + 32) / K; }
+
+cudaError_t launch_backproj_dirichlet_tc(int bn, int n_valid, const BackprojArgs &a, const FusedDirichletArgs &d,
+                                         cudaStream_t st) {
+    if (bn % d.K || d.K > 32 || d.ldf % 4 || a.ldb % 4) return cudaErrorInvalidValue;
+    TcParams p{};
+    p.mode = TC_DIRICHLET;
+    p.M = a.M;
+    p.bn = bn;
+    p.n_tiles = (n_valid + bn - 1) / bn;
+    p.k_begin = 0;
+    p.k_end = a.Kpad;
+    p.nbc = tc_fused_blocks_per_chunk(d.K);
+    p.ring_off = (RING_OFF + EPI_WARPS * p.nbc * 128 + 1023) & ~1023;
+    p.stages = stages_for(bn, p.ring_off);
+    p.tma_epi = 1;
+    p.Bsplit = a.Bsplit;
+    p.nkb_total = a.nkb_total;
+    p.ldc = a.ldb;
+    p.K = d.K;
+    p.Kt = d.Kt;
+    p.SN = d.SN;
+    p.ldf = d.ldf;
+    p.fconst = d.fconst;
+    p.spsT = d.spsT;
+    p.sps2T = d.sps2T;
+    p.hpartT = d.hpartT;
+    p.alpha_out = d.alpha_out;
+    return launch_tc(p, a.A, a.lda, a.theta, const_cast<float *>(a.theta), st, d.dvT);
 }
 
 }  // namespace nfk

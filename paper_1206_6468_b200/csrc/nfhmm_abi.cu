@@ -34,6 +34,12 @@ struct nfhmm {
     float *bs_a = nullptr, *bs_b = nullptr;   // tensor-core path: pre-split beta for (a) and betaT for (b)
     double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
     double *fconst = nullptr;   // per-frame alpha_0, psi(alpha_0), bound constant (set_observations)
+    // Dirichlet step fused into the back-projection epilogue (tensor-core engine, K <= 32): block-major
+    // pseudo-counts, Eq. 8 block sums and g~ partials, frame pitch ldf
+    bool fused = false;
+    int ldf = 0, nt_tc_b = 0;
+    float *dvT = nullptr;
+    double *spsT = nullptr, *sps2T = nullptr, *hpartT = nullptr;
     // parallel-in-time forward-backward (few chains): chunks, their transfer matrices and start messages
     int fb_nchunk = 0, fb_len = 0;
     float *fbP = nullptr, *fbPT = nullptr, *fbF = nullptr, *fbB = nullptr;
@@ -174,6 +180,13 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take((size_t)h->M * h->S * h->T * h->F * 4); h->vsrc = (float *)p;
     p = take(tc_presplit_floats(h->F, h->Kt, h->bn_tc_a) * 4); h->bs_a = (float *)p;
     p = take(tc_presplit_floats(h->Kt, h->Fa, h->bn_tc_b) * 4); h->bs_b = (float *)p;
+    if (h->fused) {
+        const size_t sn = (size_t)h->S * h->N, ldf = (size_t)h->ldf;
+        p = take(sn * ldf * 4);                  h->dvT = (float *)p;
+        p = take(sn * ldf * 8);                  h->spsT = (double *)p;
+        p = take(sn * ldf * 8);                  h->sps2T = (double *)p;
+        p = take((size_t)h->nt_tc_b * ldf * 8);  h->hpartT = (double *)p;
+    }
     p = take(256);                               h->flags = (unsigned *)p;
     return o;
 }
@@ -232,8 +245,11 @@ int recon_ratio(nfhmm_t *h) {
     return run_recon(h, NFHMM_K_RECON, a);
 }
 
-// (b) n = theta .* (R beta): the Eq. 6 data term  sum_l V_lt z_{t,l,k}
-int step_backproj(nfhmm_t *h) {
+DirichletArgs dirichlet_args(nfhmm_t *h, bool write_alpha);
+
+// (b) n = theta .* (R beta): the Eq. 6 data term  sum_l V_lt z_{t,l,k}; fused engine: (b) with the
+// element step of (c)+(d) in its epilogue (theta updated in place, alpha stored on the last sweep)
+int step_backproj(nfhmm_t *h, bool last = true) {
     BackprojArgs b{};
     b.M = (int)h->frames;
     b.Kpad = h->Fa;
@@ -247,6 +263,21 @@ int step_backproj(nfhmm_t *h) {
         b.B = h->betaT;     // [Kt_pad][F_pad], K-major rows
         b.Bsplit = h->bs_b;
         b.nkb_total = (h->Fa + 15) / 16;
+        if (h->fused) {
+            FusedDirichletArgs d{};
+            d.K = h->K;
+            d.Kt = h->Kt;
+            d.SN = h->S * h->N;
+            d.ldf = h->ldf;
+            d.dvT = h->dvT;
+            d.fconst = h->fconst;
+            d.spsT = h->spsT;
+            d.sps2T = h->sps2T;
+            d.hpartT = h->free_energy ? h->hpartT : nullptr;
+            d.alpha_out = last ? h->alpha : nullptr;
+            LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj_dirichlet_tc(h->bn_tc_b, h->Kt, b, d, h->st));
+            return NFHMM_OK;
+        }
         LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj_tc(h->bn_tc_b, h->Kt, b, h->st));
     } else {
         LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj(h->bn_b, b, h->st));
@@ -255,7 +286,7 @@ int step_backproj(nfhmm_t *h) {
 }
 
 // (c)+(d) Eq. 6, digamma/exp, Eq. 8
-int step_dirichlet(nfhmm_t *h, bool write_alpha) {
+DirichletArgs dirichlet_args(nfhmm_t *h, bool write_alpha) {
     DirichletArgs d{};
     d.frames = (int)h->frames;
     d.T = (int)h->T;
@@ -276,7 +307,25 @@ int step_dirichlet(nfhmm_t *h, bool write_alpha) {
     d.write_alpha = write_alpha ? 1 : 0;
     d.hdir = h->free_energy ? h->hdir : nullptr;
     d.flags = h->flags;
+    d.ldf = h->ldf;
+    return d;
+}
+
+int step_dirichlet(nfhmm_t *h, bool write_alpha) {
+    const DirichletArgs d = dirichlet_args(h, write_alpha);
     LAUNCH(h, NFHMM_K_DIRICHLET, launch_dirichlet(d, h->st));
+    return NFHMM_OK;
+}
+
+// fused engine: pseudo-counts gamma d + 1 before (b), Eq. 8 emissions and H_t after it
+int step_dv(nfhmm_t *h) {
+    const DirichletArgs d = dirichlet_args(h, false);
+    LAUNCH(h, NFHMM_K_DIRICHLET, launch_dv(d, h->dvT, h->st));
+    return NFHMM_OK;
+}
+int step_eq8(nfhmm_t *h) {
+    const DirichletArgs d = dirichlet_args(h, false);
+    LAUNCH(h, NFHMM_K_DIRICHLET, launch_eq8(d, h->spsT, h->sps2T, h->hpartT, h->nt_tc_b, h->bn_tc_b, h->st));
     return NFHMM_OK;
 }
 
@@ -313,8 +362,15 @@ int sweep(nfhmm_t *h, bool last) {
         if (r) return r;
         h->R_valid = true;
     }
-    int r = step_backproj(h);
-    if (!r) r = step_dirichlet(h, last);
+    int r;
+    if (h->fused) {
+        r = step_dv(h);
+        if (!r) r = step_backproj(h, last);
+        if (!r) r = step_eq8(h);
+    } else {
+        r = step_backproj(h);
+        if (!r) r = step_dirichlet(h, last);
+    }
     if (!r) r = step_fb(h);
     if (r) return r;
     // (a) z-step of the new alpha: R for the next sweep and the data term of L_i
@@ -451,7 +507,19 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         h->fb_len = nc > 1 ? L : 0;
     }
     h->bn_tc_a = tc_pick_bn(F);
-    h->bn_tc_b = tc_pick_bn(Kt);
+    {   // Dirichlet element step fused into the back-projection epilogue (opt-in, NFHMM_FUSED=1): correct
+        // but measured slower (DESIGN "Fused Dirichlet epilogue"): the element work competes with the
+        // GEMM's own epilogue / converter issue slots and stalls the MMAs.  Column tiles of whole K-blocks.
+        const char *e = getenv("NFHMM_FUSED");
+        int l = 16;
+        while (l % K) l += 16;   // lcm(16, K)
+        const int64_t SN = (int64_t)S * N;
+        h->fused = h->math == NFHMM_MATH_TC && K <= 32 && l <= 192 && SN * 33 * 8 <= 200 * 1024 &&
+                   e && atoi(e) != 0;
+        h->bn_tc_b = h->fused ? tc_pick_bn(Kt, l) : tc_pick_bn(Kt);
+        h->nt_tc_b = (int)((Kt + h->bn_tc_b - 1) / h->bn_tc_b);
+        h->ldf = (int)((frames + 31) / 32 * 32);
+    }
     h->nt_tc_a = (int)((F + h->bn_tc_a - 1) / h->bn_tc_a);
     // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)
     h->c_prior_T = (double)T * (lgamma((double)Kt + o.gamma * S * K) - (double)S * K * lgamma(1.0 + o.gamma));
@@ -756,7 +824,14 @@ int nfhmm_bench_kernel(nfhmm_t *h, int cls, int32_t reps, double *ms_per_launch)
         switch (cls) {
             case NFHMM_K_RECON: r = recon_ratio(h); break;
             case NFHMM_K_BACKPROJ: r = step_backproj(h); break;
-            case NFHMM_K_DIRICHLET: r = step_dirichlet(h, true); break;
+            case NFHMM_K_DIRICHLET:
+                if (h->fused) {
+                    r = step_dv(h);
+                    if (!r) r = step_eq8(h);
+                } else {
+                    r = step_dirichlet(h, true);
+                }
+                break;
             default: r = step_fb(h); break;
         }
     }

@@ -60,7 +60,7 @@ cudaError_t launch_backproj(int bn, const BackprojArgs &a, cudaStream_t st);
 
 // tcgen05 3xTF32 variants (gemm_tc.cu).  recon: a.B = beta [F_pad][Kt_pad] K-major (ldb = Kt_pad);
 // backproj: a.B = betaT [Kt_pad][F_pad] K-major, a.Kpad = F_pad, a.ldb = row length of theta / n.
-int tc_pick_bn(int64_t n);
+int tc_pick_bn(int64_t n, int mult = 16);   // tile width: a multiple of mult (itself a multiple of 16)
 // The static operand B[n][k] (n < n_rows, k < k_len; src[n*ld + k], or src[k*ld + n] if transposed) split
 // into tf32 hi/lo and re-tiled into the shared-memory image of each pipeline stage (host side, once).
 size_t tc_presplit_floats(int64_t n_rows, int64_t k_len, int bn);
@@ -68,6 +68,19 @@ void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t
                       float *dst);
 cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st);
 cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st);
+
+// Back-projection with the Dirichlet element step fused into its epilogue (bn % K == 0, K <= 32):
+// theta is updated in place; Eq. 8 block sums and g~ partials leave block-major ([block][ldf]).
+struct FusedDirichletArgs {
+    int K, Kt, SN, ldf;       // ldf: frame pitch of the block-major arrays (a multiple of 4)
+    const float *dvT;         // [SN][ldf]   gamma d + 1 (dv_kernel)
+    const double *fconst;     // [frames][4] (DirichletArgs)
+    double *spsT, *sps2T;     // [SN][ldf]   psi block sums (first / second parts)
+    double *hpartT;           // [n_tiles][ldf] g~ partial sums per column tile (NULL: no bound)
+    float *alpha_out;         // [frames][ldb] alpha, or NULL (not the last sweep)
+};
+cudaError_t launch_backproj_dirichlet_tc(int bn, int n_valid, const BackprojArgs &a, const FusedDirichletArgs &d,
+                                         cudaStream_t st);
 
 struct DirichletArgs {
     int frames, T, S, N, K, Kt, ld;   // ld = padded row length of n/alpha/theta
@@ -83,9 +96,14 @@ struct DirichletArgs {
     float *ec;                // [M][S][T][N]  out: emission exp(gamma*(phi - max_n phi)) in (0, 1]
     double *eoff;             // [M][S][T]     out: gamma * max_n phi (FP64)
     double *hdir;             // [frames]      out: Dirichlet entropy terms of the bound (or NULL)
+    int ldf;                  // fused path: frame pitch of the block-major arrays
     unsigned *flags;
 };
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st);
+// Fused path: pseudo-counts before the back-projection GEMM, Eq. 8 / bound terms after it (dirichlet.cu)
+cudaError_t launch_dv(const DirichletArgs &a, float *dvT, cudaStream_t st);
+cudaError_t launch_eq8(const DirichletArgs &a, const double *spsT, const double *sps2T, const double *hpartT,
+                       int n_tiles, int bn, cudaStream_t st);
 
 struct FBArgs {
     int M, S, T, N;

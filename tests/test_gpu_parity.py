@@ -197,3 +197,20 @@ def test_parallel_in_time_fb_matches_sequential(c, over, monkeypatch):
     o = run_oracle(cfg, model, V[0], 6)
     assert rel_l2(par["V_star"][0], o["V_star"]) <= TOL_VSTAR
     assert np.all(np.abs(par["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
+
+
+@pytest.mark.parametrize("c,over", [(0, {}), (1, dict(T=300)), (3, dict(T=200, M=3))])
+def test_fused_dirichlet_epilogue_matches_separate_kernel(c, over, monkeypatch):
+    """Opt-in engine (NFHMM_FUSED=1): the Dirichlet element step in the back-projection GEMM's epilogue
+    gives the separate kernel's results (same per-element arithmetic, other summation order of the Eq. 8
+    block sums and of the bound terms) and the oracle's."""
+    cfg, model, V = make_inputs(c, **over)
+    sep = run_gpu(cfg, model, V, 5)
+    monkeypatch.setenv("NFHMM_FUSED", "1")
+    fus = run_gpu(cfg, model, V, 5)
+    for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
+        assert rel_l2(fus[key], sep[key]) <= 2e-6, key
+    assert np.all(np.abs(fus["free_energy"] - sep["free_energy"]) <= 1e-7 * np.abs(sep["free_energy"]))
+    o = run_oracle(cfg, model, V[0], 5)
+    assert rel_l2(fus["V_star"][0], o["V_star"]) <= TOL_VSTAR
+    assert np.all(np.abs(fus["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
