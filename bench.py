@@ -277,32 +277,55 @@ def run_ours(args):
     value = frame_iters / (ms_per_step / 1000.0)
 
     # ---- e2e: public API with host buffers, copies inside the timed region -------------------
+    # Every step copies its V from pinned host memory, runs the sweeps and the separation, and reads
+    # the separated spectrograms back into pinned host memory.  Steps alternate between two handles on
+    # two streams (the public API's batch pipeline: nfhmm_separate_async + nfhmm_sync), so one step's
+    # host<->device copies run while the other step computes; the timed region spans all steps' copies.
     e2e = None
     if not args.no_e2e:
         Vh = torch.from_numpy(V).pin_memory()
-        out_h = torch.empty((M, cfg.S, cfg.T, cfg.F), dtype=torch.float32).pin_memory()
+        out_h = [torch.empty((M, cfg.S, cfg.T, cfg.F), dtype=torch.float32).pin_memory() for _ in range(2)]
+        streams = [torch.cuda.Stream(dev) for _ in range(2)]
+        hs = [NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, device=dev, max_iters=max(iters, 1), stream=st,
+                    math=args.math) for st in streams]
+        for hh in hs:
+            hh.set_model(model.beta, model.trans, model.prior)
 
-        def e2e_step():
-            h.set_observations(Vh)
-            h.vb_iterate_async(iters)
-            h.separate_into(out_h)
+        def e2e_step(i):
+            hh = hs[i % 2]
+            hh.set_observations(Vh)
+            hh.vb_iterate_async(iters)
+            hh.separate_into(out_h[i % 2], sync=False)
 
-        e2e_step()
+        for i in range(2):   # warm both handles (graph capture, first-touch)
+            e2e_step(i)
+        for hh in hs:
+            hh.sync()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        j0 = torch.cuda.Event()
         e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        j0.record(stream)
+        for st in streams:
+            st.wait_event(j0)
+        for i in range(args.steps):
+            e2e_step(i)
+        for st in streams:
+            stream.wait_stream(st)
         e1.record(stream)
         torch.cuda.synchronize()
+        for hh in hs:
+            hh.sync()   # sticky device flags of every step
         el = e0.elapsed_time(e1)
         if world > 1:
             el = pdist.max_over_ranks(el, device=f"cuda:{dev}")
         e2e = {"value": frame_iters / (el / args.steps / 1000.0), "unit": UNIT,
-               "h2d_bytes_per_step": int(Vh.numel() * 4) * world, "d2h_bytes_per_step": int(out_h.numel() * 4) * world,
-               "ms_per_step": el / args.steps}
+               "h2d_bytes_per_step": int(Vh.numel() * 4) * world, "d2h_bytes_per_step": int(out_h[0].numel() * 4) * world,
+               "ms_per_step": el / args.steps, "pipeline": "2 handles on 2 streams: copies of one step overlap the other's compute"}
+        for hh in hs:
+            hh.close()
 
     # ---- roofline of the dominant kernel ------------------------------------------------------
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}

@@ -127,6 +127,12 @@ int nfhmm_posteriors(nfhmm_t *h, float *d_hat, float *alpha_hat, float *V_hat, d
  * V_src [n_mix][S][T][F] (nullable, the unmasked V_hat^(s)).  Synchronises. */
 int nfhmm_separate(nfhmm_t *h, float *V_star, float *V_src);
 
+/* Same, enqueue only (no synchronisation, no flag check; follow with nfhmm_sync).  Host outputs must
+ * be pinned for the copies to stay asynchronous, and must not be read before nfhmm_sync returns.
+ * With two handles on two streams a caller pipelines batches: one handle's host<->device copies run
+ * while the other computes. */
+int nfhmm_separate_async(nfhmm_t *h, float *V_star, float *V_src);
+
 /* Free the handle (and the workspace if the library allocated it). NULL is a no-op. */
 int nfhmm_destroy(nfhmm_t *h);
 

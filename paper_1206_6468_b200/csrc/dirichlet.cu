@@ -24,6 +24,9 @@
 // last sweep of a call: alpha is not read inside the sweep loop).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "dirichlet_math.cuh"
 #include "nfhmm_internal.cuh"
@@ -366,6 +369,259 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_pipe_kernel(DirichletArgs 
     if (bad) atomicOr(p.flags, bad);
 }
 
+// Frame-tile variant (N, Kt multiples of 4; configs 0-3): a CTA owns a tile of FT consecutive frames.
+// The tile's n rows, FB message rows (consecutive t of one mixture are contiguous) and constants arrive
+// by a few cp.async.bulk copies issued by one thread and tracked by one mbarrier; per-frame small-vector
+// work is vectorised across the CTA instead of being repeated per warp: the Eq. 6 per-source sums and
+// the Eq. 8 per-source maxima run one thread per (frame, source), the emissions one thread per (frame,
+// block); the element pass runs one lane per (frame, block) over a warp's frames, so its lanes stay
+// busy when S N is not a multiple of 32.  Same element arithmetic as the kernels above; the FP32 sums
+// of u .* b over n are associated sequentially.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(b))
+                 : "memory");
+}
+
+__device__ __forceinline__ int div_small(int x, int d, float inv) {   // x / d for 0 <= x < 2^24
+    int q = __float2int_rz(__int2float_rn(x) * inv);
+    const int r = x - q * d;
+    if (r < 0) --q;
+    else if (r >= d) ++q;
+    return q;
+}
+
+constexpr int TILE_MAXFW = 4;   // frames per warp (FT <= 4 * warps)
+
+struct TileLayout {   // bytes from the start of dynamic shared memory
+    size_t bar, nb, ub, bb, fc, sps, gq, ecb, total;
+    __host__ __device__ TileLayout(int S, int N, int Kt, int FT) {
+        const size_t SN = (size_t)S * N;
+        bar = 0;
+        nb = 16;
+        ub = nb + (size_t)FT * Kt * 4;
+        bb = ub + SN * FT * 4;
+        fc = bb + SN * FT * 4;
+        sps = fc + (size_t)FT * 32;
+        gq = sps + SN * FT * 8;
+        ecb = gq + (size_t)FT * S * 4;
+        ecb = (ecb + 7) & ~size_t(7);
+        total = ecb + (size_t)FT * 8;
+    }
+    __host__ __device__ static size_t per_frame(int S, int N, int Kt) {
+        return (size_t)Kt * 4 + (size_t)S * N * 16 + 32 + (size_t)S * 4 + 8;
+    }
+};
+
+template <bool EVEN, int NW>   // NW warps per CTA
+__global__ void __launch_bounds__(NW * 32) dirichlet_tile_kernel(DirichletArgs p, int FT) {
+    constexpr int TILE_THREADS = NW * 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int S = p.S, N = p.N, SN = S * N, K = p.K, Kt = p.Kt, T = p.T;
+    const TileLayout L(S, N, Kt, FT);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw + L.bar);
+    float *nb = reinterpret_cast<float *>(smem_raw + L.nb);       // [FT][Kt]   n, then theta in place
+    float *ub = reinterpret_cast<float *>(smem_raw + L.ub);       // [S][FT][N] u
+    float *bb = reinterpret_cast<float *>(smem_raw + L.bb);       // [S][FT][N] b
+    double *fc = reinterpret_cast<double *>(smem_raw + L.fc);     // [FT][4]    frame constants
+    double *sps = reinterpret_cast<double *>(smem_raw + L.sps);   // [FT][SN]   Eq. 8 block sums
+    float *gq = reinterpret_cast<float *>(smem_raw + L.gq);       // [FT][S]    gamma / sum_n u b
+    long long *ecb = reinterpret_cast<long long *>(smem_raw + L.ecb);   // [FT] m S T + t: (m, s=0, t) row
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float gamma = p.gamma;
+    const bool want_h = p.hdir != nullptr, want_a = p.write_alpha != 0;
+    const float invN = 1.f / (float)N, invSN = 1.f / (float)SN, invS = 1.f / (float)S;
+    const int ntiles = (p.frames + FT - 1) / FT;
+    unsigned bad = 0;
+    if (tid == 0) {
+        bar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, phase ^= 1) {
+        const int f0 = tile * FT, nf = min(FT, p.frames - f0);
+        if (tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // the previous tile's reads first
+            bar_expect_tx(bar, (uint32_t)nf * ((uint32_t)Kt * 4 + 8u * (uint32_t)SN + 32u));
+            if (p.ld == Kt) {
+                bulk_load(nb, p.n_in + (size_t)f0 * Kt, (uint32_t)nf * Kt * 4, bar);
+            } else {
+                for (int f = 0; f < nf; ++f) bulk_load(nb + (size_t)f * Kt, p.n_in + (size_t)(f0 + f) * p.ld, Kt * 4, bar);
+            }
+            for (int f = f0; f < f0 + nf;) {   // runs of consecutive t inside one mixture
+                const int m = f / T, t = f - m * T, len = min(f0 + nf - f, T - t);
+                for (int s2 = 0; s2 < S; ++s2) {
+                    const size_t row = ((size_t)(m * S + s2) * T + t) * N;
+                    const size_t dst = ((size_t)s2 * FT + (f - f0)) * N;
+                    bulk_load(ub + dst, p.u_fwd + row, (uint32_t)len * N * 4, bar);
+                    bulk_load(bb + dst, p.b_bwd + row, (uint32_t)len * N * 4, bar);
+                }
+                f += len;
+            }
+            bulk_load(fc, p.fconst + 4 * (size_t)f0, (uint32_t)nf * 32, bar);
+        }
+        if (tid < nf) {
+            const int f = f0 + tid, m = f / T, t = f - m * T;
+            ecb[tid] = (long long)m * S * T + t;
+        }
+        bar_wait(bar, phase);
+
+        // Eq. 6 prior pseudo-counts: gq = gamma / sum_n u .* b, one warp per (frame, source)
+        for (int k = warp; k < nf * S; k += NW) {
+            const int f = div_small(k, S, invS), s2 = k - f * S;
+            const float *u = ub + ((size_t)s2 * FT + f) * N, *b = bb + ((size_t)s2 * FT + f) * N;
+            float q = 0.f;
+            for (int n = lane; n < N; n += 32) q = fmaf(u[n], b[n], q);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+            if (!(q > 0.f) || !(q < INFINITY)) bad |= FLAG_NONFINITE;
+            if (lane == 0) gq[k] = gamma * __frcp_rn(q);
+        }
+        __syncthreads();
+
+        // element pass: warp w owns frames w, w + NW, ...; lane = (frame, block) item
+        {
+            const int nfw = warp < nf ? (nf - warp + NW - 1) / NW : 0;
+            float hsum[TILE_MAXFW] = {0.f, 0.f, 0.f, 0.f};
+            const int items = nfw * SN;
+            for (int i0 = 0; i0 < items; i0 += 32) {
+                const int i = i0 + lane;
+                if (i < items) {
+                    const int jj = div_small(i, SN, invSN), b = i - jj * SN;
+                    const int f = warp + NW * jj;
+                    const int s2 = div_small(b, N, invN), n = b - s2 * N;
+                    const size_t ui = ((size_t)s2 * FT + f) * N + n;
+                    const uint64_t dv2 = f2c(fmaf(gq[f * S + s2], ub[ui] * bb[ui], 1.f));
+                    const uint64_t e0_2 = f2c((float)fc[4 * f + 3]);
+                    float *pn = nb + (size_t)f * Kt + b * K;
+                    float *arow = p.alpha + (size_t)(f0 + f) * p.ld + b * K;
+                    double sp = 0.0;
+                    uint64_t hg2 = 0ull;
+                    if (EVEN) {
+                        for (int j = 0; j < K; j += 2) {
+                            const float2 nv = *reinterpret_cast<const float2 *>(pn + j);
+                            const uint64_t a2 = f2add(f2pack(nv.x, nv.y), dv2);
+                            float a0, a1;
+                            f2unpack(a2, a0, a1);
+                            uint64_t ps2, th2, g2;
+                            elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                            float p0, p1, t0, t1;
+                            f2unpack(ps2, p0, p1);
+                            f2unpack(th2, t0, t1);
+                            sp += (double)p0 + (double)p1;
+                            hg2 = f2add(hg2, g2);
+                            *reinterpret_cast<float2 *>(pn + j) = make_float2(t0, t1);
+                            if (want_a) *reinterpret_cast<float2 *>(arow + j) = make_float2(a0, a1);
+                        }
+                    } else {
+                        for (int j = 0; j < K; j += 2) {
+                            const bool two = j + 1 < K;
+                            const uint64_t a2 = f2add(f2pack(pn[j], two ? pn[j + 1] : 0.f), dv2);
+                            float a0, a1;
+                            f2unpack(a2, a0, a1);
+                            uint64_t ps2, th2, g2;
+                            elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                            float p0, p1, t0, t1, g0, g1;
+                            f2unpack(ps2, p0, p1);
+                            f2unpack(th2, t0, t1);
+                            f2unpack(g2, g0, g1);
+                            sp += (double)p0 + (two ? (double)p1 : 0.0);
+                            hg2 = f2add(hg2, f2pack(g0, two ? g1 : 0.f));
+                            pn[j] = t0;
+                            if (two) pn[j + 1] = t1;
+                            if (want_a) {
+                                arow[j] = a0;
+                                if (two) arow[j + 1] = a1;
+                            }
+                        }
+                    }
+                    sps[(size_t)f * SN + b] = sp;
+                    float h0, h1;
+                    f2unpack(hg2, h0, h1);
+#pragma unroll
+                    for (int k = 0; k < TILE_MAXFW; ++k)
+                        if (k == jj) hsum[k] += h0 + h1;
+                }
+            }
+            if (want_h) {   // per-frame bound term (FP32 warp sum, as in the kernels above)
+#pragma unroll
+                for (int k = 0; k < TILE_MAXFW; ++k) {
+                    if (k >= nfw) break;
+                    float h = hsum[k];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+                    const int f = warp + NW * k;
+                    if (lane == 0) p.hdir[f0 + f] = (double)h + fc[4 * f + 2];
+                }
+            }
+        }
+        __syncthreads();
+
+        // theta leaves (coalesced float4 rows; contiguous when ld == Kt)
+        {
+            const int q4 = Kt >> 2;
+            if (p.ld == Kt) {
+                float4 *dst = reinterpret_cast<float4 *>(p.theta + (size_t)f0 * Kt);
+                const float4 *src = reinterpret_cast<const float4 *>(nb);
+                for (int q = tid; q < nf * q4; q += TILE_THREADS) dst[q] = src[q];
+            } else {
+                for (int q = tid; q < nf * q4; q += TILE_THREADS) {
+                    const int f = q / q4, c = q - f * q4;
+                    reinterpret_cast<float4 *>(p.theta + (size_t)(f0 + f) * p.ld)[c] =
+                        reinterpret_cast<const float4 *>(nb + (size_t)f * Kt)[c];
+                }
+            }
+        }
+        // Eq. 8 per (frame, source): max in FP32 (over the FP64 sums), offset eoff = gamma (max - K psi_0);
+        // the max goes to gq (no longer needed)
+        for (int k = warp; k < nf * S; k += NW) {   // one warp per (frame, source)
+            const int f = div_small(k, S, invS), s2 = k - f * S;
+            const double *v = sps + (size_t)f * SN + s2 * N;
+            float mxf = -INFINITY;
+            for (int n = lane; n < N; n += 32) mxf = fmaxf(mxf, (float)v[n]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+            if (lane == 0) {
+                gq[k] = mxf;
+                const double off = (double)gamma * ((double)mxf - (double)K * fc[4 * f + 1]);
+                p.eoff[(size_t)ecb[f] + (size_t)s2 * T] = off;
+                if (!isfinite(off)) bad |= FLAG_NONFINITE;
+            }
+        }
+        __syncthreads();
+        // emissions, one thread per (frame, block): e = exp(gamma (phi - max)) in (0, 1]
+        for (int j = tid; j < nf * SN; j += TILE_THREADS) {
+            const int f = div_small(j, SN, invSN), b = j - f * SN;
+            const int s2 = div_small(b, N, invN), n = b - s2 * N;
+            const double mx = (double)gq[f * S + s2];
+            p.ec[((size_t)ecb[f] + (size_t)s2 * T) * N + n] =
+                ex2_sfu((float)((double)gamma * (sps[j] - mx)) * 1.44269504088896341f);
+        }
+        __syncthreads();   // the next tile's copies overwrite the buffers
+    }
+    if (bad) atomicOr(p.flags, bad);
+}
+
 // ---------------------------------------------------------------------------------------------------
 // Fused path (the element work of (c)+(d) runs in the back-projection GEMM's epilogue, gemm_tc.cu):
 //   dv_kernel   (before the GEMM)  dvT[b][f] = gamma d_{s,t,n} + 1 for block b = s N + n,
@@ -506,6 +762,49 @@ cudaError_t launch_eq8(const DirichletArgs &a, const double *spsT, const double 
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
     const int SN = a.S * a.N;
     const PipeLayout L(a.S, a.N, a.Kt);
+    if (a.variant == 1 && a.N % 4 == 0 && a.Kt % 4 == 0 && a.ld % 4 == 0) {
+        // frame tile: 2 frames per warp (so a warp's (frame, block) items fill its lanes), as many warps as
+        // fit the shared-memory budget, 4 or 8 (NFHMM_DIR_TILE=warps,KB overrides for experiments)
+        static int nw = 4, budget = 37;
+        static bool env_read = false;
+        if (!env_read) {
+            env_read = true;
+            const char *e = getenv("NFHMM_DIR_TILE");
+            if (e) sscanf(e, "%d,%d", &nw, &budget);
+            if (nw != 8) nw = 4;
+        }
+        int FT = (int)(((size_t)budget * 1024 - 16) / TileLayout::per_frame(a.S, a.N, a.Kt));
+        if (FT > TILE_MAXFW * nw) FT = TILE_MAXFW * nw;
+        FT &= ~(nw - 1);
+        if (FT >= nw) {
+            const size_t smem = TileLayout(a.S, a.N, a.Kt, FT).total;
+            const bool even = (a.K & 1) == 0;
+            const int ki = (even ? 1 : 0) + (nw == 8 ? 2 : 0);
+            auto kern = nw == 8 ? (even ? dirichlet_tile_kernel<true, 8> : dirichlet_tile_kernel<false, 8>)
+                                : (even ? dirichlet_tile_kernel<true, 4> : dirichlet_tile_kernel<false, 4>);
+            static size_t attr_t[4] = {0, 0, 0, 0};
+            if (smem > 48 * 1024 && attr_t[ki] < smem) {
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+                attr_t[ki] = smem;
+            }
+            static int sms_t = 0, per_sm_t[4] = {0, 0, 0, 0};
+            static size_t per_sm_smem_t[4] = {0, 0, 0, 0};
+            if (!sms_t || per_sm_smem_t[ki] != smem) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms_t, cudaDevAttrMultiProcessorCount, dev);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t[ki], kern, nw * 32, smem);
+                if (per_sm_t[ki] < 1) per_sm_t[ki] = 1;
+                per_sm_smem_t[ki] = smem;
+            }
+            const long long need = (a.frames + FT - 1) / FT;
+            const long long cap = (long long)sms_t * per_sm_t[ki];
+            const int grid = (int)(need < cap ? need : cap);
+            kern<<<grid, nw * 32, smem, st>>>(a, FT);
+            return cudaGetLastError();
+        }
+    }
     if (L.total <= 12 * 1024) {   // pipelined variant (configs 0-3); config 4's 32 KB rows use the other
         const size_t smem = L.total * WPB;
         const bool even = (a.K & 1) == 0;

@@ -34,6 +34,12 @@ __device__ __forceinline__ float ex2_sfu(float x) {
 __device__ __forceinline__ void elem_pair(float a0, float a1, uint64_t e0_2, bool want_h, uint64_t &psi2,
                                           uint64_t &th2, uint64_t &g2t) {
     const uint64_t a2 = f2pack(a0, a1);
+#ifdef NFHMM_EXP_NOMATH   // bandwidth experiment only: no element math
+    psi2 = a2;
+    th2 = f2mul(a2, e0_2);
+    g2t = want_h ? a2 : 0ull;
+    return;
+#endif
     const uint64_t u2 = f2pack(rcp_sfu(a0), rcp_sfu(a1));
     const uint64_t lx2 = ln_sfu2(a0, a1);
     const uint64_t t2 = f2fma(u2, f2c(2.f), f2c(-1.f));

@@ -37,6 +37,7 @@ struct nfhmm {
     // Dirichlet step fused into the back-projection epilogue (tensor-core engine, K <= 32): block-major
     // pseudo-counts, Eq. 8 block sums and g~ partials, frame pitch ldf
     bool fused = false;
+    int dir_variant = 0;   // Dirichlet kernel variant (NFHMM_DIRICHLET=tile: frame-tile kernel)
     int ldf = 0, nt_tc_b = 0;
     float *dvT = nullptr;
     double *spsT = nullptr, *sps2T = nullptr, *hpartT = nullptr;
@@ -308,6 +309,7 @@ DirichletArgs dirichlet_args(nfhmm_t *h, bool write_alpha) {
     d.hdir = h->free_energy ? h->hdir : nullptr;
     d.flags = h->flags;
     d.ldf = h->ldf;
+    d.variant = h->dir_variant;
     return d;
 }
 
@@ -519,6 +521,8 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         h->bn_tc_b = h->fused ? tc_pick_bn(Kt, l) : tc_pick_bn(Kt);
         h->nt_tc_b = (int)((Kt + h->bn_tc_b - 1) / h->bn_tc_b);
         h->ldf = (int)((frames + 31) / 32 * 32);
+        const char *ed = getenv("NFHMM_DIRICHLET");
+        h->dir_variant = (ed && strcmp(ed, "tile") == 0) ? 1 : 0;
     }
     h->nt_tc_a = (int)((F + h->bn_tc_a - 1) / h->bn_tc_a);
     // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)
@@ -746,6 +750,12 @@ int nfhmm_posteriors(nfhmm_t *h, float *d_hat, float *alpha_hat, float *V_hat, d
 }
 
 int nfhmm_separate(nfhmm_t *h, float *V_star, float *V_src) {
+    int r = nfhmm_separate_async(h, V_star, V_src);
+    if (r) return r;
+    return check_flags(h);
+}
+
+int nfhmm_separate_async(nfhmm_t *h, float *V_star, float *V_src) {
     int r = enter(h);
     if (r) return r;
     if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "model and observations required");
@@ -777,7 +787,7 @@ int nfhmm_separate(nfhmm_t *h, float *V_star, float *V_src) {
     const bool dev = is_device_ptr(V_star);
     LAUNCH(h, NFHMM_K_SEPARATE, launch_wiener(h->V, h->Fa, h->vsrc, dev ? V_star : h->vsrc, (int)h->M, h->S, (int)h->T, (int)h->F, h->st));
     if (!dev) CU(h, cudaMemcpyAsync(V_star, h->vsrc, n * 4, cudaMemcpyDeviceToHost, h->st));
-    return check_flags(h);
+    return NFHMM_OK;
 }
 
 int nfhmm_profile_enable(nfhmm_t *h, int on) {

@@ -97,6 +97,7 @@ struct DirichletArgs {
     double *eoff;             // [M][S][T]     out: gamma * max_n phi (FP64)
     double *hdir;             // [frames]      out: Dirichlet entropy terms of the bound (or NULL)
     int ldf;                  // fused path: frame pitch of the block-major arrays
+    int variant;              // 0: per-warp pipelined kernel; 1: frame-tile kernel (NFHMM_DIRICHLET=tile)
     unsigned *flags;
 };
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st);

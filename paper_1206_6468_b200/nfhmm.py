@@ -52,6 +52,7 @@ SIGNATURES = {
     "nfhmm_sync": (ctypes.c_int, [_P]),
     "nfhmm_posteriors": (ctypes.c_int, [_P, _P, _P, _P, _P, ctypes.POINTER(_I32)]),
     "nfhmm_separate": (ctypes.c_int, [_P, _P, _P]),
+    "nfhmm_separate_async": (ctypes.c_int, [_P, _P, _P]),
     "nfhmm_destroy": (ctypes.c_int, [_P]),
     "nfhmm_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "nfhmm_last_error": (ctypes.c_char_p, [_P]),
@@ -161,6 +162,10 @@ def nfhmm_posteriors(h, d_hat=None, alpha_hat=None, V_hat=None, free_energy=None
 
 def nfhmm_separate(h, V_star, V_src=None):
     _check(h, _lib.nfhmm_separate(h, _ptr(V_star), _ptr(V_src)))
+
+
+def nfhmm_separate_async(h, V_star, V_src=None):
+    _check(h, _lib.nfhmm_separate_async(h, _ptr(V_star), _ptr(V_src)))
 
 
 def nfhmm_destroy(h):
@@ -295,9 +300,10 @@ class NFHMM:
             out["free_energy"] = fe[:, :min(it, self.max_iters)]
         return out
 
-    def separate_into(self, V_star, V_src=None):
-        """Separation into caller buffers (torch CUDA tensors, pinned host tensors or numpy arrays)."""
-        nfhmm_separate(self.h, V_star, V_src)
+    def separate_into(self, V_star, V_src=None, sync=True):
+        """Separation into caller buffers (torch CUDA tensors, pinned host tensors or numpy arrays).
+        sync=False: enqueue only (nfhmm_separate_async); read the outputs after sync()."""
+        (nfhmm_separate if sync else nfhmm_separate_async)(self.h, V_star, V_src)
 
     def separate(self, V_src=False):
         M, S, T, F = self.n_mix, self.S, self.T, self.F

@@ -214,3 +214,18 @@ def test_fused_dirichlet_epilogue_matches_separate_kernel(c, over, monkeypatch):
     o = run_oracle(cfg, model, V[0], 5)
     assert rel_l2(fus["V_star"][0], o["V_star"]) <= TOL_VSTAR
     assert np.all(np.abs(fus["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
+
+
+@pytest.mark.parametrize("c,over", [(0, {}), (2, dict(T=150))])
+def test_frame_tile_dirichlet_variant_matches(c, over, monkeypatch):
+    """Opt-in NFHMM_DIRICHLET=tile (frame-tile Dirichlet kernel: bulk copies, per-(frame, source) work
+    spread over the CTA) agrees with the default kernel and the oracle."""
+    cfg, model, V = make_inputs(c, **over)
+    ref = run_gpu(cfg, model, V, 5)
+    monkeypatch.setenv("NFHMM_DIRICHLET", "tile")
+    tile = run_gpu(cfg, model, V, 5)
+    for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
+        assert rel_l2(tile[key], ref[key]) <= 2e-6, key
+    assert np.all(np.abs(tile["free_energy"] - ref["free_energy"]) <= 1e-7 * np.abs(ref["free_energy"]))
+    o = run_oracle(cfg, model, V[0], 5)
+    assert rel_l2(tile["V_star"][0], o["V_star"]) <= TOL_VSTAR
