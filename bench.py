@@ -346,13 +346,16 @@ def run_ours(args):
             flops = 2.0 * frames_local * cfg.F * cfg.Kt       # algorithmic FLOPs per launch (true F, Kt)
             achieved = flops / t_launch / 1e12
             if args.math == "tc":
-                # FP32 contraction as 3xTF32 on tcgen05: TF32 dense = measured bf16 burst x 1/2 (nominal
-                # 1.1 / 2.25 PFLOP/s), three MMAs per product -> FP32-equivalent peak = TF32 / 3
-                tf32 = float(peaks.get("bf16_tflops", 1645.8)) * 0.5
-                peak = tf32 / 3.0
+                # FP32 contraction as 3xTF32 on tcgen05: TF32 dense = measured bf16 x 1/2 (nominal 1.1 / 2.25
+                # PFLOP/s), three MMAs per product -> FP32-equivalent peak = TF32 / 3.  The GEMMs run inside
+                # a long step (hundreds of ms back to back, power-capped clocks), so the sustained bf16
+                # figure is the denominator (the recipe's rule); the burst-based fraction is reported too.
+                bf16_s = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1645.8)))
+                bf16_b = float(peaks.get("bf16_tflops", 1645.8))
+                peak = bf16_s * 0.5 / 3.0
                 return {"kernel": k, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                        "frac": achieved / peak,
-                        "peak_note": f"3xTF32 FP32-equivalent: measured bf16 {peaks.get('bf16_tflops', 1645.8)} TF/s x 1/2 (TF32) / 3",
+                        "frac": achieved / peak, "frac_vs_burst": achieved / (bf16_b * 0.5 / 3.0),
+                        "peak_note": f"3xTF32 FP32-equivalent: measured sustained bf16 {bf16_s} TF/s x 1/2 (TF32) / 3",
                         "fp32_ffma_peak": fp32_peak}
             return {"kernel": k, "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                     "frac": achieved / fp32_peak, "peak_note": f"FP32 FFMA 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz"}
