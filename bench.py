@@ -43,7 +43,7 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--iters", type=int, default=None, help="VB sweeps per step (default: the config's)")

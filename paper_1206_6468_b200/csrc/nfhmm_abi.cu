@@ -38,6 +38,7 @@ struct nfhmm {
     // pseudo-counts, Eq. 8 block sums and g~ partials, frame pitch ldf
     bool fused = false;
     int dir_variant = 0;   // Dirichlet kernel variant (NFHMM_DIRICHLET=tile: frame-tile kernel)
+    int fb_wide = 1;       // N > 64: multi-warp forward-backward (NFHMM_FB_WIDE=0: one warp per direction)
     int ldf = 0, nt_tc_b = 0;
     float *dvT = nullptr;
     double *spsT = nullptr, *sps2T = nullptr, *hpartT = nullptr;
@@ -353,6 +354,7 @@ int step_fb(nfhmm_t *h) {
     f.bstart = h->fbB;
     f.logZ = h->logZ;
     f.flags = h->flags;
+    f.wide = h->fb_wide;
     LAUNCH(h, NFHMM_K_FB, launch_fb(f, h->st));
     return NFHMM_OK;
 }
@@ -523,6 +525,8 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         h->ldf = (int)((frames + 31) / 32 * 32);
         const char *ed = getenv("NFHMM_DIRICHLET");
         h->dir_variant = (ed && strcmp(ed, "tile") == 0) ? 1 : 0;
+        const char *ew = getenv("NFHMM_FB_WIDE");
+        h->fb_wide = (ew && atoi(ew) == 0) ? 0 : 1;
     }
     h->nt_tc_a = (int)((F + h->bn_tc_a - 1) / h->bn_tc_a);
     // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)

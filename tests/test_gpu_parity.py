@@ -229,3 +229,19 @@ def test_frame_tile_dirichlet_variant_matches(c, over, monkeypatch):
     assert np.all(np.abs(tile["free_energy"] - ref["free_energy"]) <= 1e-7 * np.abs(ref["free_energy"]))
     o = run_oracle(cfg, model, V[0], 5)
     assert rel_l2(tile["V_star"][0], o["V_star"]) <= TOL_VSTAR
+
+
+@pytest.mark.parametrize("c,over", [(4, dict(T=120, M=2)), (4, dict(T=97, M=1, N=70))])
+def test_wide_forward_backward_matches_one_warp_kernel(c, over, monkeypatch):
+    """N > 64: the multi-warp forward-backward (a CTA of ceil(N/32) warps per chain and direction, A in
+    registers) agrees with the one-warp kernel (A in shared memory) and with the oracle."""
+    cfg, model, V = make_inputs(c, **over)
+    wide = run_gpu(cfg, model, V, 4)
+    monkeypatch.setenv("NFHMM_FB_WIDE", "0")
+    one = run_gpu(cfg, model, V, 4)
+    for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
+        assert rel_l2(wide[key], one[key]) <= 2e-6, key
+    assert np.all(np.abs(wide["free_energy"] - one["free_energy"]) <= 1e-7 * np.abs(one["free_energy"]))
+    o = run_oracle(cfg, model, V[0], 4)
+    assert rel_l2(wide["V_star"][0], o["V_star"]) <= TOL_VSTAR
+    assert np.all(np.abs(wide["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
