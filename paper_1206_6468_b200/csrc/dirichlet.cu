@@ -41,11 +41,14 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int SN = p.S * p.N, K = p.K;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // per warp: sps [SN] doubles (Eq. 8 block sums) | dvs [SN] floats (prior pseudo-counts), 16-B aligned
+    // per warp: sps [SN] doubles (Eq. 8 block sums) | dvs [SN] floats (prior pseudo-counts) | rb [32 K]
+    // floats (one round of 32 blocks of the n row, staged with coalesced loads), 16-B aligned
     const size_t sps_b = ((size_t)SN * 8 + 15) & ~size_t(15), dvs_b = ((size_t)SN * 4 + 15) & ~size_t(15);
-    unsigned char *base = smem_raw + warp * (sps_b + dvs_b);
+    const size_t rb_b = ((size_t)32 * K * 4 + 15) & ~size_t(15);
+    unsigned char *base = smem_raw + warp * (sps_b + dvs_b + rb_b);
     double *sps = reinterpret_cast<double *>(base);
     float *dvs = reinterpret_cast<float *>(base + sps_b);
+    float *rb = reinterpret_cast<float *>(base + sps_b + dvs_b);
 
     const int f = blockIdx.x * WPB + warp;
     if (f >= p.frames) return;
@@ -74,58 +77,63 @@ __global__ void __launch_bounds__(WPB * 32) dirichlet_kernel(DirichletArgs p) {
     const uint64_t e0_2 = f2c((float)p.fconst[4 * (size_t)f + 3]);   // e^{-psi(alpha_0)}
     __syncwarp();
 
-    // lane b owns (s, n) block b of each round of 32 blocks: its K elements are contiguous, so the
-    // pseudo-count is one register, the Eq. 8 sum is lane-local, and I/O is in 8-byte pairs (K even;
-    // the warp's accesses of one pair index cover 32 K consecutive floats)
+    // rounds of 32 blocks: the round's n span (32 K contiguous floats) is staged with coalesced float4
+    // loads, lane b owns block b of the round (pseudo-count in one register, lane-local Eq. 8 sum), theta
+    // replaces n in the staging buffer and leaves with coalesced stores
     const float *nrow = p.n_in + (size_t)f * p.ld;
     float *arow = p.alpha + (size_t)f * p.ld;
     float *trow = p.theta + (size_t)f * p.ld;
     const bool want_h = p.hdir != nullptr, want_a = p.write_alpha != 0;
     uint64_t hg2 = 0ull;   // packed running sum of g~ over this lane's elements
-    for (int b = lane; b - lane < SN; b += 32) {
-        if (b < SN) {
+    for (int r0 = 0; r0 < SN; r0 += 32) {
+        const int nb = min(32, SN - r0), cnt = nb * K, k0r = r0 * K;   // k0r * 4 is a multiple of 16
+        const int c4 = cnt >> 2;
+        {
+            const float4 *src = reinterpret_cast<const float4 *>(nrow + k0r);
+            float4 *dst = reinterpret_cast<float4 *>(rb);
+            for (int q = lane; q < c4; q += 32) dst[q] = src[q];
+            for (int q = 4 * c4 + lane; q < cnt; q += 32) rb[q] = nrow[k0r + q];
+        }
+        __syncwarp();
+        if (lane < nb) {
+            const int b = r0 + lane;
             const float dv = dvs[b];
             const uint64_t dv2 = f2c(dv);
+            float *pn = rb + lane * K;
             const int k0 = b * K;
             double sp = 0.0;
-            if ((K & 1) == 0) {
-                for (int j = 0; j < K; j += 2) {
-                    const float2 nv = *reinterpret_cast<const float2 *>(nrow + k0 + j);
-                    uint64_t a2 = f2add(f2pack(nv.x, nv.y), dv2);
-                    float a0, a1;
-                    f2unpack(a2, a0, a1);
-                    uint64_t ps2, th2, g2;
-                    elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
-                    float p0, p1, t0, t1;
-                    f2unpack(ps2, p0, p1);
-                    f2unpack(th2, t0, t1);
-                    sp += (double)p0 + (double)p1;
-                    hg2 = f2add(hg2, g2);
-                    if (want_a) *reinterpret_cast<float2 *>(arow + k0 + j) = make_float2(a0, a1);
-                    *reinterpret_cast<float2 *>(trow + k0 + j) = make_float2(t0, t1);
-                }
-            } else {   // odd K: scalar I/O, pairs (j, j+1) with a dummy partner for the last element
-                for (int j = 0; j < K; j += 2) {
-                    const bool two = j + 1 < K;
-                    const float a0 = nrow[k0 + j] + dv, a1 = two ? nrow[k0 + j + 1] + dv : 1.f;
-                    uint64_t ps2, th2, g2;
-                    elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
-                    float p0, p1, t0, t1, g0, g1;
-                    f2unpack(ps2, p0, p1);
-                    f2unpack(th2, t0, t1);
-                    f2unpack(g2, g0, g1);
-                    sp += (double)p0 + (two ? (double)p1 : 0.0);
-                    hg2 = f2add(hg2, f2pack(g0, two ? g1 : 0.f));
-                    if (want_a) arow[k0 + j] = a0;
-                    trow[k0 + j] = t0;
-                    if (two) {
-                        if (want_a) arow[k0 + j + 1] = a1;
-                        trow[k0 + j + 1] = t1;
-                    }
+            for (int j = 0; j < K; j += 2) {
+                const bool two = j + 1 < K;
+                const float n0 = pn[j], n1 = two ? pn[j + 1] : 0.f;
+                const uint64_t a2 = f2add(f2pack(n0, n1), dv2);
+                float a0, a1;
+                f2unpack(a2, a0, a1);
+                if (!two) a1 = 1.f;
+                uint64_t ps2, th2, g2;
+                elem_pair(a0, a1, e0_2, want_h, ps2, th2, g2);
+                float p0, p1, t0, t1, g0, g1;
+                f2unpack(ps2, p0, p1);
+                f2unpack(th2, t0, t1);
+                f2unpack(g2, g0, g1);
+                sp += (double)p0 + (two ? (double)p1 : 0.0);
+                hg2 = f2add(hg2, f2pack(g0, two ? g1 : 0.f));
+                pn[j] = t0;
+                if (two) pn[j + 1] = t1;
+                if (want_a) {
+                    arow[k0 + j] = a0;
+                    if (two) arow[k0 + j + 1] = a1;
                 }
             }
             sps[b] = sp;
         }
+        __syncwarp();
+        {
+            const float4 *src = reinterpret_cast<const float4 *>(rb);
+            float4 *dst = reinterpret_cast<float4 *>(trow + k0r);
+            for (int q = lane; q < c4; q += 32) dst[q] = src[q];
+            for (int q = 4 * c4 + lane; q < cnt; q += 32) trow[k0r + q] = rb[q];
+        }
+        __syncwarp();
     }
     float hg;
     {
@@ -845,7 +853,8 @@ cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
         kern<<<grid, WPB * 32, smem, st>>>(a);
         return cudaGetLastError();
     }
-    const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15));
+    const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15)) +
+                            (((size_t)32 * a.K * 4 + 15) & ~size_t(15));
     const size_t smem = per_warp * WPB;
     static size_t attr = 0;
     if (smem > 48 * 1024 && attr < smem) {
