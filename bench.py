@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--math", choices=["tc", "simt"], default="tc",
                     help="contraction engine: tcgen05 3xTF32 (default) or FP32 FFMA")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-bound-off", action="store_true", help="skip the timing with the free energy off")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds for the oracle sample")
     return ap.parse_args()
@@ -276,6 +277,35 @@ def run_ours(args):
     frame_iters = cfg.M * cfg.T * iters                     # whole job, all ranks
     value = frame_iters / (ms_per_step / 1000.0)
 
+    # ---- the same steps with the bound off (report L-on and L-off) ------------------
+    value_bound_off = None
+    if not args.no_bound_off:
+        hb = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, device=dev, max_iters=max(iters, 1), stream=stream,
+                   math=args.math, free_energy=False)
+        hb.set_model(model.beta, model.trans, model.prior)
+        hb.set_observations(Vd)
+
+        def step_b():
+            hb.reset()
+            hb.vb_iterate_async(iters)
+            hb.separate_into(vstar_d)
+
+        step_b()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            step_b()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        elb = b0.elapsed_time(b1)
+        if world > 1:
+            elb = pdist.max_over_ranks(elb, device=f"cuda:{dev}")
+        value_bound_off = frame_iters / (elb / args.steps / 1000.0)
+        hb.close()
+
     # ---- e2e: public API with host buffers, copies inside the timed region -------------------
     # Every step copies its V from pinned host memory, runs the sweeps and the separation, and reads
     # the separated spectrograms back into pinned host memory.  Steps alternate between two handles on
@@ -398,6 +428,7 @@ def run_ours(args):
                        "l2": "no flush: per-step inputs/state exceed L2 (V %.2f GB, theta %.2f GB per GPU)" % (
                            M * cfg.T * h.layout()["F_pad"] * 4 / 1e9, M * cfg.T * h.layout()["Kt_pad"] * 4 / 1e9),
                        "step": "reset + iters sweeps + separate, inputs resident in HBM"},
+            "value_bound_off": value_bound_off,
             "roofline": roof, "rooflines": roof_all, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches, "gen_seconds": round(t_gen, 2),
         }
