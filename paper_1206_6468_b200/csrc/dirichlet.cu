@@ -822,13 +822,12 @@ cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
     if (L.total <= 12 * 1024) {   // pipelined variant (configs 0-3); config 4's 32 KB rows use the other
         // one frame buffer per warp (4 CTAs = 32 warps per SM hide the load latency) measured 4.5 % faster
         // than two buffers (3 CTAs, next frame prefetched); NFHMM_DIR_NBUF=2 selects the latter
-        static int nbuf = -1;   // NFHMM_DIR_NBUF=0: the round-staged kernel below (experiment)
-        if (nbuf < 0) {
+        // (the round-staged kernel below measured 1.50 vs 1.13 ms at config 3)
+        static int nbuf = 0;
+        if (!nbuf) {
             const char *e = getenv("NFHMM_DIR_NBUF");
-            nbuf = e ? atoi(e) : 1;
-            if (nbuf < 0 || nbuf > 2) nbuf = 1;
+            nbuf = (e && atoi(e) == 2) ? 2 : 1;
         }
-        if (nbuf == 0) goto rounds;
         const size_t smem = PipeLayout(a.S, a.N, a.Kt, nbuf).total * WPB;
         const bool even = (a.K & 1) == 0;
         auto kern = nbuf == 1 ? (even ? dirichlet_pipe_kernel<true, 1> : dirichlet_pipe_kernel<false, 1>)
@@ -855,7 +854,6 @@ cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
         kern<<<grid, WPB * 32, smem, st>>>(a);
         return cudaGetLastError();
     }
-rounds:
     const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15)) +
                             (((size_t)32 * a.K * 4 + 15) & ~size_t(15));
     const size_t smem = per_warp * WPB;
