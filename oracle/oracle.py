@@ -17,6 +17,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "nfhmm_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "nhmm_em_oracle.c")]   # VB iteration; N-HMM EM training (NEXT-3)
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 OR_OK, OR_EINVAL, OR_EZEROSUPPORT, OR_ENUMERIC = 0, -1, -5, -6
@@ -24,8 +25,8 @@ OR_OK, OR_EINVAL, OR_EZEROSUPPORT, OR_ENUMERIC = 0, -1, -5, -6
 
 def build(force: bool = False) -> str:
     """Compile the oracle: plain gcc -O2, IEEE FP64, no -ffast-math, no threads, no BLAS."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f) for f in _SRCS):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-o", _LIB, *_SRCS, "-lm"])
     return _LIB
 
 
@@ -52,6 +53,9 @@ def lib():
         L.or_bound.argtypes = [i, i, i, i, d, d, P, P]
         L.or_separate.argtypes = [i, i, i, i, i, P, P, P, P, P]
         L.or_vb_run.argtypes = [i, i, i, i, i, d, P, P, P, P, i, i, P, P, P, P, P]
+        L.or_fb_pairwise.argtypes = [i, i, P, P, P, P, P, P]
+        L.or_nhmm_loglik.argtypes = [i, i, i, i, P, P, P, P]
+        L.or_nhmm_em_step.argtypes = [i, i, i, i, P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -175,3 +179,42 @@ def vb_run(beta, trans, prior, V, dims, n_iters, gamma=1.0, state=None):
     _check(lib().or_vb_run(F, T, S, N, K, gamma, _p(b), _p(tr), _p(pr), _p(v), n_iters, init,
                            _p(alpha), _p(d), _p(vh), _p(fe), _p(lz)))
     return dict(alpha=alpha, d_hat=d, V_hat=vh, free_energy=fe[:n_iters], logZ=lz)
+
+
+# ---- N-HMM maximum-likelihood EM (nhmm_em_oracle.c) ----------------------------------
+
+def fb_pairwise(loglik, A, pi):
+    """Returns (marg [T][N], xi_sum [N][N] = sum_{t>=1} xi_t, logZ)."""
+    ll, A, pi = _f64(loglik), _f64(A), _f64(pi)
+    T, N = ll.shape
+    marg = np.empty((T, N))
+    xi = np.empty((N, N))
+    lz = ctypes.c_double()
+    _check(lib().or_fb_pairwise(T, N, _p(ll), _p(A), _p(pi), _p(marg), _p(xi), ctypes.byref(lz)))
+    return marg, xi, lz.value
+
+
+def nhmm_loglik(V, beta, theta):
+    """V [T][F], beta [N][K][F], theta [T][N][K] -> loglik [T][N]."""
+    v, b, th = _f64(V), _f64(beta), _f64(theta)
+    T, F = v.shape
+    N, K, _ = b.shape
+    ll = np.empty((T, N))
+    _check(lib().or_nhmm_loglik(F, T, N, K, _p(v), _p(b), _p(th), _p(ll)))
+    return ll
+
+
+def nhmm_em(V, beta, theta, A, pi, n_iters):
+    """n_iters EM iterations from (beta [N][K][F], theta [T][N][K], A [N][N], pi [N]); returns
+    dict(beta, theta, A, pi, loglik [n_iters]) -- loglik[i] is the log evidence of the parameters
+    iteration i started from."""
+    v = _f64(V)
+    b, th, a, p = _f64(beta).copy(), _f64(theta).copy(), _f64(A).copy(), _f64(pi).copy()
+    T, F = v.shape
+    N, K, _ = b.shape
+    ll = np.empty(n_iters)
+    for i in range(n_iters):
+        lz = ctypes.c_double()
+        _check(lib().or_nhmm_em_step(F, T, N, K, _p(v), _p(b), _p(th), _p(a), _p(p), ctypes.byref(lz)))
+        ll[i] = lz.value
+    return dict(beta=b, theta=th, A=a, pi=p, loglik=ll)
