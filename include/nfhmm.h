@@ -174,6 +174,47 @@ int nfhmm_profile_read(nfhmm_t *h, double *ms, int64_t *launches);
  * ms_per_launch. */
 int nfhmm_bench_kernel(nfhmm_t *h, int cls, int32_t reps, double *ms_per_launch);
 
+/* ---------------------------------------------------------------------------------------------------
+ * N-HMM maximum-likelihood EM training: learns each source's dictionaries,
+ * transition matrix and initial distribution from an isolated-source spectrogram, the step before the
+ * separation path.  The paper gives only "maximum-likelihood (ML) values of all these parameters may be
+ * found by the EM algorithm" for the model of P:76-83; the iteration follows SPEC's em_step
+ * (S:179-181): E-step lhat_{t,d}(l) = sum_z theta_t(d)_z beta_l(d,z), log-likelihood of frame t in state d
+ * sum_l V_lt log lhat, forward-backward -> gamma, xi; M-step theta_t(d)_z ∝ sum_l V_lt P(z|l,t,d),
+ * beta_l(d,z) ∝ sum_t gamma_t(d) V_lt P(z|l,t,d), rho ∝ sum_t xi_t, pi = gamma_0.  n_src independent sources
+ * are trained in the same launches.
+ * Layouts (FP32, row-major; any argument may be a host or a device pointer, as above):
+ *   V       [n_src][T][F]      counts >= 0, finite
+ *   dict    [n_src][N][K][F]   beta_l(d, z) = dict[s][d][z][l], each element sums to 1 over l
+ *   trans   [n_src][N][N]      row-stochastic, trans[s][i][j] = P(D_t = j | D_{t-1} = i) (DESIGN R4)
+ *   prior   [n_src][N]
+ *   weights [n_src][T][N][K]   theta_t(d), each (t, d) row sums to 1 (NULL at set_params: uniform 1/K)
+ *   loglik  [n_src][max_iters] FP64 log evidence (multinomial coefficient omitted) of the parameters
+ *                              iteration i started from; non-decreasing in i
+ * Limits: 1 <= N <= 128, 1 <= K <= 32, K*F <= 51200.  The handle allocates its own device memory.
+ * Errors: NFHMM_EINVAL (dimensions, NULL, negative / non-finite data, n_iters beyond max_iters),
+ * NFHMM_ESTATE (em before set_data + set_params), NFHMM_EZEROSUPPORT (a frame no state can explain),
+ * NFHMM_ENUMERIC, NFHMM_ECUDA, NFHMM_ENOMEM; detail in nhmm_train_last_error(). */
+typedef struct nhmm_train nhmm_train_t;   /* opaque, library-owned */
+
+int nhmm_train_create(int64_t F, int64_t T, int32_t N, int32_t K, int64_t n_src, int32_t max_iters, int32_t device,
+                      void *stream /* cudaStream_t or NULL */, nhmm_train_t **out);
+/* Copy and validate the training spectrograms.  Synchronises. */
+int nhmm_train_set_data(nhmm_train_t *h, const float *V);
+/* Initial parameters (the paper does not state an initialisation; S:168 draws Dirichlet dictionaries,
+ * a near-uniform chain and uniform pi).  Resets the iteration count.  Synchronises. */
+int nhmm_train_set_params(nhmm_train_t *h, const float *dict, const float *trans, const float *prior,
+                          const float *weights);
+/* n_iters EM iterations; synchronises and returns the sticky device status. */
+int nhmm_train_em(nhmm_train_t *h, int32_t n_iters);
+/* Copy out the current parameters and the log-evidence trace (any output may be NULL).  Synchronises. */
+int nhmm_train_get(nhmm_train_t *h, float *dict, float *trans, float *prior, float *weights, double *loglik,
+                   int32_t *iters_done);
+/* Kernel launches enqueued by this handle (instrumentation). */
+int nhmm_train_kernel_launches(const nhmm_train_t *h, int64_t *n);
+int nhmm_train_destroy(nhmm_train_t *h);
+const char *nhmm_train_last_error(const nhmm_train_t *h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,8 @@
  *           P(z | l, t, d) = theta_t(d)_z beta_l(d,z) / lhat_{t,d}(l);
  *   M-step  theta_t(d)_z  ∝ sum_l V_lt P(z | l, t, d);
  *           beta_l(d,z)   ∝ sum_t gamma_t(d) V_lt P(z | l, t, d);
- *           rho(i -> j)   ∝ sum_{t>=1} xi_t(i,j);  pi = gamma_0.
+ *           rho(i -> j)   ∝ sum_{t>=1} xi_t(i,j);  pi = gamma_0;
+ *           rho rows and pi floored at 1e-30 and renormalised (DESIGN R21, see floor_renorm).
  * (theta's update carries no gamma: gamma_t(d) is constant in z for fixed (t, d) and cancels in the
  * normalisation.)  Every step is the exact maximiser of the expected complete-data log-likelihood,
  * so the returned log evidence is non-decreasing across iterations.
@@ -127,6 +128,21 @@ int or_nhmm_loglik(int F, int T, int N, int K, const double *V, const double *be
     return OR_OK;
 }
 
+/* DESIGN R21: chain probabilities are floored at 1e-30 after each M-step (then renormalised).  At 10^4-10^5
+ * counts per frame the per-state log-likelihoods of a frame differ by thousands of nats, so most
+ * emission ratios exp(loglik - max) underflow to exactly 0; transitions that no posterior path used
+ * then come out exactly 0 and, one iteration later, a frame whose only explaining state is unreachable
+ * has zero evidence in floating point.  The floor keeps every path feasible and changes the evidence by
+ * O(1e-30) relative. */
+static void floor_renorm(double *p, int n) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) {
+        if (p[i] < 1e-30) p[i] = 1e-30;
+        s += p[i];
+    }
+    for (int i = 0; i < n; ++i) p[i] /= s;
+}
+
 /* One EM iteration (order of the file header).  beta, theta, A, pi are updated in place; *loglik_out is
  * the log evidence of the parameters the iteration started from. */
 int or_nhmm_em_step(int F, int T, int N, int K, const double *V, double *beta, double *theta, double *A,
@@ -180,8 +196,10 @@ int or_nhmm_em_step(int F, int T, int N, int K, const double *V, double *beta, d
         for (int j = 0; j < N; ++j) s += xi[i * N + j];
         if (s > 0.0)
             for (int j = 0; j < N; ++j) A[i * N + j] = xi[i * N + j] / s;
+        floor_renorm(A + (size_t)i * N, N);
     }
     for (int d = 0; d < N; ++d) pi[d] = g[d];
+    floor_renorm(pi, N);
 done:
     free(ll); free(g); free(xi); free(nb); free(nt);
     return st;

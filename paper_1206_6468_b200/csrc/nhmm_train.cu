@@ -1,0 +1,521 @@
+// nhmm_train.cu -- maximum-likelihood EM training of single-source N-HMMs on the GPU (SURVEY §8(f)
+// NEXT-3: "learn beta, rho, pi from isolated sources ... reuses K-a/K-b/K-e plus pairwise posteriors and
+// an M-step").  The paper states only that "maximum-likelihood (ML) values of all these parameters may
+// be found by the EM algorithm" (model P:76-83); the steps follow SPEC's em_step:
+//   E-step  lhat_{t,d}(l) = sum_z theta_t(d)_z beta_l(d,z);  loglik_{t,d} = sum_l V_lt log lhat_{t,d}(l);
+//           scaled forward-backward over each source's chain (the VB path's fb kernels, S = n_src)
+//           -> gamma_t(d), xi_t(i,j), log evidence;
+//   M-step  theta_t(d)_z ∝ theta_t(d)_z C_{t,d,z},  C_{t,d,z} = sum_l beta_l(d,z) V_lt / lhat_{t,d}(l);
+//           beta_l(d,z)  ∝ beta_l(d,z) sum_t gamma_t(d) theta_t(d)_z V_lt / lhat_{t,d}(l);
+//           rho(i -> j)  ∝ sum_{t>=1} xi_t(i,j),  xi_t(i,j) = u_{t-1}(i) A_ij e_t(j) b_t(j) / Z_t;  pi = gamma_0;
+//           rho rows and pi floored at 1e-30 and renormalised (DESIGN R21: keeps every path feasible when
+//           the emission ratios of a 1e5-count frame underflow).
+// Kernels, per EM iteration (n_src independent sources batched in every launch):
+//   estep_kernel<KM>     CTA per (source, state d, tile of frames): beta(d) [K][F] staged in shared memory,
+//                        a warp per frame, lanes over l; loglik in FP64 (per-bin terms v log lhat are
+//                        ~1e3 and the frame totals ~1e5: FP32 sums would move e = exp(loglik - max) by
+//                        ~1e-3), C_{t,d,:} by warp reductions;
+//   emission_kernel      e_t(d) = exp(loglik - max_d loglik), eoff_t = max (FP64) -> launch_fb;
+//   posterior_kernel     gamma_t = u_t .* b_t / sum and the pairwise normaliser Z_t = u_{t-1} A (e_t .* b_t);
+//   xi_kernel            sum_{t>=1} xi_t(i,j), thread per (i, j), FP64 accumulation over t;
+//   beta_kernel<KM>      thread per (source, d, l): beta_l(d,:) in registers, FP64 accumulation over t;
+//   beta_norm_kernel / mstep_kernel  normalisations, theta, rho, pi.
+// The forward-backward messages are power-of-two scaled per step (fb.cu); every consumer normalises
+// per frame, so the scales cancel exactly.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "nfhmm_internal.cuh"
+#include "../../include/nfhmm.h"
+
+namespace nfk {
+namespace {
+
+constexpr int ES_FT = 16;     // frames per estep CTA (8 warps x 2)
+constexpr int BK_THREADS = 128;
+
+template <int KM>
+__global__ void __launch_bounds__(256) estep_kernel(int F, int T, int N, int K, const float *V, const float *beta,
+                                                    const float *theta, double *LL, float *C) {
+    extern __shared__ __align__(16) float bs[];   // beta(m, d) [K][F]
+    const int m = blockIdx.z, d = blockIdx.y, t0 = blockIdx.x * ES_FT;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float *bg = beta + ((size_t)m * N + d) * K * F;
+    for (int i = threadIdx.x; i < K * F; i += blockDim.x) bs[i] = bg[i];
+    __syncthreads();
+    for (int t = t0 + warp; t < min(T, t0 + ES_FT); t += 8) {
+        const float *th = theta + (((size_t)m * T + t) * N + d) * K;
+        float tz[KM], cz[KM];
+#pragma unroll
+        for (int z = 0; z < KM; ++z) {
+            tz[z] = z < K ? th[z] : 0.f;
+            cz[z] = 0.f;
+        }
+        const float *vr = V + ((size_t)m * T + t) * F;
+        double ll = 0.0;
+        bool zero = false;
+        for (int l = lane; l < F; l += 32) {
+            const float v = vr[l];
+            if (v > 0.f) {
+                float lh = 0.f;
+#pragma unroll
+                for (int z = 0; z < KM; ++z)
+                    if (z < K) lh = fmaf(tz[z], bs[z * F + l], lh);
+                if (lh > 0.f) {
+                    ll += (double)v * log((double)lh);
+                    const float r = __fdiv_rn(v, lh);
+#pragma unroll
+                    for (int z = 0; z < KM; ++z)
+                        if (z < K) cz[z] = fmaf(bs[z * F + l], r, cz[z]);
+                } else {
+                    zero = true;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, o);
+        zero = __any_sync(0xffffffffu, zero);
+#pragma unroll
+        for (int z = 0; z < KM; ++z)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cz[z] += __shfl_xor_sync(0xffffffffu, cz[z], o);
+        if (lane == 0) LL[((size_t)m * T + t) * N + d] = zero ? -INFINITY : ll;
+        float *cd = C + (((size_t)m * T + t) * N + d) * K;
+        if (lane < K) {
+            float c = cz[0];
+#pragma unroll
+            for (int z = 1; z < KM; ++z)
+                if (z == lane) c = cz[z];
+            cd[lane] = c;
+        }
+    }
+}
+
+// one warp per (source, frame): e = exp(loglik - max_d), eoff = max_d (FP64)
+__global__ void emission_kernel(int T, int N, int MT, const double *LL, float *ec, double *eoff, unsigned *flags) {
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (w >= MT) return;
+    const double *l = LL + (size_t)w * N;
+    double mx = -INFINITY;
+    for (int d = lane; d < N; d += 32) mx = fmax(mx, l[d]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (!(mx > -INFINITY)) {
+        if (lane == 0) atomicOr(flags, FLAG_ZERO_SUPPORT);
+        mx = 0.0;
+    }
+    for (int d = lane; d < N; d += 32) ec[(size_t)w * N + d] = (float)exp(l[d] - mx);
+    if (lane == 0) eoff[w] = mx;
+}
+
+// one warp per (source, frame): gamma_t = u .* b / sum; for t >= 1, Z_t = sum_i u_{t-1}(i) sum_j A_ij e_t(j) b_t(j)
+__global__ void posterior_kernel(int T, int N, int MT, const float *u, const float *b, const float *ec, const float *A,
+                                 float *gamma, float *Zt) {
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (w >= MT) return;
+    const int m = w / T, t = w - m * T;
+    const size_t row = (size_t)w * N;
+    float s = 0.f;
+    for (int d = lane; d < N; d += 32) s += u[row + d] * b[row + d];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float is = 1.f / s;
+    for (int d = lane; d < N; d += 32) gamma[row + d] = u[row + d] * b[row + d] * is;
+    if (t == 0) {
+        if (lane == 0) Zt[w] = 1.f;
+        return;
+    }
+    const float *Am = A + (size_t)m * N * N;
+    double z = 0.0;
+    for (int i = lane; i < N; i += 32) {
+        float y = 0.f;
+        for (int j = 0; j < N; ++j) y = fmaf(Am[i * N + j], ec[row + j] * b[row + j], y);
+        z += (double)u[row - N + i] * (double)y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if (lane == 0) Zt[w] = (float)z;
+}
+
+// thread per (source, i, j): xi_sum = A_ij sum_{t>=1} u_{t-1}(i) e_t(j) b_t(j) / Z_t  (FP64 over t)
+__global__ void xi_kernel(int T, int N, int M, const float *u, const float *b, const float *ec, const float *Zt,
+                          const float *A, float *xi) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= M * N * N) return;
+    const int m = idx / (N * N), ij = idx - m * N * N, i = ij / N, j = ij - i * N;
+    const size_t base = (size_t)m * T * N;
+    double acc = 0.0;
+    for (int t = 1; t < T; ++t)
+        acc += (double)u[base + (size_t)(t - 1) * N + i] * (double)(ec[base + (size_t)t * N + j] * b[base + (size_t)t * N + j]) /
+               (double)Zt[(size_t)m * T + t];
+    xi[idx] = (float)(acc * (double)A[(size_t)m * N * N + ij]);
+}
+
+// thread per (source, d, l): nb_l(d, z) = beta_l(d,z) sum_t gamma_t(d) theta_t(d)_z V_lt / lhat_{t,d}(l)
+template <int KM>
+__global__ void __launch_bounds__(BK_THREADS) beta_kernel(int F, int T, int N, int K, const float *V, const float *beta,
+                                                          const float *theta, const float *gamma, float *nb) {
+    const int m = blockIdx.z, d = blockIdx.y, l = blockIdx.x * BK_THREADS + threadIdx.x;
+    const bool lv = l < F;
+    const float *bg = beta + ((size_t)m * N + d) * K * F;
+    float bz[KM];
+    double acc[KM];
+#pragma unroll
+    for (int z = 0; z < KM; ++z) {
+        bz[z] = (lv && z < K) ? bg[z * F + l] : 0.f;
+        acc[z] = 0.0;
+    }
+    for (int t = 0; t < T; ++t) {
+        const float v = lv ? V[((size_t)m * T + t) * F + l] : 0.f;
+        if (v > 0.f) {
+            const float *th = theta + (((size_t)m * T + t) * N + d) * K;
+            float lh = 0.f;
+#pragma unroll
+            for (int z = 0; z < KM; ++z)
+                if (z < K) lh = fmaf(th[z], bz[z], lh);
+            if (lh > 0.f) {
+                const float g = gamma[((size_t)m * T + t) * N + d] * __fdiv_rn(v, lh);
+#pragma unroll
+                for (int z = 0; z < KM; ++z)
+                    if (z < K) acc[z] += (double)(g * th[z]);
+            }
+        }
+    }
+    if (lv)
+#pragma unroll
+        for (int z = 0; z < KM; ++z)
+            if (z < K) nb[(((size_t)m * N + d) * K + z) * F + l] = (float)(acc[z] * (double)bz[z]);
+}
+
+// warp per (source, d, z): beta <- nb / sum_l nb (kept when the sum is 0: the element saw no data)
+__global__ void beta_norm_kernel(int F, int rows, const float *nb, float *beta) {
+    const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float *r = nb + (size_t)w * F;
+    double s = 0.0;
+    for (int l = lane; l < F; l += 32) s += r[l];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (s > 0.0)
+        for (int l = lane; l < F; l += 32) beta[(size_t)w * F + l] = (float)((double)r[l] / s);
+}
+
+// theta_t(d) <- theta .* C / sum (thread per (source, t, d)); rho rows from xi, pi = gamma_0 (threads of
+// the first blocks)
+__global__ void mstep_kernel(int T, int N, int K, int M, float *theta, const float *C, const float *xi, float *A,
+                             float *prior, const float *gamma) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < M * T * N) {
+        float *th = theta + (size_t)idx * K;
+        const float *c = C + (size_t)idx * K;
+        double s = 0.0;
+        for (int z = 0; z < K; ++z) s += (double)th[z] * (double)c[z];
+        if (s > 0.0)
+            for (int z = 0; z < K; ++z) th[z] = (float)((double)th[z] * (double)c[z] / s);
+    }
+    if (idx < M * N) {   // rho row i of source m; rows and pi floored at 1e-30 and renormalised (DESIGN R21)
+        const int m = idx / N, i = idx - m * N;
+        const float *x = xi + (size_t)m * N * N + (size_t)i * N;
+        float *a = A + (size_t)m * N * N + (size_t)i * N;
+        double s = 0.0;
+        for (int j = 0; j < N; ++j) s += x[j];
+        if (s > 0.0)
+            for (int j = 0; j < N; ++j) a[j] = (float)((double)x[j] / s);
+        double s2 = 0.0;
+        for (int j = 0; j < N; ++j) s2 += fmax((double)a[j], 1e-30);
+        for (int j = 0; j < N; ++j) a[j] = (float)(fmax((double)a[j], 1e-30) / s2);
+    }
+    if (idx < M) {
+        const float *g = gamma + (size_t)idx * T * N;
+        double s = 0.0;
+        for (int d = 0; d < N; ++d) s += fmax((double)g[d], 1e-30);
+        for (int d = 0; d < N; ++d) prior[(size_t)idx * N + d] = (float)(fmax((double)g[d], 1e-30) / s);
+    }
+}
+
+__global__ void trace_kernel(int M, int iter, int max_iters, const double *logZ, double *trace) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < M) trace[(size_t)m * max_iters + iter] = logZ[m];
+}
+
+__global__ void check_data_kernel(size_t n, const float *V, unsigned *flags) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        if (!(V[i] >= 0.f) || !(V[i] < INFINITY)) atomicOr(flags, FLAG_BAD_INPUT);
+}
+
+template <int KM>
+cudaError_t launch_estep(int F, int T, int N, int K, int M, const float *V, const float *beta, const float *theta,
+                         double *LL, float *C, cudaStream_t st) {
+    const size_t smem = (size_t)K * F * 4;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && attr < smem) {
+        cudaError_t e = cudaFuncSetAttribute(estep_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    estep_kernel<KM><<<dim3((T + ES_FT - 1) / ES_FT, N, M), 256, smem, st>>>(F, T, N, K, V, beta, theta, LL, C);
+    return cudaGetLastError();
+}
+
+template <int KM>
+cudaError_t launch_beta(int F, int T, int N, int K, int M, const float *V, const float *beta, const float *theta,
+                        const float *gamma, float *nb, cudaStream_t st) {
+    beta_kernel<KM><<<dim3((F + BK_THREADS - 1) / BK_THREADS, N, M), BK_THREADS, 0, st>>>(F, T, N, K, V, beta, theta, gamma, nb);
+    return cudaGetLastError();
+}
+
+}  // namespace
+}  // namespace nfk
+
+using namespace nfk;
+
+struct nhmm_train {
+    int64_t F = 0, T = 0, M = 0;
+    int N = 0, K = 0, max_iters = 0, device = 0, iters = 0;
+    cudaStream_t st = nullptr;
+    void *mem = nullptr;
+    float *V = nullptr, *beta = nullptr, *nb = nullptr, *theta = nullptr, *A = nullptr, *prior = nullptr;
+    float *C = nullptr, *ec = nullptr, *fwd = nullptr, *bwd = nullptr, *gamma = nullptr, *Zt = nullptr, *xi = nullptr;
+    double *LL = nullptr, *eoff = nullptr, *logZ = nullptr, *trace = nullptr;
+    unsigned *flags = nullptr;
+    bool have_data = false, have_params = false;
+    int64_t launches = 0;
+    std::string err;
+};
+
+namespace {
+
+int tfail(nhmm_train_t *h, int code, const char *fmt, ...) {
+    if (h) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        h->err = buf;
+    }
+    return code;
+}
+
+#define TCU(h, call)                                                                                 \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess) return tfail(h, NFHMM_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+int kmax_of(int K) { return K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32; }
+
+int t_flags(nhmm_train_t *h) {
+    unsigned f = 0;
+    TCU(h, cudaMemcpyAsync(&f, h->flags, sizeof f, cudaMemcpyDeviceToHost, h->st));
+    TCU(h, cudaStreamSynchronize(h->st));
+    if (f & FLAG_BAD_INPUT) return tfail(h, NFHMM_EINVAL, "training data contain negative or non-finite values");
+    if (f & FLAG_ZERO_SUPPORT) return tfail(h, NFHMM_EZEROSUPPORT, "a frame no state can explain (V > 0 where every lhat = 0)");
+    if (f & FLAG_NONFINITE) return tfail(h, NFHMM_ENUMERIC, "non-finite log evidence");
+    return NFHMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nhmm_train_create(int64_t F, int64_t T, int32_t N, int32_t K, int64_t n_src, int32_t max_iters, int32_t device,
+                      void *stream, nhmm_train_t **out) {
+    if (!out) return NFHMM_EINVAL;
+    *out = nullptr;
+    if (F < 1 || T < 1 || N < 1 || N > 128 || K < 1 || K > 32 || n_src < 1 || max_iters < 1 || (int64_t)K * F > 51200 ||
+        n_src * T > (int64_t)1 << 28)
+        return NFHMM_EINVAL;
+    nhmm_train_t *h = new (std::nothrow) nhmm_train;
+    if (!h) return NFHMM_ENOMEM;
+    h->F = F;
+    h->T = T;
+    h->M = n_src;
+    h->N = N;
+    h->K = K;
+    h->max_iters = max_iters;
+    h->device = device;
+    h->st = (cudaStream_t)stream;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete h;
+        return NFHMM_ECUDA;
+    }
+    const size_t MT = (size_t)n_src * T, MN = (size_t)n_src * N;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) & ~size_t(255);
+        return o;
+    };
+    const size_t oV = take(MT * F * 4), oB = take(MN * K * F * 4), oNB = take(MN * K * F * 4), oTh = take(MT * N * K * 4),
+                 oA = take(MN * N * 4), oP = take(MN * 4), oC = take(MT * N * K * 4), oE = take(MT * N * 4),
+                 oF = take(MT * N * 4), oBw = take(MT * N * 4), oG = take(MT * N * 4), oZ = take(MT * 4),
+                 oX = take(MN * N * 4), oLL = take(MT * N * 8), oEo = take(MT * 8), oLZ = take(n_src * 8),
+                 oTr = take((size_t)n_src * max_iters * 8), oFl = take(256);
+    if (cudaMalloc(&h->mem, off) != cudaSuccess) {
+        delete h;
+        return NFHMM_ENOMEM;
+    }
+    char *b = (char *)h->mem;
+    h->V = (float *)(b + oV);
+    h->beta = (float *)(b + oB);
+    h->nb = (float *)(b + oNB);
+    h->theta = (float *)(b + oTh);
+    h->A = (float *)(b + oA);
+    h->prior = (float *)(b + oP);
+    h->C = (float *)(b + oC);
+    h->ec = (float *)(b + oE);
+    h->fwd = (float *)(b + oF);
+    h->bwd = (float *)(b + oBw);
+    h->gamma = (float *)(b + oG);
+    h->Zt = (float *)(b + oZ);
+    h->xi = (float *)(b + oX);
+    h->LL = (double *)(b + oLL);
+    h->eoff = (double *)(b + oEo);
+    h->logZ = (double *)(b + oLZ);
+    h->trace = (double *)(b + oTr);
+    h->flags = (unsigned *)(b + oFl);
+    if (cudaMemsetAsync(h->flags, 0, 256, h->st) != cudaSuccess) {
+        cudaFree(h->mem);
+        delete h;
+        return NFHMM_ECUDA;
+    }
+    *out = h;
+    return NFHMM_OK;
+}
+
+int nhmm_train_set_data(nhmm_train_t *h, const float *V) {
+    if (!h) return NFHMM_EINVAL;
+    h->err.clear();
+    if (!V) return tfail(h, NFHMM_EINVAL, "NULL data");
+    TCU(h, cudaSetDevice(h->device));
+    const size_t n = (size_t)h->M * h->T * h->F;
+    TCU(h, cudaMemcpyAsync(h->V, V, n * 4, cudaMemcpyDefault, h->st));
+    TCU(h, cudaMemsetAsync(h->flags, 0, sizeof(unsigned), h->st));
+    check_data_kernel<<<256, 256, 0, h->st>>>(n, h->V, h->flags);
+    TCU(h, cudaGetLastError());
+    h->launches++;
+    int r = t_flags(h);
+    if (r) return r;
+    h->have_data = true;
+    return NFHMM_OK;
+}
+
+int nhmm_train_set_params(nhmm_train_t *h, const float *dict, const float *trans, const float *prior, const float *weights) {
+    if (!h) return NFHMM_EINVAL;
+    h->err.clear();
+    if (!dict || !trans || !prior) return tfail(h, NFHMM_EINVAL, "dict, trans and prior are required");
+    TCU(h, cudaSetDevice(h->device));
+    const size_t MN = (size_t)h->M * h->N, MTN = (size_t)h->M * h->T * h->N;
+    TCU(h, cudaMemcpyAsync(h->beta, dict, MN * h->K * h->F * 4, cudaMemcpyDefault, h->st));
+    TCU(h, cudaMemcpyAsync(h->A, trans, MN * h->N * 4, cudaMemcpyDefault, h->st));
+    TCU(h, cudaMemcpyAsync(h->prior, prior, MN * 4, cudaMemcpyDefault, h->st));
+    if (weights) {
+        TCU(h, cudaMemcpyAsync(h->theta, weights, MTN * h->K * 4, cudaMemcpyDefault, h->st));
+    } else {   // uniform weights 1/K
+        float *tmp = new (std::nothrow) float[MTN * h->K];
+        if (!tmp) return tfail(h, NFHMM_ENOMEM, "host buffer");
+        for (size_t i = 0; i < MTN * h->K; ++i) tmp[i] = 1.f / (float)h->K;
+        cudaError_t e = cudaMemcpy(h->theta, tmp, MTN * h->K * 4, cudaMemcpyHostToDevice);
+        delete[] tmp;
+        TCU(h, e);
+    }
+    TCU(h, cudaStreamSynchronize(h->st));
+    h->have_params = true;
+    h->iters = 0;
+    return NFHMM_OK;
+}
+
+int nhmm_train_em(nhmm_train_t *h, int32_t n_iters) {
+    if (!h) return NFHMM_EINVAL;
+    h->err.clear();
+    if (!h->have_data || !h->have_params) return tfail(h, NFHMM_ESTATE, "set_data and set_params must precede em");
+    if (n_iters < 0 || h->iters + n_iters > h->max_iters) return tfail(h, NFHMM_EINVAL, "n_iters beyond max_iters");
+    TCU(h, cudaSetDevice(h->device));
+    const int F = (int)h->F, T = (int)h->T, N = h->N, K = h->K, M = (int)h->M, MT = M * T;
+    const int km = kmax_of(K);
+    for (int it = 0; it < n_iters; ++it) {
+        cudaError_t e;
+        switch (km) {
+            case 4: e = launch_estep<4>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
+            case 8: e = launch_estep<8>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
+            case 16: e = launch_estep<16>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
+            default: e = launch_estep<32>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
+        }
+        TCU(h, e);
+        emission_kernel<<<(MT + 7) / 8, 256, 0, h->st>>>(T, N, MT, h->LL, h->ec, h->eoff, h->flags);
+        TCU(h, cudaGetLastError());
+        FBArgs f{};   // each source is its own chain: M = 1 mixture, S = n_src sources
+        f.M = 1;
+        f.S = M;
+        f.T = T;
+        f.N = N;
+        f.ec = h->ec;
+        f.eoff = h->eoff;
+        f.trans = h->A;
+        f.prior = h->prior;
+        f.fwd = h->fwd;
+        f.bwd = h->bwd;
+        f.logZ = h->logZ;
+        f.flags = h->flags;
+        f.wide = 1;
+        TCU(h, launch_fb(f, h->st));
+        trace_kernel<<<(M + 127) / 128, 128, 0, h->st>>>(M, h->iters, h->max_iters, h->logZ, h->trace);
+        posterior_kernel<<<(MT + 7) / 8, 256, 0, h->st>>>(T, N, MT, h->fwd, h->bwd, h->ec, h->A, h->gamma, h->Zt);
+        xi_kernel<<<(M * N * N + 255) / 256, 256, 0, h->st>>>(T, N, M, h->fwd, h->bwd, h->ec, h->Zt, h->A, h->xi);
+        switch (km) {
+            case 4: e = launch_beta<4>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            case 8: e = launch_beta<8>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            case 16: e = launch_beta<16>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            default: e = launch_beta<32>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+        }
+        TCU(h, e);
+        beta_norm_kernel<<<(M * N * K + 7) / 8, 256, 0, h->st>>>(F, M * N * K, h->nb, h->beta);
+        mstep_kernel<<<(MT * N + 255) / 256, 256, 0, h->st>>>(T, N, K, M, h->theta, h->C, h->xi, h->A, h->prior, h->gamma);
+        TCU(h, cudaGetLastError());
+        h->launches += 10;
+        h->iters++;
+    }
+    return t_flags(h);
+}
+
+int nhmm_train_get(nhmm_train_t *h, float *dict, float *trans, float *prior, float *weights, double *loglik,
+                   int32_t *iters_done) {
+    if (!h) return NFHMM_EINVAL;
+    h->err.clear();
+    TCU(h, cudaSetDevice(h->device));
+    const size_t MN = (size_t)h->M * h->N, MTN = (size_t)h->M * h->T * h->N;
+    if (dict) TCU(h, cudaMemcpyAsync(dict, h->beta, MN * h->K * h->F * 4, cudaMemcpyDefault, h->st));
+    if (trans) TCU(h, cudaMemcpyAsync(trans, h->A, MN * h->N * 4, cudaMemcpyDefault, h->st));
+    if (prior) TCU(h, cudaMemcpyAsync(prior, h->prior, MN * 4, cudaMemcpyDefault, h->st));
+    if (weights) TCU(h, cudaMemcpyAsync(weights, h->theta, MTN * h->K * 4, cudaMemcpyDefault, h->st));
+    if (loglik) TCU(h, cudaMemcpyAsync(loglik, h->trace, (size_t)h->M * h->max_iters * 8, cudaMemcpyDefault, h->st));
+    TCU(h, cudaStreamSynchronize(h->st));
+    if (iters_done) *iters_done = h->iters;
+    return NFHMM_OK;
+}
+
+int nhmm_train_kernel_launches(const nhmm_train_t *h, int64_t *n) {
+    if (!h || !n) return NFHMM_EINVAL;
+    *n = h->launches;
+    return NFHMM_OK;
+}
+
+int nhmm_train_destroy(nhmm_train_t *h) {
+    if (!h) return NFHMM_OK;
+    cudaSetDevice(h->device);
+    if (h->mem) cudaFree(h->mem);
+    delete h;
+    return NFHMM_OK;
+}
+
+const char *nhmm_train_last_error(const nhmm_train_t *h) { return h ? h->err.c_str() : ""; }
+
+}  // extern "C"

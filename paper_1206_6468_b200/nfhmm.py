@@ -62,6 +62,15 @@ SIGNATURES = {
     "nfhmm_bench_kernel": (ctypes.c_int, [_P, ctypes.c_int, _I32, ctypes.POINTER(_D)]),
     "nfhmm_layout": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32),
                                     ctypes.POINTER(_I32)]),
+    # N-HMM EM training
+    "nhmm_train_create": (ctypes.c_int, [_I64, _I64, _I32, _I32, _I64, _I32, _I32, _P, ctypes.POINTER(_P)]),
+    "nhmm_train_set_data": (ctypes.c_int, [_P, _P]),
+    "nhmm_train_set_params": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "nhmm_train_em": (ctypes.c_int, [_P, _I32]),
+    "nhmm_train_get": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, ctypes.POINTER(_I32)]),
+    "nhmm_train_kernel_launches": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+    "nhmm_train_destroy": (ctypes.c_int, [_P]),
+    "nhmm_train_last_error": (ctypes.c_char_p, [_P]),
 }
 
 
@@ -311,3 +320,67 @@ class NFHMM:
         vs = np.empty((M, S, T, F), np.float32) if V_src else None
         nfhmm_separate(self.h, vst, vs)
         return (vst, vs) if V_src else vst
+
+
+# ---- N-HMM EM training (include/nfhmm.h nhmm_train_*) --------------------------------
+
+def _tcheck(h, status):
+    if status != NFHMM_OK:
+        msg = _lib.nhmm_train_last_error(h).decode() if h else ""
+        raise NFHMMError(status, msg or _lib.nfhmm_strerror(status).decode())
+
+
+class NHMMTrainer:
+    """Maximum-likelihood EM for n_src independent single-source N-HMMs (argument marshalling only; the
+    iteration runs in libnfhmm's kernels)."""
+
+    def __init__(self, F, T, N, K, n_src=1, max_iters=256, device=0, stream=None):
+        import torch
+        self.F, self.T, self.N, self.K, self.n_src, self.max_iters = F, T, N, K, n_src, max_iters
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        h = ctypes.c_void_p()
+        st = _lib.nhmm_train_create(F, T, N, K, n_src, max_iters, device, stream, ctypes.byref(h))
+        if st != NFHMM_OK:
+            raise NFHMMError(st, _lib.nfhmm_strerror(st).decode())
+        self.h = h
+
+    def set_data(self, V):
+        _tcheck(self.h, _lib.nhmm_train_set_data(self.h, _ptr(V)))
+
+    def set_params(self, dict_, trans, prior, weights=None):
+        _tcheck(self.h, _lib.nhmm_train_set_params(self.h, _ptr(dict_), _ptr(trans), _ptr(prior), _ptr(weights)))
+
+    def em(self, n_iters):
+        _tcheck(self.h, _lib.nhmm_train_em(self.h, n_iters))
+
+    def get(self):
+        """Host numpy arrays: dict [n_src][N][K][F], trans [n_src][N][N], prior [n_src][N],
+        weights [n_src][T][N][K], loglik [n_src][iters_done] (FP64)."""
+        S, T, N, K, F = self.n_src, self.T, self.N, self.K, self.F
+        d = np.empty((S, N, K, F), np.float32)
+        tr = np.empty((S, N, N), np.float32)
+        pr = np.empty((S, N), np.float32)
+        w = np.empty((S, T, N, K), np.float32)
+        ll = np.empty((S, self.max_iters), np.float64)
+        it = ctypes.c_int32()
+        _tcheck(self.h, _lib.nhmm_train_get(self.h, _ptr(d), _ptr(tr), _ptr(pr), _ptr(w), _ptr(ll), ctypes.byref(it)))
+        return dict(dict=d, trans=tr, prior=pr, weights=w, loglik=ll[:, :it.value])
+
+    def kernel_launches(self):
+        n = ctypes.c_int64()
+        _tcheck(self.h, _lib.nhmm_train_kernel_launches(self.h, ctypes.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.nhmm_train_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -137,3 +137,34 @@ def make_batch(cfg: Config, model: Model, seed: int, mixtures, workers: int | No
     with ProcessPoolExecutor(max_workers=workers) as ex:
         out = list(ex.map(_mix_worker, [(cfg, model, seed, m) for m in mixtures], chunksize=1))
     return np.stack(out)
+
+
+# ---- N-HMM EM training inputs (SURVEY NEXT-3) ------------------------------------------------------
+# Isolated-source training spectrograms: source s of config c's model sampled ALONE through the same
+# generative process (steps 1-7 above with S = 1, key (seed_c, 0xE0000000 + s)), i.e. the "training data
+# of each speaker" the separation models are learned from (P:219).  EM start (the paper does not state
+# one; S:168): dictionaries ~ Dirichlet(1) over F, transition rows Dirichlet(1) + 1 on the diagonal
+# (near-uniform with a small boost), uniform pi, uniform weights (passed as NULL).
+
+def make_training_data(cfg: Config, model: Model, seed: int, T: int | None = None) -> np.ndarray:
+    """[S][T][F] float32: one isolated-source spectrogram per source of cfg's model."""
+    T = T or cfg.T
+    out = []
+    for s in range(cfg.S):
+        c1 = dataclasses.replace(cfg, S=1, T=T)
+        m1 = Model(model.beta[s:s + 1], model.trans[s:s + 1], model.prior[s:s + 1])
+        out.append(make_mixture(c1, m1, seed, 0xE0000000 + s).V)
+    return np.stack(out).astype(np.float32)
+
+
+def make_em_init(cfg: Config, seed: int):
+    """(dict [S][N][K][F], trans [S][N][N], prior [S][N]) float32 starting point for EM."""
+    rng = np.random.default_rng([seed, 0xE1000000])
+    S, N, K, F = cfg.S, cfg.N, cfg.K, cfg.F
+    beta = rng.dirichlet(np.ones(F), size=(S, N, K))
+    beta = np.maximum(beta, 1e-30)
+    beta /= beta.sum(-1, keepdims=True)
+    trans = rng.dirichlet(np.ones(N), size=(S, N)) + np.eye(N)[None]
+    trans /= trans.sum(-1, keepdims=True)
+    prior = np.full((S, N), 1.0 / N)
+    return beta.astype(np.float32), trans.astype(np.float32), prior.astype(np.float32)

@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "nfhmm.h")
 def header_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(nfhmm_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b((?:nfhmm|nhmm_train)_\w+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
