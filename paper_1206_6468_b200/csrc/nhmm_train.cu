@@ -8,8 +8,10 @@
 //   M-step  theta_t(d)_z ∝ theta_t(d)_z C_{t,d,z},  C_{t,d,z} = sum_l beta_l(d,z) V_lt / lhat_{t,d}(l);
 //           beta_l(d,z)  ∝ beta_l(d,z) sum_t gamma_t(d) theta_t(d)_z V_lt / lhat_{t,d}(l);
 //           rho(i -> j)  ∝ sum_{t>=1} xi_t(i,j),  xi_t(i,j) = u_{t-1}(i) A_ij e_t(j) b_t(j) / Z_t;  pi = gamma_0;
-//           rho rows and pi floored at 1e-30 and renormalised (DESIGN R21: keeps every path feasible when
-//           the emission ratios of a 1e5-count frame underflow).
+//           rho rows and pi floored at 1e-15 and renormalised (DESIGN R21: keeps every path feasible when
+//           the emission ratios of a 1e5-count frame underflow; large enough that two floored steps in a
+//           row stay normal in the FP32 recursion); states / rows with posterior mass below 1e-8 T keep
+//           their dictionary / row (DESIGN R22).
 // Kernels, per EM iteration (n_src independent sources batched in every launch):
 //   estep_kernel<KM>     CTA per (source, state d, tile of frames): beta(d) [K][F] staged in shared memory,
 //                        a warp per frame, lanes over l; loglik in FP64 (per-bin terms v log lhat are
@@ -63,13 +65,15 @@ __global__ void __launch_bounds__(256) estep_kernel(int F, int T, int N, int K, 
         for (int l = lane; l < F; l += 32) {
             const float v = vr[l];
             if (v > 0.f) {
-                float lh = 0.f;
+                // lhat in FP64: an FP32 sum (~3e-7 relative) times counts of 1e2-1e3 per bin would move
+                // loglik by ~1e-3 and the emission ratios of the non-dominant states by as much
+                double lh = 0.0;
 #pragma unroll
                 for (int z = 0; z < KM; ++z)
-                    if (z < K) lh = fmaf(tz[z], bs[z * F + l], lh);
-                if (lh > 0.f) {
-                    ll += (double)v * log((double)lh);
-                    const float r = __fdiv_rn(v, lh);
+                    if (z < K) lh = fma((double)tz[z], (double)bs[z * F + l], lh);
+                if (lh > 0.0) {
+                    ll += (double)v * log(lh);
+                    const float r = (float)((double)v / lh);
 #pragma unroll
                     for (int z = 0; z < KM; ++z)
                         if (z < K) cz[z] = fmaf(bs[z * F + l], r, cz[z]);
@@ -116,35 +120,37 @@ __global__ void emission_kernel(int T, int N, int MT, const double *LL, float *e
 
 // one warp per (source, frame): gamma_t = u .* b / sum; for t >= 1, Z_t = sum_i u_{t-1}(i) sum_j A_ij e_t(j) b_t(j)
 __global__ void posterior_kernel(int T, int N, int MT, const float *u, const float *b, const float *ec, const float *A,
-                                 float *gamma, float *Zt) {
+                                 float *gamma, double *Zt) {
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (w >= MT) return;
     const int m = w / T, t = w - m * T;
     const size_t row = (size_t)w * N;
-    float s = 0.f;
-    for (int d = lane; d < N; d += 32) s += u[row + d] * b[row + d];
+    // FP64 products: the messages carry the scale of the PREVIOUS step (fb.cu), so u_t and b_t can each be
+    // ~1e-15 when the chain passes a floored transition and their FP32 product would underflow
+    double s = 0.0;
+    for (int d = lane; d < N; d += 32) s += (double)u[row + d] * (double)b[row + d];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const float is = 1.f / s;
-    for (int d = lane; d < N; d += 32) gamma[row + d] = u[row + d] * b[row + d] * is;
+    const double is = 1.0 / s;
+    for (int d = lane; d < N; d += 32) gamma[row + d] = (float)((double)u[row + d] * (double)b[row + d] * is);
     if (t == 0) {
-        if (lane == 0) Zt[w] = 1.f;
+        if (lane == 0) Zt[w] = 1.0;
         return;
     }
     const float *Am = A + (size_t)m * N * N;
     double z = 0.0;
     for (int i = lane; i < N; i += 32) {
-        float y = 0.f;
-        for (int j = 0; j < N; ++j) y = fmaf(Am[i * N + j], ec[row + j] * b[row + j], y);
-        z += (double)u[row - N + i] * (double)y;
+        double y = 0.0;
+        for (int j = 0; j < N; ++j) y = fma((double)Am[i * N + j], (double)ec[row + j] * (double)b[row + j], y);
+        z += (double)u[row - N + i] * y;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-    if (lane == 0) Zt[w] = (float)z;
+    if (lane == 0) Zt[w] = z;
 }
 
 // thread per (source, i, j): xi_sum = A_ij sum_{t>=1} u_{t-1}(i) e_t(j) b_t(j) / Z_t  (FP64 over t)
-__global__ void xi_kernel(int T, int N, int M, const float *u, const float *b, const float *ec, const float *Zt,
+__global__ void xi_kernel(int T, int N, int M, const float *u, const float *b, const float *ec, const double *Zt,
                           const float *A, float *xi) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= M * N * N) return;
@@ -152,8 +158,8 @@ __global__ void xi_kernel(int T, int N, int M, const float *u, const float *b, c
     const size_t base = (size_t)m * T * N;
     double acc = 0.0;
     for (int t = 1; t < T; ++t)
-        acc += (double)u[base + (size_t)(t - 1) * N + i] * (double)(ec[base + (size_t)t * N + j] * b[base + (size_t)t * N + j]) /
-               (double)Zt[(size_t)m * T + t];
+        acc += (double)u[base + (size_t)(t - 1) * N + i] * ((double)ec[base + (size_t)t * N + j] * (double)b[base + (size_t)t * N + j]) /
+               Zt[(size_t)m * T + t];
     xi[idx] = (float)(acc * (double)A[(size_t)m * N * N + ij]);
 }
 
@@ -175,15 +181,15 @@ __global__ void __launch_bounds__(BK_THREADS) beta_kernel(int F, int T, int N, i
         const float v = lv ? V[((size_t)m * T + t) * F + l] : 0.f;
         if (v > 0.f) {
             const float *th = theta + (((size_t)m * T + t) * N + d) * K;
-            float lh = 0.f;
+            double lh = 0.0;   // as in estep_kernel
 #pragma unroll
             for (int z = 0; z < KM; ++z)
-                if (z < K) lh = fmaf(th[z], bz[z], lh);
-            if (lh > 0.f) {
-                const float g = gamma[((size_t)m * T + t) * N + d] * __fdiv_rn(v, lh);
+                if (z < K) lh = fma((double)th[z], (double)bz[z], lh);
+            if (lh > 0.0) {
+                const double g = (double)gamma[((size_t)m * T + t) * N + d] * ((double)v / lh);
 #pragma unroll
                 for (int z = 0; z < KM; ++z)
-                    if (z < K) acc[z] += (double)(g * th[z]);
+                    if (z < K) acc[z] += g * (double)th[z];
             }
         }
     }
@@ -193,16 +199,23 @@ __global__ void __launch_bounds__(BK_THREADS) beta_kernel(int F, int T, int N, i
             if (z < K) nb[(((size_t)m * N + d) * K + z) * F + l] = (float)(acc[z] * (double)bz[z]);
 }
 
-// warp per (source, d, z): beta <- nb / sum_l nb (kept when the sum is 0: the element saw no data)
-__global__ void beta_norm_kernel(int F, int rows, const float *nb, float *beta) {
+// warp per (source, d, z): beta <- nb / sum_l nb; kept when the element saw no data or the state's
+// posterior mass sum_t gamma_t(d) is below 1e-8 T (DESIGN R22)
+__global__ void beta_norm_kernel(int F, int T, int N, int K, int rows, const float *nb, const float *gamma, float *beta) {
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (w >= rows) return;
+    const int m = w / (N * K), d = (w / K) % N;
+    double mass = 0.0;
+    for (int t = lane; t < T; t += 32) mass += gamma[((size_t)m * T + t) * N + d];
     const float *r = nb + (size_t)w * F;
     double s = 0.0;
     for (int l = lane; l < F; l += 32) s += r[l];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (s > 0.0)
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        mass += __shfl_xor_sync(0xffffffffu, mass, o);
+    }
+    if (s > 0.0 && mass >= 1e-8 * T)
         for (int l = lane; l < F; l += 32) beta[(size_t)w * F + l] = (float)((double)r[l] / s);
 }
 
@@ -219,23 +232,23 @@ __global__ void mstep_kernel(int T, int N, int K, int M, float *theta, const flo
         if (s > 0.0)
             for (int z = 0; z < K; ++z) th[z] = (float)((double)th[z] * (double)c[z] / s);
     }
-    if (idx < M * N) {   // rho row i of source m; rows and pi floored at 1e-30 and renormalised (DESIGN R21)
+    if (idx < M * N) {   // rho row i of source m; rows and pi floored at 1e-15 and renormalised (DESIGN R21)
         const int m = idx / N, i = idx - m * N;
         const float *x = xi + (size_t)m * N * N + (size_t)i * N;
         float *a = A + (size_t)m * N * N + (size_t)i * N;
         double s = 0.0;
         for (int j = 0; j < N; ++j) s += x[j];
-        if (s > 0.0)
+        if (s >= 1e-8 * T)   // s = sum_{t < T-1} gamma_t(i), the row's posterior mass (DESIGN R22)
             for (int j = 0; j < N; ++j) a[j] = (float)((double)x[j] / s);
         double s2 = 0.0;
-        for (int j = 0; j < N; ++j) s2 += fmax((double)a[j], 1e-30);
-        for (int j = 0; j < N; ++j) a[j] = (float)(fmax((double)a[j], 1e-30) / s2);
+        for (int j = 0; j < N; ++j) s2 += fmax((double)a[j], 1e-15);
+        for (int j = 0; j < N; ++j) a[j] = (float)(fmax((double)a[j], 1e-15) / s2);
     }
     if (idx < M) {
         const float *g = gamma + (size_t)idx * T * N;
         double s = 0.0;
-        for (int d = 0; d < N; ++d) s += fmax((double)g[d], 1e-30);
-        for (int d = 0; d < N; ++d) prior[(size_t)idx * N + d] = (float)(fmax((double)g[d], 1e-30) / s);
+        for (int d = 0; d < N; ++d) s += fmax((double)g[d], 1e-15);
+        for (int d = 0; d < N; ++d) prior[(size_t)idx * N + d] = (float)(fmax((double)g[d], 1e-15) / s);
     }
 }
 
@@ -282,8 +295,8 @@ struct nhmm_train {
     cudaStream_t st = nullptr;
     void *mem = nullptr;
     float *V = nullptr, *beta = nullptr, *nb = nullptr, *theta = nullptr, *A = nullptr, *prior = nullptr;
-    float *C = nullptr, *ec = nullptr, *fwd = nullptr, *bwd = nullptr, *gamma = nullptr, *Zt = nullptr, *xi = nullptr;
-    double *LL = nullptr, *eoff = nullptr, *logZ = nullptr, *trace = nullptr;
+    float *C = nullptr, *ec = nullptr, *fwd = nullptr, *bwd = nullptr, *gamma = nullptr, *xi = nullptr;
+    double *Zt = nullptr, *LL = nullptr, *eoff = nullptr, *logZ = nullptr, *trace = nullptr;
     unsigned *flags = nullptr;
     bool have_data = false, have_params = false;
     int64_t launches = 0;
@@ -356,7 +369,7 @@ int nhmm_train_create(int64_t F, int64_t T, int32_t N, int32_t K, int64_t n_src,
     };
     const size_t oV = take(MT * F * 4), oB = take(MN * K * F * 4), oNB = take(MN * K * F * 4), oTh = take(MT * N * K * 4),
                  oA = take(MN * N * 4), oP = take(MN * 4), oC = take(MT * N * K * 4), oE = take(MT * N * 4),
-                 oF = take(MT * N * 4), oBw = take(MT * N * 4), oG = take(MT * N * 4), oZ = take(MT * 4),
+                 oF = take(MT * N * 4), oBw = take(MT * N * 4), oG = take(MT * N * 4), oZ = take(MT * 8),
                  oX = take(MN * N * 4), oLL = take(MT * N * 8), oEo = take(MT * 8), oLZ = take(n_src * 8),
                  oTr = take((size_t)n_src * max_iters * 8), oFl = take(256);
     if (cudaMalloc(&h->mem, off) != cudaSuccess) {
@@ -375,7 +388,7 @@ int nhmm_train_create(int64_t F, int64_t T, int32_t N, int32_t K, int64_t n_src,
     h->fwd = (float *)(b + oF);
     h->bwd = (float *)(b + oBw);
     h->gamma = (float *)(b + oG);
-    h->Zt = (float *)(b + oZ);
+    h->Zt = (double *)(b + oZ);
     h->xi = (float *)(b + oX);
     h->LL = (double *)(b + oLL);
     h->eoff = (double *)(b + oEo);
@@ -477,7 +490,7 @@ int nhmm_train_em(nhmm_train_t *h, int32_t n_iters) {
             default: e = launch_beta<32>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
         }
         TCU(h, e);
-        beta_norm_kernel<<<(M * N * K + 7) / 8, 256, 0, h->st>>>(F, M * N * K, h->nb, h->beta);
+        beta_norm_kernel<<<(M * N * K + 7) / 8, 256, 0, h->st>>>(F, T, N, K, M * N * K, h->nb, h->gamma, h->beta);
         mstep_kernel<<<(MT * N + 255) / 256, 256, 0, h->st>>>(T, N, K, M, h->theta, h->C, h->xi, h->A, h->prior, h->gamma);
         TCU(h, cudaGetLastError());
         h->launches += 10;
