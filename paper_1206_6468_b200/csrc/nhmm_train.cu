@@ -53,10 +53,11 @@ __global__ void __launch_bounds__(256) estep_kernel(int F, int T, int N, int K, 
     __syncthreads();
     for (int t = t0 + warp; t < min(T, t0 + ES_FT); t += 8) {
         const float *th = theta + (((size_t)m * T + t) * N + d) * K;
-        float tz[KM], cz[KM];
+        double tz[KM];
+        float cz[KM];
 #pragma unroll
         for (int z = 0; z < KM; ++z) {
-            tz[z] = z < K ? th[z] : 0.f;
+            tz[z] = z < K ? (double)th[z] : 0.0;
             cz[z] = 0.f;
         }
         const float *vr = V + ((size_t)m * T + t) * F;
@@ -70,10 +71,10 @@ __global__ void __launch_bounds__(256) estep_kernel(int F, int T, int N, int K, 
                 double lh = 0.0;
 #pragma unroll
                 for (int z = 0; z < KM; ++z)
-                    if (z < K) lh = fma((double)tz[z], (double)bs[z * F + l], lh);
+                    if (z < K) lh = fma(tz[z], (double)bs[z * F + l], lh);
                 if (lh > 0.0) {
                     ll += (double)v * log(lh);
-                    const float r = (float)((double)v / lh);
+                    const float r = __fdiv_rn(v, (float)lh);   // a weight: FP32 suffices
 #pragma unroll
                     for (int z = 0; z < KM; ++z)
                         if (z < K) cz[z] = fmaf(bs[z * F + l], r, cz[z]);
@@ -118,7 +119,8 @@ __global__ void emission_kernel(int T, int N, int MT, const double *LL, float *e
     if (lane == 0) eoff[w] = mx;
 }
 
-// one warp per (source, frame): gamma_t = u .* b / sum; for t >= 1, Z_t = sum_i u_{t-1}(i) sum_j A_ij e_t(j) b_t(j)
+// one warp per (source, frame): gamma_t = u .* b / sum; for t >= 1, 1 / Z_t with
+// Z_t = sum_i u_{t-1}(i) sum_j A_ij e_t(j) b_t(j) (the pairwise normaliser; reciprocal once per frame)
 __global__ void posterior_kernel(int T, int N, int MT, const float *u, const float *b, const float *ec, const float *A,
                                  float *gamma, double *Zt) {
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -134,7 +136,7 @@ __global__ void posterior_kernel(int T, int N, int MT, const float *u, const flo
     const double is = 1.0 / s;
     for (int d = lane; d < N; d += 32) gamma[row + d] = (float)((double)u[row + d] * (double)b[row + d] * is);
     if (t == 0) {
-        if (lane == 0) Zt[w] = 1.0;
+        if (lane == 0) Zt[w] = 0.0;
         return;
     }
     const float *Am = A + (size_t)m * N * N;
@@ -146,83 +148,108 @@ __global__ void posterior_kernel(int T, int N, int MT, const float *u, const flo
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-    if (lane == 0) Zt[w] = z;
+    if (lane == 0) Zt[w] = 1.0 / z;
 }
 
-// thread per (source, i, j): xi_sum = A_ij sum_{t>=1} u_{t-1}(i) e_t(j) b_t(j) / Z_t  (FP64 over t)
-__global__ void xi_kernel(int T, int N, int M, const float *u, const float *b, const float *ec, const double *Zt,
-                          const float *A, float *xi) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+// thread per (source, i, j) and chunk of frames: partial xi sums A_ij sum_{t in chunk, t>=1}
+// u_{t-1}(i) e_t(j) b_t(j) / Z_t (FP64); mstep_kernel adds the chunks in a fixed order
+__global__ void xi_kernel(int T, int N, int M, int tchunk, const float *u, const float *b, const float *ec,
+                          const double *invZ, const float *A, float *xi_part) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
     if (idx >= M * N * N) return;
     const int m = idx / (N * N), ij = idx - m * N * N, i = ij / N, j = ij - i * N;
     const size_t base = (size_t)m * T * N;
     double acc = 0.0;
-    for (int t = 1; t < T; ++t)
-        acc += (double)u[base + (size_t)(t - 1) * N + i] * ((double)ec[base + (size_t)t * N + j] * (double)b[base + (size_t)t * N + j]) /
-               Zt[(size_t)m * T + t];
-    xi[idx] = (float)(acc * (double)A[(size_t)m * N * N + ij]);
+    for (int t = max(1, c * tchunk); t < min(T, (c + 1) * tchunk); ++t)
+        acc += (double)u[base + (size_t)(t - 1) * N + i] * ((double)ec[base + (size_t)t * N + j] * (double)b[base + (size_t)t * N + j]) *
+               invZ[(size_t)m * T + t];
+    xi_part[(size_t)c * M * N * N + idx] = (float)(acc * (double)A[(size_t)m * N * N + ij]);
 }
 
-// thread per (source, d, l): nb_l(d, z) = beta_l(d,z) sum_t gamma_t(d) theta_t(d)_z V_lt / lhat_{t,d}(l)
+// thread per (source, d, l) and chunk of frames: partial nb_l(d, z) = beta_l(d,z) sum_{t in chunk}
+// gamma_t(d) theta_t(d)_z V_lt / lhat_{t,d}(l), compensated FP32 accumulation; beta_norm_kernel adds the chunks
 template <int KM>
-__global__ void __launch_bounds__(BK_THREADS) beta_kernel(int F, int T, int N, int K, const float *V, const float *beta,
-                                                          const float *theta, const float *gamma, float *nb) {
-    const int m = blockIdx.z, d = blockIdx.y, l = blockIdx.x * BK_THREADS + threadIdx.x;
+__global__ void __launch_bounds__(BK_THREADS) beta_kernel(int F, int T, int N, int K, int tchunk, const float *V,
+                                                          const float *beta, const float *theta, const float *gamma,
+                                                          float *nb_part) {
+    const int M = gridDim.z / ((T + tchunk - 1) / tchunk);
+    const int c = blockIdx.z / M, m = blockIdx.z - c * M, d = blockIdx.y, l = blockIdx.x * BK_THREADS + threadIdx.x;
     const bool lv = l < F;
     const float *bg = beta + ((size_t)m * N + d) * K * F;
-    float bz[KM];
-    double acc[KM];
+    float bz[KM], acc[KM], cmp[KM];   // compensated (Kahan) FP32 sums over the chunk's frames
 #pragma unroll
     for (int z = 0; z < KM; ++z) {
         bz[z] = (lv && z < K) ? bg[z * F + l] : 0.f;
-        acc[z] = 0.0;
+        acc[z] = 0.f;
+        cmp[z] = 0.f;
     }
-    for (int t = 0; t < T; ++t) {
+    const int t1 = min(T, (c + 1) * tchunk);
+    for (int t = c * tchunk; t < t1; ++t) {
         const float v = lv ? V[((size_t)m * T + t) * F + l] : 0.f;
         if (v > 0.f) {
             const float *th = theta + (((size_t)m * T + t) * N + d) * K;
-            double lh = 0.0;   // as in estep_kernel
+            float tz[KM];
+            float lh = 0.f;   // the weights need FP32 only (the log-likelihood's lhat is FP64, estep_kernel)
 #pragma unroll
-            for (int z = 0; z < KM; ++z)
-                if (z < K) lh = fma((double)th[z], (double)bz[z], lh);
-            if (lh > 0.0) {
-                const double g = (double)gamma[((size_t)m * T + t) * N + d] * ((double)v / lh);
+            for (int z = 0; z < KM; ++z) {
+                tz[z] = z < K ? th[z] : 0.f;
+                lh = fmaf(tz[z], bz[z], lh);
+            }
+            if (lh > 0.f) {
+                const float g = gamma[((size_t)m * T + t) * N + d] * __fdiv_rn(v, lh);
 #pragma unroll
                 for (int z = 0; z < KM; ++z)
-                    if (z < K) acc[z] += g * (double)th[z];
+                    if (z < K) {
+                        const float y = __fsub_rn(g * tz[z], cmp[z]);
+                        const float t2 = __fadd_rn(acc[z], y);
+                        cmp[z] = __fsub_rn(__fsub_rn(t2, acc[z]), y);
+                        acc[z] = t2;
+                    }
             }
         }
     }
-    if (lv)
+    if (lv) {
+        float *dst = nb_part + (size_t)c * gridDim.y * M * K * F;   // [chunk][M][N][K][F]
 #pragma unroll
         for (int z = 0; z < KM; ++z)
-            if (z < K) nb[(((size_t)m * N + d) * K + z) * F + l] = (float)(acc[z] * (double)bz[z]);
+            if (z < K) dst[(((size_t)m * N + d) * K + z) * F + l] = (float)(((double)acc[z] - (double)cmp[z]) * (double)bz[z]);
+    }
 }
 
-// warp per (source, d, z): beta <- nb / sum_l nb; kept when the element saw no data or the state's
-// posterior mass sum_t gamma_t(d) is below 1e-8 T (DESIGN R22)
-__global__ void beta_norm_kernel(int F, int T, int N, int K, int rows, const float *nb, const float *gamma, float *beta) {
+// warp per (source, d, z): nb = sum over frame chunks of the partials (fixed order), beta <- nb / sum_l nb;
+// kept when the element saw no data or the state's posterior mass sum_t gamma_t(d) is below 1e-8 T
+// (DESIGN R22)
+__global__ void beta_norm_kernel(int F, int T, int N, int K, int rows, int nchunk, const float *nb_part,
+                                 const float *gamma, float *beta) {
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (w >= rows) return;
     const int m = w / (N * K), d = (w / K) % N;
     double mass = 0.0;
     for (int t = lane; t < T; t += 32) mass += gamma[((size_t)m * T + t) * N + d];
-    const float *r = nb + (size_t)w * F;
+    const size_t stride = (size_t)rows * F;
     double s = 0.0;
-    for (int l = lane; l < F; l += 32) s += r[l];
+    for (int l = lane; l < F; l += 32) {
+        double v = 0.0;
+        for (int c = 0; c < nchunk; ++c) v += nb_part[c * stride + (size_t)w * F + l];
+        s += v;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         s += __shfl_xor_sync(0xffffffffu, s, o);
         mass += __shfl_xor_sync(0xffffffffu, mass, o);
     }
     if (s > 0.0 && mass >= 1e-8 * T)
-        for (int l = lane; l < F; l += 32) beta[(size_t)w * F + l] = (float)((double)r[l] / s);
+        for (int l = lane; l < F; l += 32) {
+            double v = 0.0;
+            for (int c = 0; c < nchunk; ++c) v += nb_part[c * stride + (size_t)w * F + l];
+            beta[(size_t)w * F + l] = (float)(v / s);
+        }
 }
 
 // theta_t(d) <- theta .* C / sum (thread per (source, t, d)); rho rows from xi, pi = gamma_0 (threads of
 // the first blocks)
-__global__ void mstep_kernel(int T, int N, int K, int M, float *theta, const float *C, const float *xi, float *A,
-                             float *prior, const float *gamma) {
+__global__ void mstep_kernel(int T, int N, int K, int M, int nchunk, float *theta, const float *C, const float *xi_part,
+                             float *A, float *prior, const float *gamma) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx < M * T * N) {
         float *th = theta + (size_t)idx * K;
@@ -234,12 +261,17 @@ __global__ void mstep_kernel(int T, int N, int K, int M, float *theta, const flo
     }
     if (idx < M * N) {   // rho row i of source m; rows and pi floored at 1e-15 and renormalised (DESIGN R21)
         const int m = idx / N, i = idx - m * N;
-        const float *x = xi + (size_t)m * N * N + (size_t)i * N;
-        float *a = A + (size_t)m * N * N + (size_t)i * N;
+        const size_t row = (size_t)m * N * N + (size_t)i * N, cs = (size_t)M * N * N;
+        float *a = A + row;
         double s = 0.0;
-        for (int j = 0; j < N; ++j) s += x[j];
+        for (int j = 0; j < N; ++j)
+            for (int c = 0; c < nchunk; ++c) s += xi_part[c * cs + row + j];
         if (s >= 1e-8 * T)   // s = sum_{t < T-1} gamma_t(i), the row's posterior mass (DESIGN R22)
-            for (int j = 0; j < N; ++j) a[j] = (float)((double)x[j] / s);
+            for (int j = 0; j < N; ++j) {
+                double x = 0.0;
+                for (int c = 0; c < nchunk; ++c) x += xi_part[c * cs + row + j];
+                a[j] = (float)(x / s);
+            }
         double s2 = 0.0;
         for (int j = 0; j < N; ++j) s2 += fmax((double)a[j], 1e-15);
         for (int j = 0; j < N; ++j) a[j] = (float)(fmax((double)a[j], 1e-15) / s2);
@@ -266,7 +298,7 @@ template <int KM>
 cudaError_t launch_estep(int F, int T, int N, int K, int M, const float *V, const float *beta, const float *theta,
                          double *LL, float *C, cudaStream_t st) {
     const size_t smem = (size_t)K * F * 4;
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;
     static size_t attr = 0;
     if (smem > 48 * 1024 && attr < smem) {
         cudaError_t e = cudaFuncSetAttribute(estep_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -278,9 +310,11 @@ cudaError_t launch_estep(int F, int T, int N, int K, int M, const float *V, cons
 }
 
 template <int KM>
-cudaError_t launch_beta(int F, int T, int N, int K, int M, const float *V, const float *beta, const float *theta,
-                        const float *gamma, float *nb, cudaStream_t st) {
-    beta_kernel<KM><<<dim3((F + BK_THREADS - 1) / BK_THREADS, N, M), BK_THREADS, 0, st>>>(F, T, N, K, V, beta, theta, gamma, nb);
+cudaError_t launch_beta(int F, int T, int N, int K, int M, int tchunk, const float *V, const float *beta,
+                        const float *theta, const float *gamma, float *nb, cudaStream_t st) {
+    const int nc = (T + tchunk - 1) / tchunk;
+    beta_kernel<KM><<<dim3((F + BK_THREADS - 1) / BK_THREADS, N, M * nc), BK_THREADS, 0, st>>>(F, T, N, K, tchunk, V, beta,
+                                                                                              theta, gamma, nb);
     return cudaGetLastError();
 }
 
@@ -323,7 +357,8 @@ int tfail(nhmm_train_t *h, int code, const char *fmt, ...) {
         if (e_ != cudaSuccess) return tfail(h, NFHMM_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
     } while (0)
 
-int kmax_of(int K) { return K <= 4 ? 4 : K <= 8 ? 8 : K <= 16 ? 16 : 32; }
+int kmax_of(int K) { return K <= 4 ? 4 : K <= 8 ? 8 : K <= 10 ? 10 : K <= 16 ? 16 : K <= 20 ? 20 : 32; }
+constexpr int TCHUNK = 256;   // frames per partial sum of the beta / xi reductions
 
 int t_flags(nhmm_train_t *h) {
     unsigned f = 0;
@@ -360,18 +395,19 @@ int nhmm_train_create(int64_t F, int64_t T, int32_t N, int32_t K, int64_t n_src,
         delete h;
         return NFHMM_ECUDA;
     }
-    const size_t MT = (size_t)n_src * T, MN = (size_t)n_src * N;
+    const size_t MT = (size_t)n_src * T, MN = (size_t)n_src * N, nchunk = (size_t)((T + TCHUNK - 1) / TCHUNK);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
         off += (bytes + 255) & ~size_t(255);
         return o;
     };
-    const size_t oV = take(MT * F * 4), oB = take(MN * K * F * 4), oNB = take(MN * K * F * 4), oTh = take(MT * N * K * 4),
+    const size_t oV = take(MT * F * 4), oB = take(MN * K * F * 4), oNB = take(nchunk * MN * K * F * 4), oTh = take(MT * N * K * 4),
                  oA = take(MN * N * 4), oP = take(MN * 4), oC = take(MT * N * K * 4), oE = take(MT * N * 4),
                  oF = take(MT * N * 4), oBw = take(MT * N * 4), oG = take(MT * N * 4), oZ = take(MT * 8),
-                 oX = take(MN * N * 4), oLL = take(MT * N * 8), oEo = take(MT * 8), oLZ = take(n_src * 8),
+                 oX = take(nchunk * MN * N * 4), oLL = take(MT * N * 8), oEo = take(MT * 8), oLZ = take(n_src * 8),
                  oTr = take((size_t)n_src * max_iters * 8), oFl = take(256);
+
     if (cudaMalloc(&h->mem, off) != cudaSuccess) {
         delete h;
         return NFHMM_ENOMEM;
@@ -395,6 +431,7 @@ int nhmm_train_create(int64_t F, int64_t T, int32_t N, int32_t K, int64_t n_src,
     h->logZ = (double *)(b + oLZ);
     h->trace = (double *)(b + oTr);
     h->flags = (unsigned *)(b + oFl);
+
     if (cudaMemsetAsync(h->flags, 0, 256, h->st) != cudaSuccess) {
         cudaFree(h->mem);
         delete h;
@@ -453,13 +490,15 @@ int nhmm_train_em(nhmm_train_t *h, int32_t n_iters) {
     if (n_iters < 0 || h->iters + n_iters > h->max_iters) return tfail(h, NFHMM_EINVAL, "n_iters beyond max_iters");
     TCU(h, cudaSetDevice(h->device));
     const int F = (int)h->F, T = (int)h->T, N = h->N, K = h->K, M = (int)h->M, MT = M * T;
-    const int km = kmax_of(K);
+    const int km = kmax_of(K), nch = (T + TCHUNK - 1) / TCHUNK;
     for (int it = 0; it < n_iters; ++it) {
         cudaError_t e;
         switch (km) {
             case 4: e = launch_estep<4>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
             case 8: e = launch_estep<8>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
+            case 10: e = launch_estep<10>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
             case 16: e = launch_estep<16>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
+            case 20: e = launch_estep<20>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
             default: e = launch_estep<32>(F, T, N, K, M, h->V, h->beta, h->theta, h->LL, h->C, h->st); break;
         }
         TCU(h, e);
@@ -478,20 +517,25 @@ int nhmm_train_em(nhmm_train_t *h, int32_t n_iters) {
         f.bwd = h->bwd;
         f.logZ = h->logZ;
         f.flags = h->flags;
-        f.wide = 1;
+        f.wide = 1;   // sequential recursion: the chunked (parallel-in-time) variant multiplies emission
+                      // ratios of ~1e-30 along 32-64 steps in FP32 and loses whole rows (measured)
         TCU(h, launch_fb(f, h->st));
         trace_kernel<<<(M + 127) / 128, 128, 0, h->st>>>(M, h->iters, h->max_iters, h->logZ, h->trace);
         posterior_kernel<<<(MT + 7) / 8, 256, 0, h->st>>>(T, N, MT, h->fwd, h->bwd, h->ec, h->A, h->gamma, h->Zt);
-        xi_kernel<<<(M * N * N + 255) / 256, 256, 0, h->st>>>(T, N, M, h->fwd, h->bwd, h->ec, h->Zt, h->A, h->xi);
+        xi_kernel<<<dim3((M * N * N + 255) / 256, nch), 256, 0, h->st>>>(T, N, M, TCHUNK, h->fwd, h->bwd, h->ec, h->Zt, h->A,
+                                                                          h->xi);
         switch (km) {
-            case 4: e = launch_beta<4>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
-            case 8: e = launch_beta<8>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
-            case 16: e = launch_beta<16>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
-            default: e = launch_beta<32>(F, T, N, K, M, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            case 4: e = launch_beta<4>(F, T, N, K, M, TCHUNK, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            case 8: e = launch_beta<8>(F, T, N, K, M, TCHUNK, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            case 10: e = launch_beta<10>(F, T, N, K, M, TCHUNK, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            case 16: e = launch_beta<16>(F, T, N, K, M, TCHUNK, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            case 20: e = launch_beta<20>(F, T, N, K, M, TCHUNK, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
+            default: e = launch_beta<32>(F, T, N, K, M, TCHUNK, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
         }
         TCU(h, e);
-        beta_norm_kernel<<<(M * N * K + 7) / 8, 256, 0, h->st>>>(F, T, N, K, M * N * K, h->nb, h->gamma, h->beta);
-        mstep_kernel<<<(MT * N + 255) / 256, 256, 0, h->st>>>(T, N, K, M, h->theta, h->C, h->xi, h->A, h->prior, h->gamma);
+        beta_norm_kernel<<<(M * N * K + 7) / 8, 256, 0, h->st>>>(F, T, N, K, M * N * K, nch, h->nb, h->gamma, h->beta);
+        mstep_kernel<<<(MT * N + 255) / 256, 256, 0, h->st>>>(T, N, K, M, nch, h->theta, h->C, h->xi, h->A, h->prior,
+                                                              h->gamma);
         TCU(h, cudaGetLastError());
         h->launches += 10;
         h->iters++;
