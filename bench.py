@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-bound-off", action="store_true", help="skip the timing with the free energy off")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU seconds for the oracle sample")
+    ap.add_argument("--workload", choices=["vb", "train"], default="vb",
+                    help="vb: the separation hot path (default); train: N-HMM EM training (SURVEY NEXT-3)")
+    ap.add_argument("--train-T", type=int, default=None, help="frames per training source (default 2000)")
     return ap.parse_args()
 
 
@@ -439,8 +442,86 @@ def run_ours(args):
     return 0
 
 
+# ------------------------------------------------------------------------------------------------
+# --workload train: N-HMM maximum-likelihood EM, one GPU
+# ------------------------------------------------------------------------------------------------
+TRAIN_METRIC = "EM frame-iterations/sec, N-HMM training (isolated sources, N=40,K=10,F=513)"
+
+
+def run_train(args):
+    """Each step: reset to the EM start, `iters` EM iterations over every source of the config (each
+    source's isolated spectrogram, T frames), parameters read back.  value = sources x T x iters / time."""
+    import torch
+    from paper_1206_6468_b200.nfhmm import NHMMTrainer
+    torch.cuda.set_device(0)
+    cfg = synth.config(args.config)
+    T = args.train_T or 2000
+    iters = args.iters or 10
+    seed = synth.seed_of(args.config)
+    model = synth.make_model(cfg, seed)
+    V = synth.make_training_data(cfg, model, seed, T)
+    b0, a0, p0 = synth.make_em_init(cfg, seed)
+    dev = "cuda:0"
+    Vd = torch.from_numpy(V).to(dev)
+    b0d, a0d, p0d = (torch.from_numpy(x).to(dev) for x in (b0, a0, p0))
+    stream = torch.cuda.current_stream()
+    tr = NHMMTrainer(cfg.F, T, cfg.N, cfg.K, n_src=cfg.S, max_iters=iters, stream=stream)
+    tr.set_data(Vd)
+    out = torch.empty((cfg.S, cfg.N, cfg.K, cfg.F), dtype=torch.float32, device=dev)
+
+    def step():
+        tr.set_params(b0d, a0d, p0d)
+        tr.em(iters)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(0)
+    clocks.start()
+    l0 = tr.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = tr.kernel_launches() - l0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    units = cfg.S * T * iters
+    value = units / (ms / 1000.0)
+    ll = tr.get()["loglik"]
+    cpu = None
+    if not args.no_cpu_baseline:   # the oracle on a bounded sample: one source, T_s frames, a few iterations
+        from oracle import oracle
+        oracle.build()
+        T_s = min(T, 100)
+        th = np.full((T_s, cfg.N, cfg.K), 1.0 / cfg.K)
+        t0 = time.perf_counter()
+        oracle.nhmm_em(V[0, :T_s], b0[0], th, a0[0], p0[0], 1)
+        t1 = time.perf_counter() - t0
+        it_s = max(1, min(20, int(args.cpu_seconds / max(t1, 1e-3))))
+        t0 = time.perf_counter()
+        oracle.nhmm_em(V[0, :T_s], b0[0], th, a0[0], p0[0], it_s)
+        wall = time.perf_counter() - t0
+        cpu = {"value": T_s * it_s / wall, "unit": "frame-iterations/s", "cores": 1, "kind": "oracle",
+               "sample": f"1 source x T={T_s} frames x {it_s} EM iterations (N={cfg.N},K={cfg.K},F={cfg.F}); {wall:.1f} s wall"}
+    line = {"metric": TRAIN_METRIC, "value": value, "unit": "frame-iterations/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32 (f64 log-likelihood)", "data": "synthetic",
+            "config": {"workload": f"train-cfg{args.config}", "sources": cfg.S, "N": cfg.N, "K": cfg.K, "F": cfg.F,
+                       "T": T, "iters": iters, "step": "reset to the EM start + iters EM iterations, data resident"},
+            "loglik_first_last": [float(ll[0, 0]), float(ll[0, -1])], "cpu_baseline": cpu, "clocks": clk,
+            "gpu_launches": launches}
+    print(json.dumps(line), flush=True)
+    tr.close()
+    return 0
+
+
 def main():
     args = parse()
+    if args.workload == "train":
+        return run_train(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
