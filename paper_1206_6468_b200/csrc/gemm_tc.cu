@@ -259,6 +259,7 @@ struct TcParams {
     unsigned *flags;
     // DIRICHLET (back-projection with the fused Eq. 6-8 element step): see launch_backproj_dirichlet_tc
     int ring_off;           // byte offset of the stage ring
+    int max_ctas;           // cap on the persistent grid (0 = one CTA per SM)
     int K, Kt, SN, nbc, ldf;
     const double *fconst;
     double *spsT, *sps2T, *hpartT;
@@ -789,7 +790,8 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
         if (e != cudaSuccess) return e;
     }
     const int n_total = ((p.M + TC_BM - 1) / TC_BM) * p.n_tiles;
-    const int grid = n_total < g_num_sms ? n_total : g_num_sms;
+    const int sms = (p.max_ctas > 0 && p.max_ctas < g_num_sms) ? p.max_ctas : g_num_sms;
+    const int grid = n_total < sms ? n_total : sms;
     static int dbg = -1, chunk = CHUNK_KB;
     if (dbg < 0) {
         const char *ev = getenv("NFHMM_TC_DEBUG");
@@ -868,6 +870,7 @@ cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st) {
     p.S = a.S;
     p.s = a.s;
     p.flags = a.flags;
+    p.max_ctas = a.max_ctas;
     if (p.mode == TC_RATIO && a.Vhat) return cudaErrorInvalidValue;   // RATIO always goes through TMA
     return launch_tc(p, a.A, a.lda, a.V, a.R, st);
 }

@@ -39,6 +39,11 @@ struct nfhmm {
     bool fused = false;
     int dir_variant = 0;   // Dirichlet kernel variant (NFHMM_DIRICHLET=tile: frame-tile kernel)
     int fb_wide = 1;       // N > 64: multi-warp forward-backward (NFHMM_FB_WIDE=0: one warp per direction)
+    // forward-backward overlapped with the reconstruction GEMM: the GEMM's persistent grid leaves
+    // `overlap_sms` SMs to the latency-bound recursion, which runs on a side stream (fork / join events)
+    int overlap_sms = 0, num_sms = 0;
+    cudaStream_t fbst = nullptr;
+    cudaEvent_t fev[2] = {nullptr, nullptr};
     int ldf = 0, nt_tc_b = 0;
     float *dvT = nullptr;
     double *spsT = nullptr, *sps2T = nullptr, *hpartT = nullptr;
@@ -229,8 +234,9 @@ int run_recon(nfhmm_t *h, int cls, ReconArgs a) {
 
 int data_tiles(const nfhmm_t *h) { return h->math == NFHMM_MATH_TC ? h->nt_tc_a : h->nt_a; }
 
-int recon_ratio(nfhmm_t *h) {
+int recon_ratio(nfhmm_t *h, int max_ctas = 0) {
     ReconArgs a{};
+    a.max_ctas = max_ctas;
     a.M = (int)h->frames;
     a.k_begin = 0;
     a.k_end = h->Kt;
@@ -375,11 +381,34 @@ int sweep(nfhmm_t *h, bool last) {
         r = step_backproj(h);
         if (!r) r = step_dirichlet(h, last);
     }
-    if (!r) r = step_fb(h);
     if (r) return r;
-    // (a) z-step of the new alpha: R for the next sweep and the data term of L_i
-    r = recon_ratio(h);
-    if (r) return r;
+    if (h->overlap_sms > 0) {
+        // (a) and (e) are independent given the new alpha: the reconstruction GEMM (launched first, on
+        // num_sms - overlap_sms SMs) and the forward-backward (side stream, the remaining SMs) overlap;
+        // the bound waits for both
+        if (!h->fbst) {
+            CU(h, cudaStreamCreateWithFlags(&h->fbst, cudaStreamNonBlocking));
+            CU(h, cudaEventCreateWithFlags(&h->fev[0], cudaEventDisableTiming));
+            CU(h, cudaEventCreateWithFlags(&h->fev[1], cudaEventDisableTiming));
+        }
+        CU(h, cudaEventRecord(h->fev[0], h->st));
+        CU(h, cudaStreamWaitEvent(h->fbst, h->fev[0], 0));
+        r = recon_ratio(h, h->num_sms - h->overlap_sms);
+        if (r) return r;
+        cudaStream_t main_st = h->st;
+        h->st = h->fbst;
+        r = step_fb(h);
+        h->st = main_st;
+        if (r) return r;
+        CU(h, cudaEventRecord(h->fev[1], h->fbst));
+        CU(h, cudaStreamWaitEvent(h->st, h->fev[1], 0));
+    } else {
+        r = step_fb(h);
+        if (r) return r;
+        // (a) z-step of the new alpha: R for the next sweep and the data term of L_i
+        r = recon_ratio(h);
+        if (r) return r;
+    }
     // (g) L_i (row iters_done of fe; the kernel keeps the index in a device counter)
     if (h->free_energy) {
         ElboArgs e{};
@@ -527,6 +556,13 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         h->dir_variant = (ed && strcmp(ed, "tile") == 0) ? 1 : 0;
         const char *ew = getenv("NFHMM_FB_WIDE");
         h->fb_wide = (ew && atoi(ew) == 0) ? 0 : 1;
+        // Large batches (> 65,536 frames, sequential forward-backward): the reconstruction GEMM leaves 32
+        // SMs to the forward-backward running beside it (measured at config 3: 16 / 24 / 32 / 40 / 48 / 64
+        // reserved SMs -> -5 / -6 / +1.9 / +1.6 / -0.2 / -4.7 %).  NFHMM_OVERLAP=n overrides (0 = off).
+        const char *eo = getenv("NFHMM_OVERLAP");
+        h->overlap_sms = (h->math == NFHMM_MATH_TC && frames > 65536 && h->fb_nchunk == 0) ? 32 : 0;
+        if (eo) h->overlap_sms = h->math == NFHMM_MATH_TC ? atoi(eo) : 0;
+        if (h->overlap_sms < 0 || h->overlap_sms > 64) h->overlap_sms = 0;
     }
     h->nt_tc_a = (int)((F + h->bn_tc_a - 1) / h->bn_tc_a);
     // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)
@@ -546,6 +582,7 @@ int nfhmm_workspace_size(const nfhmm_t *h, size_t *bytes) {
 int nfhmm_set_workspace(nfhmm_t *h, void *dptr, size_t bytes) {
     int r = enter(h);
     if (r) return r;
+    if (!h->num_sms) CU(h, cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device));
     const size_t need = ws_need(h);
     if (h->ws_owned && h->ws) {
         cudaFree(h->ws);
@@ -871,6 +908,9 @@ int nfhmm_destroy(nfhmm_t *h) {
     for (cudaEvent_t e : h->gev)
         if (e) cudaEventDestroy(e);
     if (h->gst) cudaStreamDestroy(h->gst);
+    for (cudaEvent_t e : h->fev)
+        if (e) cudaEventDestroy(e);
+    if (h->fbst) cudaStreamDestroy(h->fbst);
     if (h->ws_owned && h->ws) cudaFree(h->ws);
     delete h;
     return NFHMM_OK;

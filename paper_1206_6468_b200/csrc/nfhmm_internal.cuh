@@ -39,6 +39,7 @@ struct ReconArgs {
     unsigned *flags;
     const float *Bsplit;      // tensor-core path: pre-split, pre-tiled beta (tc_presplit_host)
     int nkb_total;
+    int max_ctas;             // tensor-core path: cap on the persistent grid (0 = one CTA per SM)
 };
 
 struct BackprojArgs {
