@@ -87,10 +87,20 @@ class Clocks:
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        # the sampler is running before the timed region starts (nvidia-smi takes ~0.1-0.3 s to start);
+        # regions shorter than the 200 ms period (small configs) are bracketed by the samples around them
+        t0 = time.time()
+        while time.time() - t0 < 3.0 and os.path.getsize(self.path) == 0:
+            time.sleep(0.02)
+        self.n0 = sum(1 for _ in open(self.path))
 
     def stop(self):
         if self.proc is None:
             return None
+        t0 = time.time()
+        while time.time() - t0 < 1.0 and sum(1 for _ in open(self.path)) <= getattr(self, "n0", 0):
+            time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -269,7 +279,8 @@ def run_ours(args):
         dist.barrier()
     # per-kernel device times (rooflines, shares): the same steps again with every launch bracketed by
     # CUDA events on the library's stream -- outside the timed region (the events and the eager launches
-    # they force would perturb it)
+    # they force would perturb it).  Profiling also turns off the FB / reconstruction overlap, so these
+    # are standalone kernel times (in the timed steps the FB runs beside the reconstruction GEMM).
     h.profile_enable(True)
     for _ in range(args.steps):
         step()

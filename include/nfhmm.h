@@ -160,7 +160,9 @@ int nfhmm_layout(const nfhmm_t *h, int64_t *F_pad, int64_t *Kt_pad, int32_t *bn_
 #define NFHMM_K_SEPARATE 5   /* (f) Section 4 reconstruction GEMMs + ratio mask                      */
 #define NFHMM_K_OTHER 6      /* initial state, observation statistics, dictionary transpose          */
 #define NFHMM_NUM_KERNEL_CLASSES 7
-/* on != 0 starts recording (and clears previous records); on = 0 stops. */
+/* on != 0 starts recording (and clears previous records); on = 0 stops.  While recording, sweeps run
+ * eagerly (no CUDA graphs) and without the forward-backward / reconstruction overlap, so every class is
+ * timed on its own. */
 int nfhmm_profile_enable(nfhmm_t *h, int on);
 /* Synchronise and return, per class, the summed device milliseconds and launch counts recorded since
  * the last enable.  Both arrays have NFHMM_NUM_KERNEL_CLASSES entries; either may be NULL. */

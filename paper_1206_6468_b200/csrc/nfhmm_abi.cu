@@ -382,7 +382,7 @@ int sweep(nfhmm_t *h, bool last) {
         if (!r) r = step_dirichlet(h, last);
     }
     if (r) return r;
-    if (h->overlap_sms > 0) {
+    if (h->overlap_sms > 0 && !h->prof) {   // (per-launch profiling times every kernel on its own)
         // (a) and (e) are independent given the new alpha: the reconstruction GEMM (launched first, on
         // num_sms - overlap_sms SMs) and the forward-backward (side stream, the remaining SMs) overlap;
         // the bound waits for both
