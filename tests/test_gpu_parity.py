@@ -245,3 +245,17 @@ def test_wide_forward_backward_matches_one_warp_kernel(c, over, monkeypatch):
     o = run_oracle(cfg, model, V[0], 4)
     assert rel_l2(wide["V_star"][0], o["V_star"]) <= TOL_VSTAR
     assert np.all(np.abs(wide["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
+
+
+@pytest.mark.parametrize("graphs", ["0", "1"])
+def test_fb_overlap_is_bitwise_neutral(graphs, monkeypatch):
+    """Large batches run the forward-backward beside the reconstruction GEMM (grid capped at num_SMs - 32,
+    side stream, fork/join; also inside CUDA graphs): every tile and recursion is computed exactly as
+    without the overlap, so the results are bitwise identical."""
+    cfg, model, V = make_inputs(3, M=34, T=2000)          # 68,000 frames > 65,536: overlap on by default
+    monkeypatch.setenv("NFHMM_GRAPHS", graphs)
+    ov = run_gpu(cfg, model, V, 3, separate=False)
+    monkeypatch.setenv("NFHMM_OVERLAP", "0")
+    seq = run_gpu(cfg, model, V, 3, separate=False)
+    for key in ("d_hat", "alpha_hat", "V_hat", "free_energy"):
+        assert np.array_equal(ov[key], seq[key]), key
