@@ -144,3 +144,37 @@ def test_learned_dictionaries_explain_held_out_data_better():
         before = oracle.nhmm_em(held[s], b0[s], th, a0[s], p0[s], 5)["loglik"][-1]
         after = oracle.nhmm_em(held[s], g["dict"][s], th, g["trans"][s], g["prior"][s], 5)["loglik"][-1]
         assert after > before
+
+
+def test_trained_models_separate_like_the_true_models():
+    """The pipeline the trainer exists for: learn each source's N-HMM on its isolated data (GPU EM), then
+    separate a mixture with the learned models (GPU VB + Section 4 masks).  The separated spectrograms'
+    distance to the true (pre-multinomial) sources must be close to the distance reached with the true
+    models -- and far below that of the untrained EM start."""
+    from paper_1206_6468_b200.nfhmm import NFHMM
+    c = 0
+    cfg = synth.config(c, T=400)
+    seed = synth.seed_of(c)
+    model = synth.make_model(cfg, seed)
+    Vtr = synth.make_training_data(cfg, model, seed, T=1000)
+    b0, a0, p0 = synth.make_em_init(cfg, seed)
+    g = run_gpu(cfg, Vtr, b0, a0, p0, 60)
+    mix = synth.make_mixture(cfg, model, seed + 4242, 0, with_truth=True)
+    truth = mix.sources / mix.sources.sum(0, keepdims=True).clip(1e-30) * mix.V[None]   # V split by true shares
+
+    def separate(beta, trans, prior):
+        h = NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K)
+        h.set_model(np.ascontiguousarray(beta, np.float32), np.ascontiguousarray(trans, np.float32),
+                    np.ascontiguousarray(prior, np.float32))
+        h.set_observations(mix.V[None])
+        h.vb_iterate(cfg.iters)
+        vst = h.separate()[0]
+        h.close()
+        return float(np.linalg.norm(vst - truth) / np.linalg.norm(truth))
+
+    err_true = separate(model.beta, model.trans, model.prior)
+    err_learned = separate(g["dict"], g["trans"], g["prior"])
+    err_start = separate(b0, a0, p0)
+    print(f"separation rel-L2 to the true sources: true models {err_true:.4f}, learned {err_learned:.4f}, EM start {err_start:.4f}")
+    assert err_learned <= 1.5 * err_true + 0.02, (err_learned, err_true)
+    assert err_learned < 0.5 * err_start, (err_learned, err_start)
