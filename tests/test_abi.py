@@ -99,3 +99,25 @@ def test_no_device_is_a_cuda_error_not_a_crash():
         n.nfhmm_set_workspace(h, None, 0)
     assert e.value.status == n.NFHMM_ECUDA
     n.nfhmm_destroy(h)
+
+
+@pytest.mark.parametrize("dims", [(0, 10, 4, 3, 1, 5), (33, 0, 4, 3, 1, 5), (33, 10, 0, 3, 1, 5), (33, 10, 129, 3, 1, 5),
+                                  (33, 10, 4, 0, 1, 5), (33, 10, 4, 33, 1, 5), (33, 10, 4, 3, 0, 5), (33, 10, 4, 3, 1, 0),
+                                  (4000, 10, 4, 20, 1, 5)])
+def test_trainer_create_rejects_bad_dims(dims):
+    """nhmm_train_create validates F, T, N (<= 128), K (<= 32), n_src, max_iters and K*F <= 51200 before
+    touching the device (no GPU needed)."""
+    from paper_1206_6468_b200 import nfhmm as n
+    h = ctypes.c_void_p()
+    F, T, N, K, S, it = dims
+    assert n.library().nhmm_train_create(F, T, N, K, S, it, 0, None, ctypes.byref(h)) == n.NFHMM_EINVAL
+    assert not h.value
+
+
+def test_trainer_null_handle_calls_are_safe():
+    from paper_1206_6468_b200 import nfhmm as n
+    lib = n.library()
+    assert lib.nhmm_train_destroy(None) == n.NFHMM_OK
+    assert lib.nhmm_train_em(None, 1) == n.NFHMM_EINVAL
+    assert lib.nhmm_train_set_data(None, None) == n.NFHMM_EINVAL
+    assert lib.nhmm_train_last_error(None) == b""
