@@ -397,8 +397,14 @@ def run_ours(args):
                 bf16_s = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1645.8)))
                 bf16_b = float(peaks.get("bf16_tflops", 1645.8))
                 peak = bf16_s * 0.5 / 3.0
+                # also against the nominal dense peak (2.25 PFLOP/s bf16 -> 375 TFLOP/s 3xTF32)
+                # at the maximum and at the measured SM clock of the timed steps
+                nominal = 2250.0 * 0.5 / 3.0
+                clk_mhz = (clk or {}).get("sm_mhz") or sm_max
                 return {"kernel": k, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                         "frac": achieved / peak, "frac_vs_burst": achieved / (bf16_b * 0.5 / 3.0),
+                        "frac_vs_nominal_max_clock": achieved / nominal,
+                        "frac_vs_nominal_at_clock": achieved / (nominal * clk_mhz / sm_max),
                         "peak_note": f"3xTF32 FP32-equivalent: measured sustained bf16 {bf16_s} TF/s x 1/2 (TF32) / 3",
                         "fp32_ffma_peak": fp32_peak}
             return {"kernel": k, "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
