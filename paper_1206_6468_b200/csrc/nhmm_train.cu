@@ -184,29 +184,29 @@ __global__ void __launch_bounds__(BK_THREADS) beta_kernel(int F, int T, int N, i
         cmp[z] = 0.f;
     }
     const int t1 = min(T, (c + 1) * tchunk);
+    // branch-free body (a zero weight where V = 0 or lhat = 0) so the loads of the next frames issue
+    // ahead of the arithmetic (the loop is bound by their latency)
+#pragma unroll 4
     for (int t = c * tchunk; t < t1; ++t) {
         const float v = lv ? V[((size_t)m * T + t) * F + l] : 0.f;
-        if (v > 0.f) {
-            const float *th = theta + (((size_t)m * T + t) * N + d) * K;
-            float tz[KM];
-            float lh = 0.f;   // the weights need FP32 only (the log-likelihood's lhat is FP64, estep_kernel)
+        const float *th = theta + (((size_t)m * T + t) * N + d) * K;
+        const float gm = gamma[((size_t)m * T + t) * N + d];
+        float tz[KM];
+        float lh = 0.f;   // the weights need FP32 only (the log-likelihood's lhat is FP64, estep_kernel)
 #pragma unroll
-            for (int z = 0; z < KM; ++z) {
-                tz[z] = z < K ? th[z] : 0.f;
-                lh = fmaf(tz[z], bz[z], lh);
-            }
-            if (lh > 0.f) {
-                const float g = gamma[((size_t)m * T + t) * N + d] * __fdiv_rn(v, lh);
-#pragma unroll
-                for (int z = 0; z < KM; ++z)
-                    if (z < K) {
-                        const float y = __fsub_rn(g * tz[z], cmp[z]);
-                        const float t2 = __fadd_rn(acc[z], y);
-                        cmp[z] = __fsub_rn(__fsub_rn(t2, acc[z]), y);
-                        acc[z] = t2;
-                    }
-            }
+        for (int z = 0; z < KM; ++z) {
+            tz[z] = z < K ? th[z] : 0.f;
+            lh = fmaf(tz[z], bz[z], lh);
         }
+        const float g = (v > 0.f && lh > 0.f) ? gm * __fdiv_rn(v, lh) : 0.f;
+#pragma unroll
+        for (int z = 0; z < KM; ++z)
+            if (z < K) {
+                const float y = __fsub_rn(g * tz[z], cmp[z]);
+                const float t2 = __fadd_rn(acc[z], y);
+                cmp[z] = __fsub_rn(__fsub_rn(t2, acc[z]), y);
+                acc[z] = t2;
+            }
     }
     if (lv) {
         float *dst = nb_part + (size_t)c * gridDim.y * M * K * F;   // [chunk][M][N][K][F]
