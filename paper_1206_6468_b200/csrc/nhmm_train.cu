@@ -63,25 +63,24 @@ __global__ void __launch_bounds__(256) estep_kernel(int F, int T, int N, int K, 
         const float *vr = V + ((size_t)m * T + t) * F;
         double ll = 0.0;
         bool zero = false;
+        // branch-free body, unrolled: the bins' independent FP64 chains (lhat, log) interleave
+#pragma unroll 2
         for (int l = lane; l < F; l += 32) {
             const float v = vr[l];
-            if (v > 0.f) {
-                // lhat in FP64: an FP32 sum (~3e-7 relative) times counts of 1e2-1e3 per bin would move
-                // loglik by ~1e-3 and the emission ratios of the non-dominant states by as much
-                double lh = 0.0;
+            // lhat in FP64: an FP32 sum (~3e-7 relative) times counts of 1e2-1e3 per bin would move
+            // loglik by ~1e-3 and the emission ratios of the non-dominant states by as much
+            double lh = 0.0;
 #pragma unroll
-                for (int z = 0; z < KM; ++z)
-                    if (z < K) lh = fma(tz[z], (double)bs[z * F + l], lh);
-                if (lh > 0.0) {
-                    ll += (double)v * log(lh);
-                    const float r = __fdiv_rn(v, (float)lh);   // a weight: FP32 suffices
+            for (int z = 0; z < KM; ++z)
+                if (z < K) lh = fma(tz[z], (double)bs[z * F + l], lh);
+            const bool use = v > 0.f && lh > 0.0;
+            zero |= v > 0.f && !(lh > 0.0);
+            const double lg = log(use ? lh : 1.0);
+            ll = fma((double)(use ? v : 0.f), lg, ll);
+            const float r = use ? __fdiv_rn(v, (float)lh) : 0.f;   // a weight: FP32 suffices
 #pragma unroll
-                    for (int z = 0; z < KM; ++z)
-                        if (z < K) cz[z] = fmaf(bs[z * F + l], r, cz[z]);
-                } else {
-                    zero = true;
-                }
-            }
+            for (int z = 0; z < KM; ++z)
+                if (z < K) cz[z] = fmaf(bs[z * F + l], r, cz[z]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, o);
