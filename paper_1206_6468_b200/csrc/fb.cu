@@ -835,6 +835,10 @@ int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len) {
 
 cudaError_t launch_fb(const FBArgs &a, cudaStream_t st) {
     const int N = a.N;
+    if (a.wide == 2 && a.nchunk <= 1 && N > 32 && N <= 64) {   // experiment: multi-warp kernel for few chains
+        if (N <= 40) return launch_fb_wide<40>(a, st);
+        if (N <= 64) return launch_fb_wide<64>(a, st);
+    }
     if (N <= 4) return launch_fb_t<4>(a, st);
     if (N <= 8) return launch_fb_t<8>(a, st);
     if (N <= 16) return launch_fb_t<16>(a, st);

@@ -117,7 +117,8 @@ struct FBArgs {
     float *bwd;               // [M][S][T][N] out: scaled backward messages b_t (d_t = u_t .* b_t / sum)
     double *logZ;             // [M][S] out
     unsigned *flags;
-    int wide;                 // N > 64: multi-warp kernel per chain and direction (1, default) or one warp (0)
+    int wide;                 // multi-warp kernel per chain and direction: 1 for N > 64 (default), 2 also for
+                              // 32 < N <= 64 (few chains), 0 never
     // parallel-in-time path (fbp_*): nchunk chunks of chunk_len steps; exact chunk-start messages
     int nchunk, chunk_len;    // nchunk <= 1: one sequential pass over [0, T)
     float *fstart;            // [M*S][nchunk][NMAX]  u_{t0} of each chunk (scratch)

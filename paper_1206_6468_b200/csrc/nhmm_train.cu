@@ -28,6 +28,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <new>
@@ -516,8 +517,11 @@ int nhmm_train_em(nhmm_train_t *h, int32_t n_iters) {
         f.bwd = h->bwd;
         f.logZ = h->logZ;
         f.flags = h->flags;
-        f.wide = 1;   // sequential recursion: the chunked (parallel-in-time) variant multiplies emission
-                      // ratios of ~1e-30 along 32-64 steps in FP32 and loses whole rows (measured)
+        // Sequential recursion (the chunked, parallel-in-time variant multiplies emission ratios of ~1e-30
+        // along 32-64 steps in FP32 and loses whole rows -- measured).  Few chains: the multi-warp kernel
+        // also for 32 < N <= 64 (one output per lane: 0.46 -> 0.38 ms for 2 chains of 2000 steps at
+        // N = 40; with ~1000 chains it measured 3 % slower).
+        f.wide = M <= 64 ? 2 : 1;
         TCU(h, launch_fb(f, h->st));
         trace_kernel<<<(M + 127) / 128, 128, 0, h->st>>>(M, h->iters, h->max_iters, h->logZ, h->trace);
         posterior_kernel<<<(MT + 7) / 8, 256, 0, h->st>>>(T, N, MT, h->fwd, h->bwd, h->ec, h->A, h->gamma, h->Zt);
