@@ -21,11 +21,12 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // block reads it, and the last block to finish advances it.
 __global__ void __launch_bounds__(256) elbo_kernel(ElboArgs p) {
     __shared__ double scratch[8];
-    __shared__ bool last;
-    const int m = blockIdx.x;
+    __shared__ bool last_m;
+    const int m = blockIdx.y, nb = gridDim.x, b = blockIdx.x;
     const int iter = *p.iter_ctr;
+    const int chunk = (p.T + nb - 1) / nb, t0 = b * chunk, t1 = min(p.T, t0 + chunk);
     double acc = 0.0;
-    for (int t = threadIdx.x; t < p.T; t += blockDim.x) {
+    for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
         const size_t f = (size_t)m * p.T + t;
         double v = p.hdir[f];
         for (int c = 0; c < p.n_tiles; ++c) v += p.data_part[f * p.n_tiles + c];
@@ -37,16 +38,25 @@ __global__ void __launch_bounds__(256) elbo_kernel(ElboArgs p) {
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += scratch[w];
-        for (int k = 0; k < p.S; ++k) s += p.logZ[(size_t)m * p.S + k];
-        s += p.c_prior_T;
-        if (iter < p.max_iters) p.fe[(size_t)m * p.max_iters + iter] = s;
+        p.part[(size_t)m * ELBO_MAX_BLOCKS + b] = s;
         __threadfence();
-        last = atomicAdd(p.done_ctr, 1u) == gridDim.x - 1;
-        if (last) {
-            *p.done_ctr = 0u;
-            *p.iter_ctr = iter + 1;
-            __threadfence();
-        }
+        last_m = atomicAdd(&p.mix_ctr[m], 1u) == (unsigned)nb - 1;
+    }
+    __syncthreads();
+    if (!last_m || threadIdx.x != 0) return;
+    // the mixture's last block: partials in block order (deterministic), then the chain and prior terms
+    __threadfence();
+    double s = 0.0;
+    for (int k = 0; k < nb; ++k) s += ((volatile double *)p.part)[(size_t)m * ELBO_MAX_BLOCKS + k];
+    for (int k = 0; k < p.S; ++k) s += p.logZ[(size_t)m * p.S + k];
+    s += p.c_prior_T;
+    if (iter < p.max_iters) p.fe[(size_t)m * p.max_iters + iter] = s;
+    p.mix_ctr[m] = 0u;
+    __threadfence();
+    if (atomicAdd(p.done_ctr, 1u) == gridDim.y - 1) {   // the last mixture advances the sweep counter
+        *p.done_ctr = 0u;
+        *p.iter_ctr = iter + 1;
+        __threadfence();
     }
 }
 
@@ -172,7 +182,9 @@ int grid_for(size_t n, int block) {
 }  // namespace
 
 cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st) {
-    elbo_kernel<<<a.M, 256, 0, st>>>(a);
+    int nb = (a.T + 255) / 256;
+    nb = nb < 1 ? 1 : (nb > ELBO_MAX_BLOCKS ? ELBO_MAX_BLOCKS : nb);
+    elbo_kernel<<<dim3(nb, a.M), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -34,6 +34,8 @@ struct nfhmm {
     float *bs_a = nullptr, *bs_b = nullptr;   // tensor-core path: pre-split beta for (a) and betaT for (b)
     double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
     double *fconst = nullptr;   // per-frame alpha_0, psi(alpha_0), bound constant (set_observations)
+    double *elbo_part = nullptr;   // [M][ELBO_MAX_BLOCKS] bound partial sums
+    unsigned *elbo_ctr = nullptr;  // [M] per-mixture block counters of the bound kernel
     // Dirichlet step fused into the back-projection epilogue (tensor-core engine, K <= 32): block-major
     // pseudo-counts, Eq. 8 block sums and g~ partials, frame pitch ldf
     bool fused = false;
@@ -173,6 +175,8 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take(fr * (size_t)(h->nt_a > h->nt_tc_a ? h->nt_a : h->nt_tc_a) * 8); h->data_part = (double *)p;
     p = take(fr * 8);                            h->hdir = (double *)p;
     p = take(fr * 4 * 8);                        h->fconst = (double *)p;
+    p = take((size_t)h->M * ELBO_MAX_BLOCKS * 8); h->elbo_part = (double *)p;
+    p = take((size_t)h->M * 4);                  h->elbo_ctr = (unsigned *)p;
     {   // parallel-in-time FB scratch (NMAX <= 64 on that path)
         const size_t units = (size_t)h->M * h->S * (size_t)h->fb_nchunk;
         p = take(units * 64 * 64 * 4);           h->fbP = (float *)p;
@@ -418,6 +422,8 @@ int sweep(nfhmm_t *h, bool last) {
         e.S = h->S;
         e.iter_ctr = reinterpret_cast<int *>(h->flags + 1);
         e.done_ctr = h->flags + 2;
+        e.part = h->elbo_part;
+        e.mix_ctr = h->elbo_ctr;
         e.max_iters = h->max_iters;
         e.c_prior_T = h->c_prior_T;
         e.data_part = h->data_part;
@@ -686,6 +692,7 @@ int nfhmm_reset(nfhmm_t *h) {
                                 h->bwd, (long long)h->M * h->S * h->T * h->N, h->st));
     CU(h, cudaMemsetAsync(h->fe, 0, (size_t)h->M * h->max_iters * 8, h->st));
     CU(h, cudaMemsetAsync(h->flags + 1, 0, 2 * sizeof(unsigned), h->st));   // sweep counter, ELBO block count
+    CU(h, cudaMemsetAsync(h->elbo_ctr, 0, (size_t)h->M * sizeof(unsigned), h->st));
     h->R_valid = false;
     r = recon_ratio(h);
     if (r) return r;

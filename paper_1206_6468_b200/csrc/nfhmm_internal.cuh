@@ -140,7 +140,10 @@ struct ElboArgs {
     const double *hdir;       // [M*T]
     const double *logZ;       // [M][S]
     double *fe;               // [M][max_iters]
+    double *part;             // [M][ELBO_MAX_BLOCKS] per-block partial sums
+    unsigned *mix_ctr;        // [M] blocks of each mixture finished (zero between launches)
 };
+constexpr int ELBO_MAX_BLOCKS = 16;   // blocks per mixture (frames split so a single mixture fills several SMs)
 cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st);
 
 // Initial state (DESIGN R5): alpha = 1 + gamma/N, theta = exp(psi(a) - psi(Kt a)), d = 1/N.
