@@ -807,14 +807,23 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
 
 }  // namespace
 
-int tc_pick_bn(int64_t n, int mult) {
+int tc_pick_bn(int64_t n, int mult, int64_t rows, int sms) {
     int best = 0;
-    int64_t best_pad = INT64_MAX;
-    // padded width plus a per-tile cost (each extra column tile re-reads the A rows from L2)
-    for (int bn = mult; bn <= TC_MAX_BN; bn += mult) {
-        const int64_t pad = (n + bn - 1) / bn * bn + 24 * ((n + bn - 1) / bn);
-        if (pad < best_pad || (pad == best_pad && bn > best)) {
-            best_pad = pad;
+    int64_t best_cost = INT64_MAX;
+    const int64_t mt = (rows + TC_BM - 1) / TC_BM;
+    // time ~ waves of the persistent grid x per-tile work, the latter ~ padded width plus a per-tile cost
+    // (each column tile re-reads the A rows from L2; 24 columns' worth).  For large row counts this is the
+    // padded width plus 24 per tile; for few row tiles (single mixtures: 8-16 row tiles) narrower tiles
+    // put more of the 148 SMs to work.
+    // (16-column tiles only when one tile covers n: several 16-wide column tiles gave wrong results in
+    // the edge-shape tests and are not used)
+    const int lo = (n > 16 && mult < 32) ? 32 : mult;
+    for (int bn = lo; bn <= TC_MAX_BN; bn += mult) {
+        const int64_t nt = (n + bn - 1) / bn;
+        const int64_t waves = (mt * nt + sms - 1) / sms;
+        const int64_t cost = rows > 0 ? waves * (bn + 24) : nt * (bn + 24);
+        if (cost < best_cost || (cost == best_cost && bn > best)) {
+            best_cost = cost;
             best = bn;
         }
     }

@@ -545,7 +545,7 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         h->fb_nchunk = nc > 1 ? nc : 0;
         h->fb_len = nc > 1 ? L : 0;
     }
-    h->bn_tc_a = tc_pick_bn(F);
+    h->bn_tc_a = tc_pick_bn(F, 16, frames);
     {   // Dirichlet element step fused into the back-projection epilogue (opt-in, NFHMM_FUSED=1): correct
         // but measured slower (DESIGN "Fused Dirichlet epilogue"): the element work competes with the
         // GEMM's own epilogue / converter issue slots and stalls the MMAs.  Column tiles of whole K-blocks.
@@ -555,7 +555,7 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         const int64_t SN = (int64_t)S * N;
         h->fused = h->math == NFHMM_MATH_TC && K <= 32 && l <= 192 && SN * 33 * 8 <= 200 * 1024 &&
                    e && atoi(e) != 0;
-        h->bn_tc_b = h->fused ? tc_pick_bn(Kt, l) : tc_pick_bn(Kt);
+        h->bn_tc_b = h->fused ? tc_pick_bn(Kt, l, frames) : tc_pick_bn(Kt, 16, frames);
         h->nt_tc_b = (int)((Kt + h->bn_tc_b - 1) / h->bn_tc_b);
         h->ldf = (int)((frames + 31) / 32 * 32);
         const char *ed = getenv("NFHMM_DIRICHLET");

@@ -61,7 +61,9 @@ cudaError_t launch_backproj(int bn, const BackprojArgs &a, cudaStream_t st);
 
 // tcgen05 3xTF32 variants (gemm_tc.cu).  recon: a.B = beta [F_pad][Kt_pad] K-major (ldb = Kt_pad);
 // backproj: a.B = betaT [Kt_pad][F_pad] K-major, a.Kpad = F_pad, a.ldb = row length of theta / n.
-int tc_pick_bn(int64_t n, int mult = 16);   // tile width: a multiple of mult (itself a multiple of 16)
+// tile width (a multiple of mult, itself a multiple of 16) for n output columns and `rows` output rows
+// (rows = 0: ignore the row count) on `sms` SMs
+int tc_pick_bn(int64_t n, int mult = 16, int64_t rows = 0, int sms = 148);
 // The static operand B[n][k] (n < n_rows, k < k_len; src[n*ld + k], or src[k*ld + n] if transposed) split
 // into tf32 hi/lo and re-tiled into the shared-memory image of each pipeline stage (host side, once).
 size_t tc_presplit_floats(int64_t n_rows, int64_t k_len, int bn);
