@@ -815,10 +815,7 @@ int tc_pick_bn(int64_t n, int mult, int64_t rows, int sms) {
     // (each column tile re-reads the A rows from L2; 24 columns' worth).  For large row counts this is the
     // padded width plus 24 per tile; for few row tiles (single mixtures: 8-16 row tiles) narrower tiles
     // put more of the 148 SMs to work.
-    // (16-column tiles only when one tile covers n: several 16-wide column tiles gave wrong results in
-    // the edge-shape tests and are not used)
-    const int lo = (n > 16 && mult < 32) ? 32 : mult;
-    for (int bn = lo; bn <= TC_MAX_BN; bn += mult) {
+    for (int bn = mult; bn <= TC_MAX_BN; bn += mult) {
         const int64_t nt = (n + bn - 1) / bn;
         const int64_t waves = (mt * nt + sms - 1) / sms;
         const int64_t cost = rows > 0 ? waves * (bn + 24) : nt * (bn + 24);
@@ -836,10 +833,13 @@ size_t tc_presplit_floats(int64_t n_rows, int64_t k_len, int bn) {
 }
 
 // B[n][k] = get(n, k) for n < n_rows, k < k_len (zero elsewhere) -> dst in the shared-memory image of
-// each pipeline stage: chunk (nt, kb) = [hi: c4, r, 4][lo: c4, r, 4] with r < bn, c4 < 4.
+// each pipeline stage: chunk (nt, kb) = [hi: c4, r, 4][lo: c4, r, 4] with r < bn, c4 < 4.  The chunks of a
+// column tile are laid out for k_pad >= k_len (the contraction length the kernel walks, nkb_total =
+// ceil(k_pad / 16)), so tile nt starts at chunk nt * nkb_total.
 void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
-                      float *dst) {
-    const int64_t nt_n = (n_rows + bn - 1) / bn, nkb = (k_len + TC_KB - 1) / TC_KB;
+                      float *dst, int64_t k_pad) {
+    if (k_pad < k_len) k_pad = k_len;
+    const int64_t nt_n = (n_rows + bn - 1) / bn, nkb = (k_pad + TC_KB - 1) / TC_KB;
     for (int64_t nt = 0; nt < nt_n; ++nt)
         for (int64_t kb = 0; kb < nkb; ++kb) {
             float *chunk = dst + ((size_t)nt * nkb + kb) * 2 * bn * TC_KB;

@@ -662,7 +662,8 @@ int nfhmm_set_model(nfhmm_t *h, const float *dict, const float *trans, const flo
         std::vector<float> bsa(tc_presplit_floats(h->F, h->Kt, h->bn_tc_a));
         std::vector<float> bsb(tc_presplit_floats(h->Kt, h->Fa, h->bn_tc_b));
         tc_presplit_host(hd.data(), h->F, /*transposed=*/true, h->F, h->Kt, h->bn_tc_a, bsa.data());    // B[n=l][k]
-        tc_presplit_host(hd.data(), h->F, /*transposed=*/false, h->Kt, h->F, h->bn_tc_b, bsb.data());   // B[n=k][l]
+        // B[n=k][l]: bins l < F, chunks laid out for the padded contraction Fa the kernel walks
+        tc_presplit_host(hd.data(), h->F, /*transposed=*/false, h->Kt, h->F, h->bn_tc_b, bsb.data(), h->Fa);
         CU(h, cudaMemcpyAsync(h->bs_a, bsa.data(), bsa.size() * 4, cudaMemcpyHostToDevice, h->st));
         CU(h, cudaMemcpyAsync(h->bs_b, bsb.data(), bsb.size() * 4, cudaMemcpyHostToDevice, h->st));
         CU(h, cudaStreamSynchronize(h->st));

@@ -68,7 +68,7 @@ int tc_pick_bn(int64_t n, int mult = 16, int64_t rows = 0, int sms = 148);
 // into tf32 hi/lo and re-tiled into the shared-memory image of each pipeline stage (host side, once).
 size_t tc_presplit_floats(int64_t n_rows, int64_t k_len, int bn);
 void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
-                      float *dst);
+                      float *dst, int64_t k_pad = 0);
 cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st);
 cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st);
 
