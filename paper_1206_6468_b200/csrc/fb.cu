@@ -648,12 +648,12 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
     };
     // x (broadcast in smem) times the slot matrix Ms (lane-owned columns); xsum = sum of x
     auto vecmat = [&](const float *x, const float *Ms, float (&out)[NQ], float &xsum) {
-        uint64_t acc[NQ][2];
+        uint64_t acc[NQ][4];   // four independent FFMA2 chains per output (as step_products)
         uint64_t s2[2] = {0ull, 0ull};
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) acc[q][0] = acc[q][1] = 0ull;
+        for (int q = 0; q < NQ; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0ull;
         const ulonglong2 *x4 = reinterpret_cast<const ulonglong2 *>(x);
-#pragma unroll 2
+#pragma unroll
         for (int i4 = 0; i4 < NMAX / 4; ++i4) {
             const ulonglong2 v = x4[i4];
             add2(s2[0], v.x);
@@ -661,13 +661,15 @@ __global__ void __launch_bounds__(64) fbp_scan_kernel(FBArgs p, const float *P, 
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const int j = min(32 * q + lane, NMAX - 1), i = 4 * i4;
-                fma2(acc[q][0], v.x, pk2(Ms[i * NMAX + j], Ms[(i + 1) * NMAX + j]));
-                fma2(acc[q][1], v.y, pk2(Ms[(i + 2) * NMAX + j], Ms[(i + 3) * NMAX + j]));
+                fma2(acc[q][(2 * i4) & 3], v.x, pk2(Ms[i * NMAX + j], Ms[(i + 1) * NMAX + j]));
+                fma2(acc[q][(2 * i4 + 1) & 3], v.y, pk2(Ms[(i + 2) * NMAX + j], Ms[(i + 3) * NMAX + j]));
             }
         }
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             add2(acc[q][0], acc[q][1]);
+            add2(acc[q][2], acc[q][3]);
+            add2(acc[q][0], acc[q][2]);
             out[q] = hsum2(acc[q][0]);
         }
         add2(s2[0], s2[1]);
