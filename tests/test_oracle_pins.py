@@ -508,6 +508,20 @@ def test_disjoint_supports_attribute_mass(oracle):
     Et = r["alpha"] / r["alpha"].sum(1, keepdims=True)
     share0 = Et[:, : N * K].sum(1)
     assert (share0[0::2] >= 0.95).all(), share0
+    # Section 4 attributes each bin to the source whose reconstruction explains it: with
+    # disjoint supports source s's V_src is (up to the 1e-12 floor) zero off its half, so V*^(0) = V on
+    # the lower half and V*^(1) = V on the upper half of EVERY frame, and on source-0-only frames
+    # V*^(0) carries >= 95% of the frame's mass (an s <-> S-1-s swap of the outputs fails both).
+    vsrc, vst = oracle.separate(beta, V, r["alpha"], (F, T, S, N, K))
+    h = F // 2
+    np.testing.assert_allclose(vst[0][:, :h], V[:, :h], rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(vst[1][:, h:], V[:, h:], rtol=1e-6, atol=1e-6)
+    assert np.abs(vst[0][:, h:]).max() <= 1e-6 * V.max()
+    assert np.abs(vst[1][:, :h]).max() <= 1e-6 * V.max()
+    assert vsrc[0][:, h:].max() <= 1e-8 * vsrc[0].max() and vsrc[1][:, :h].max() <= 1e-8 * vsrc[1].max()
+    vt = V.sum(1)
+    assert (vst[0].sum(1)[0::2] >= 0.95 * vt[0::2]).all()
+    assert (vst[1].sum(1)[0::2] <= 0.05 * vt[0::2]).all()
 
 
 def test_S1_d_is_fb_of_surrogate(oracle):
