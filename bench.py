@@ -172,7 +172,30 @@ def cfg_id(cfg):
 
 
 # ------------------------------------------------------------------------------------------------
+def config_line(args, cfg, iters):
+    """The `config` object of the JSON line -- identical for both arms (same workload)."""
+    return {"workload": f"cfg{args.config}-{cfg.name}", "S": cfg.S, "N": cfg.N, "K": cfg.K, "F": cfg.F, "T": cfg.T,
+            "mixtures": cfg.M, "iters": iters, "parallelism": f"mixture-shard x{args.gpus}",
+            "l2": "no flush: per-step inputs/state exceed L2 (V, theta and alpha of a step are GBs)" if cfg.M * cfg.T * cfg.F * 4 > 2e8
+                  else "no flush: small config (inputs fit in L2)",
+            "step": "reset + iters sweeps + separate, inputs resident in memory"}
+
+
+def _pin_worker(counter, cores):
+    """Pool initializer: pin this worker to one host core (taskset equivalent)."""
+    with counter.get_lock():
+        i = counter.value
+        counter.value += 1
+    try:
+        os.sched_setaffinity(0, {cores[i % len(cores)]})
+    except (AttributeError, OSError):
+        pass
+
+
 def run_reference(args):
+    """The oracle as it stands (FP64, single-threaded per process), P_cpu = min(host cores, mixtures)
+    independent processes pinned one per core, each running whole mixtures of the workload (full T) for
+    a bounded number of sweeps per step (the cost per sweep is constant: no early stopping).  Rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -182,35 +205,46 @@ def run_reference(args):
     iters = args.iters or cfg.iters
     seed = synth.seed_of(args.config)
     model = synth.make_model(cfg, seed)
-    procs = max(1, min(os.cpu_count() or 1, 16))
-    # one step = every process runs its sample once; the sample is sized so all steps fit in minutes
+    try:
+        cores = sorted(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = list(range(os.cpu_count() or 1))
+    procs = max(1, min(len(cores), cfg.M))
+    # the whole --warmup W --steps K run is sized to finish in a few minutes
     per_step_s = max(2.0, min(20.0, 240.0 / max(1, args.steps + args.warmup)))
-    Vs = [synth.make_mixture(cfg, model, seed, m).V for m in range(min(procs, cfg.M))]
+    Vs = [synth.make_mixture(cfg, model, seed, m).V for m in range(procs)]
+    import multiprocessing as mp
     from concurrent.futures import ProcessPoolExecutor
     from oracle import oracle
     oracle.build()
-    T_s = min(cfg.T, 250)
-    sub = synth.Config(**{**cfg.__dict__, "T": T_s})
-    t1 = _oracle_job((sub, model, np.ascontiguousarray(Vs[0][:T_s]), 1))
+    t1 = _oracle_job((cfg, model, Vs[0], 1))                   # calibrate: one sweep of one full mixture
     sweeps = max(1, int(per_step_s / max(t1, 1e-3)))
-    jobs = [(sub, model, np.ascontiguousarray(Vs[i % len(Vs)][:T_s]), sweeps) for i in range(procs)]
+    if sweeps == 1 and t1 > per_step_s:                          # very large configs: a frame sample
+        T_s = max(1, int(cfg.T * per_step_s / t1))
+    else:
+        T_s = cfg.T
+    sub = synth.Config(**{**cfg.__dict__, "T": T_s})
+    jobs = [(sub, model, np.ascontiguousarray(Vs[i][:T_s]), sweeps) for i in range(procs)]
+    ctx = mp.get_context("fork")
+    counter = ctx.Value("i", 0)
     times = []
-    with ProcessPoolExecutor(max_workers=procs) as ex:
+    with ProcessPoolExecutor(max_workers=procs, mp_context=ctx, initializer=_pin_worker,
+                             initargs=(counter, cores)) as ex:
         for i in range(args.warmup + args.steps):
             t0 = time.perf_counter()
             list(ex.map(_oracle_job, jobs))
             dt = time.perf_counter() - t0
             if i >= args.warmup:
                 times.append(dt)
-    ms = 1000.0 * (max(times) if times else float("nan"))
+    ms = 1000.0 * statistics.mean(times) if times else float("nan")
     value = procs * T_s * sweeps / (ms / 1000.0)
-    sample = f"{procs} processes x 1 mixture x T={T_s} frames x {sweeps} sweeps per step"
+    sample = (f"{procs} processes pinned one per host core, each mixture {0}..{procs - 1} x T={T_s} frames x "
+              f"{sweeps} sweeps per step (of the config's {cfg.M} x {cfg.T} frames x {iters} sweeps); mean step time")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg{args.config}-{cfg.name}", "S": cfg.S, "N": cfg.N, "K": cfg.K, "F": cfg.F,
-                   "T": cfg.T, "mixtures": cfg.M, "iters": iters},
+        "config": config_line(args, cfg, iters),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -218,11 +252,82 @@ def run_reference(args):
     return 0
 
 
+def gather_results(h, cfg, iters, M, world, rank, dev, elapsed_ms):
+    """NCCL gathers after the timed region: free-energy traces (all_gather), d_hat (to rank 0, global
+    mixture order) and the per-rank device times.  Returns a summary for the JSON line: sizes, the
+    gather's device time and digests of the gathered arrays (equal digests across --gpus N = the
+    per-mixture results do not depend on the sharding)."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+    S, T, N = cfg.S, cfg.T, cfg.N
+    d = torch.empty((M, S, T, N), dtype=torch.float32, device=f"cuda:{dev}")
+    fe = np.empty((M, h.max_iters), np.float64)
+    from paper_1206_6468_b200.nfhmm import nfhmm_posteriors
+    nfhmm_posteriors(h.h, d, None, None, fe)
+    fe_d = torch.from_numpy(np.ascontiguousarray(fe[:, :iters])).to(f"cuda:{dev}")
+    rows = max(len(shard(cfg.M, world, r)) for r in range(world))
+    sizes = [len(shard(cfg.M, world, r)) for r in range(world)]
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    if world > 1:
+        pad = lambda x: torch.cat([x, x.new_zeros((rows - x.shape[0],) + tuple(x.shape[1:]))]) if x.shape[0] < rows else x  # noqa: E731
+        fe_all = torch.empty((world * rows, iters), dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_gather_into_tensor(fe_all, pad(fe_d))
+        d_all = torch.empty((world * rows, S, T, N), dtype=torch.float32, device=f"cuda:{dev}") if rank == 0 else None
+        dist.gather(pad(d), [d_all[r * rows:(r + 1) * rows] for r in range(world)] if rank == 0 else None, dst=0)
+        times = torch.empty(world, dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_gather_into_tensor(times, torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{dev}"))
+        keep = torch.cat([torch.arange(r * rows, r * rows + sizes[r], device=f"cuda:{dev}") for r in range(world)])
+        fe_all = fe_all[keep]
+        d_all = d_all[keep] if rank == 0 else None
+    else:
+        fe_all, d_all = fe_d, d
+        times = torch.tensor([elapsed_ms], dtype=torch.float64)
+    g1.record()
+    torch.cuda.synchronize()
+    out = {"collective": "nccl all_gather (free energies, timings) + gather to rank 0 (d_hat)" if world > 1
+           else "none (1 rank)", "ms": g0.elapsed_time(g1),
+           "bytes": int(cfg.M * S * T * N * 4 + cfg.M * iters * 8 + world * 8),
+           "rank_ms": [round(float(x), 3) for x in times.cpu().tolist()]}
+    if rank == 0:
+        fe_h = fe_all.cpu().numpy()
+        out["mixtures"] = int(fe_h.shape[0])
+        out["L_final_sum"] = float(fe_h[:, -1].sum())
+        out["L_digest"] = hashlib.sha256(fe_h.tobytes()).hexdigest()[:16]
+        out["d_hat_digest"] = hashlib.sha256(d_all.cpu().numpy().tobytes()).hexdigest()[:16]
+    del d, d_all
+    return out
+
+
+def relaunch_command(args_argv, gpus, port):
+    """bench.py --gpus N (N > 1) run outside torchrun: the same command under torch.distributed.run,
+    one rank per GPU of this node (the driver's own launch line)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *args_argv]
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch with torchrun "
+                         f"--nproc-per-node {args.gpus} (or without WORLD_SIZE to let bench.py launch it)")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: --gpus {world} needs {world} visible GPUs, found {torch.cuda.device_count()}")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -281,6 +386,10 @@ def run_ours(args):
     # CUDA events on the library's stream -- outside the timed region (the events and the eager launches
     # they force would perturb it).  Profiling also turns off the FB / reconstruction overlap, so these
     # are standalone kernel times (in the timed steps the FB runs beside the reconstruction GEMM).
+    # ---- gather (north_star: NCCL only to gather posteriors, free energies and timings) -------------
+    # After the timed region and outside it: every rank's free-energy traces all-gathered, the
+    # posteriors d_hat gathered to rank 0 in global mixture order, per-rank device times all-gathered.
+    gathered = gather_results(h, cfg, iters, M, world, rank, dev, elapsed)
     h.profile_enable(True)
     for _ in range(args.steps):
         step()
@@ -443,12 +552,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"cfg{args.config}-{cfg.name}", "S": cfg.S, "N": cfg.N, "K": cfg.K, "F": cfg.F,
-                       "T": cfg.T, "mixtures": cfg.M, "iters": iters, "parallelism": f"mixture-shard x{world}",
-                       "l2": "no flush: per-step inputs/state exceed L2 (V %.2f GB, theta %.2f GB per GPU)" % (
-                           M * cfg.T * h.layout()["F_pad"] * 4 / 1e9, M * cfg.T * h.layout()["Kt_pad"] * 4 / 1e9),
-                       "step": "reset + iters sweeps + separate, inputs resident in HBM"},
-            "value_bound_off": value_bound_off,
+            "config": config_line(args, cfg, iters),
+            "value_bound_off": value_bound_off, "gathered": gathered,
             "roofline": roof, "rooflines": roof_all, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches, "gen_seconds": round(t_gen, 2),
         }
@@ -537,6 +642,8 @@ def run_train(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return subprocess.call(relaunch_command(sys.argv[1:], args.gpus, _free_port()))
     if args.workload == "train":
         return run_train(args)
     if args.impl == "reference":

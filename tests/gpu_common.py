@@ -1,9 +1,14 @@
 """Shared helpers of the GPU parity tests: run the CUDA path (through the C-ABI) and the oracle on the
 same seeded synthetic inputs.  Inputs come only from paper_1206_6468_b200.synth; expected values only
 from oracle/ (never from the CUDA path)."""
+import json
+import os
+
 import numpy as np
 
 from paper_1206_6468_b200 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def rel_l2(x, ref):
@@ -53,4 +58,33 @@ def run_oracle(cfg, model, Vm, iters, gamma=1.0, separate=True):
     if separate:
         vs, vst = oracle.separate(model.beta, Vm, r["alpha"], cfg.dims)
         r["V_src"], r["V_star"] = vs, vst
+    return r
+
+
+RECORD_PATH = os.environ.get("NFHMM_PARITY_LOG", os.path.join(ROOT, "gpurun_out", "parity_records.jsonl"))
+
+
+def record(tag, quantity, **vals):
+    """Append one parity measurement (JSON line) to the parity record and print it."""
+    line = dict(tag=tag, quantity=quantity, **{k: (float(v) if isinstance(v, (np.floating, float)) else v)
+                                                for k, v in vals.items()})
+    print("PARITY", json.dumps(line))
+    try:
+        os.makedirs(os.path.dirname(RECORD_PATH), exist_ok=True)
+        with open(RECORD_PATH, "a") as f:
+            f.write(json.dumps(line) + "\n")
+    except OSError:
+        pass
+
+
+def compare(tag, quantity, x, ref, tol):
+    """rel-L2 gate (DESIGN R13) with max-abs and max-relative logged beside it."""
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    r = rel_l2(x, ref)
+    diff = np.abs(x - ref)
+    mx = float(diff.max()) if diff.size else 0.0
+    scale = float(np.abs(ref).max()) if ref.size else 0.0
+    record(tag, quantity, rel_l2=r, max_abs=mx, max_abs_over_max_ref=(mx / scale if scale > 0 else 0.0), tol=tol)
+    assert r <= tol, (tag, quantity, r)
     return r

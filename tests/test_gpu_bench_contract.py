@@ -39,14 +39,18 @@ def test_bench_line_has_the_contract_keys():
     assert d["gpu_launches"] > 0
 
 
-def test_reference_arm_line():
-    d = run("--impl", "reference", "--config", "0", "--steps", "1", "--warmup", "0", "--cpu-seconds", "1")
-    assert d["impl"] == "reference" and d["value"] > 0
-    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
-    assert d["cpu_baseline"]["kind"] == "oracle"
-
-
 def test_training_workload_line():
     d = run("--workload", "train", "--config", "0", "--steps", "2", "--warmup", "1", "--iters", "3", "--train-T", "200",
             "--cpu-seconds", "1")
     assert d["value"] > 0 and d["gpu_launches"] > 0 and d["config"]["workload"] == "train-cfg0"
+
+
+def test_gathered_block_and_gpus_beyond_the_node_fail_loudly():
+    import torch
+    d = run("--config", "0", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-bound-off")
+    g = d["gathered"]
+    assert g["mixtures"] == 1 and len(g["rank_ms"]) == 1 and len(g["d_hat_digest"]) == 16
+    n = torch.cuda.device_count() + 1      # more ranks than GPUs: every rank refuses, the launch fails
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--config", "0",
+                          "--steps", "3", "--warmup", "3"], capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert out.returncode != 0 and "visible GPUs" in out.stderr + out.stdout

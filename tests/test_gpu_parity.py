@@ -10,7 +10,7 @@ at full size in test_gpu_fullsize.py.
 import numpy as np
 import pytest
 
-from tests.gpu_common import make_inputs, rel_l2, run_gpu, run_oracle
+from tests.gpu_common import compare, make_inputs, rel_l2, run_gpu, run_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -25,15 +25,16 @@ MATHS = ["tc", "simt"]
 def check_parity(cfg, model, V, iters, gamma=1.0, mixtures=None, tol1=TOL1, math="tc"):
     g1 = run_gpu(cfg, model, V, 1, gamma=gamma, separate=False, math=math)
     gn = run_gpu(cfg, model, V, iters, gamma=gamma, math=math)
+    tag = f"{cfg.name}:S{cfg.S}N{cfg.N}K{cfg.K}F{cfg.F}T{cfg.T}M{V.shape[0]}:g{gamma}:{math}"
     for m in (mixtures if mixtures is not None else range(V.shape[0])):
         o1 = run_oracle(cfg, model, V[m], 1, gamma=gamma, separate=False)
-        assert rel_l2(g1["d_hat"][m], o1["d_hat"]) <= tol1
-        assert rel_l2(g1["V_hat"][m], o1["V_hat"]) <= tol1
-        assert rel_l2(g1["alpha_hat"][m], o1["alpha"]) <= tol1
+        compare(f"{tag}/m{m}/sweep1", "d_hat", g1["d_hat"][m], o1["d_hat"], tol1)
+        compare(f"{tag}/m{m}/sweep1", "V_hat", g1["V_hat"][m], o1["V_hat"], tol1)
+        compare(f"{tag}/m{m}/sweep1", "alpha_hat", g1["alpha_hat"][m], o1["alpha"], tol1)
         assert abs(g1["free_energy"][m, 0] - o1["free_energy"][0]) <= TOL_L * abs(o1["free_energy"][0])
         on = run_oracle(cfg, model, V[m], iters, gamma=gamma)
-        assert rel_l2(gn["V_star"][m], on["V_star"]) <= TOL_VSTAR
-        assert rel_l2(gn["V_src"][m], on["V_src"]) <= TOL_VSTAR
+        compare(f"{tag}/m{m}/sweep{iters}", "V_star", gn["V_star"][m], on["V_star"], TOL_VSTAR)
+        compare(f"{tag}/m{m}/sweep{iters}", "V_src", gn["V_src"][m], on["V_src"], TOL_VSTAR)
         fe_g, fe_o = gn["free_energy"][m], on["free_energy"]
         assert fe_g.shape == fe_o.shape
         assert np.all(np.abs(fe_g - fe_o) <= TOL_L * np.abs(fe_o)), np.max(np.abs(fe_g - fe_o) / np.abs(fe_o))
