@@ -749,11 +749,9 @@ size_t fused_tile_bytes(int SN, int elem) { return (size_t)SN * (FR + 1) * elem;
 cudaError_t launch_dv(const DirichletArgs &a, float *dvT, cudaStream_t st) {
     const size_t smem = fused_tile_bytes(a.S * a.N, 4);
     if (a.N > 128 || smem > 200 * 1024) return cudaErrorInvalidValue;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && attr < smem) {
-        cudaError_t e = cudaFuncSetAttribute(dv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_dyn_smem((const void *)dv_kernel, smem);
         if (e != cudaSuccess) return e;
-        attr = smem;
     }
     dv_kernel<<<(a.frames + FR - 1) / FR, WPB * 32, smem, st>>>(a, dvT);
     return cudaGetLastError();
@@ -763,17 +761,16 @@ cudaError_t launch_eq8(const DirichletArgs &a, const double *spsT, const double 
                        int n_tiles, int bn, cudaStream_t st) {
     const size_t smem = fused_tile_bytes(a.S * a.N, 8);
     if (a.N > 128 || smem > 200 * 1024) return cudaErrorInvalidValue;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && attr < smem) {
-        cudaError_t e = cudaFuncSetAttribute(eq8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_dyn_smem((const void *)eq8_kernel, smem);
         if (e != cudaSuccess) return e;
-        attr = smem;
     }
     eq8_kernel<<<(a.frames + FR - 1) / FR, WPB * 32, smem, st>>>(a, spsT, sps2T, hpartT, n_tiles, bn);
     return cudaGetLastError();
 }
 
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
+    if (a.variant == 0 && dirichlet_ring_supported(a)) return launch_dirichlet_ring(a, st);
     const int SN = a.S * a.N;
     const PipeLayout L(a.S, a.N, a.Kt);
     if (a.variant == 1 && a.N % 4 == 0 && a.Kt % 4 == 0 && a.ld % 4 == 0) {
@@ -796,24 +793,11 @@ cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
             const int ki = (even ? 1 : 0) + (nw == 8 ? 2 : 0);
             auto kern = nw == 8 ? (even ? dirichlet_tile_kernel<true, 8> : dirichlet_tile_kernel<false, 8>)
                                 : (even ? dirichlet_tile_kernel<true, 4> : dirichlet_tile_kernel<false, 4>);
-            static size_t attr_t[4] = {0, 0, 0, 0};
-            if (smem > 48 * 1024 && attr_t[ki] < smem) {
-                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                if (e != cudaSuccess) return e;
-                attr_t[ki] = smem;
-            }
-            static int sms_t = 0, per_sm_t[4] = {0, 0, 0, 0};
-            static size_t per_sm_smem_t[4] = {0, 0, 0, 0};
-            if (!sms_t || per_sm_smem_t[ki] != smem) {
-                int dev = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&sms_t, cudaDevAttrMultiProcessorCount, dev);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t[ki], kern, nw * 32, smem);
-                if (per_sm_t[ki] < 1) per_sm_t[ki] = 1;
-                per_sm_smem_t[ki] = smem;
-            }
+            (void)ki;
+            cudaError_t e = ensure_dyn_smem((const void *)kern, smem);
+            if (e != cudaSuccess) return e;
             const long long need = (a.frames + FT - 1) / FT;
-            const long long cap = (long long)sms_t * per_sm_t[ki];
+            const long long cap = (long long)device_sms() * occupancy_ctas((const void *)kern, nw * 32, smem);
             const int grid = (int)(need < cap ? need : cap);
             kern<<<grid, nw * 32, smem, st>>>(a, FT);
             return cudaGetLastError();
@@ -832,24 +816,10 @@ cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
         const bool even = (a.K & 1) == 0;
         auto kern = nbuf == 1 ? (even ? dirichlet_pipe_kernel<true, 1> : dirichlet_pipe_kernel<false, 1>)
                               : (even ? dirichlet_pipe_kernel<true, 2> : dirichlet_pipe_kernel<false, 2>);
-        static size_t attr_p[2] = {0, 0};
-        if (smem > 48 * 1024 && attr_p[even] < smem) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            attr_p[even] = smem;
-        }
-        static int sms = 0, per_sm[2] = {0, 0};
-        static size_t per_sm_smem[2] = {0, 0};
-        if (!sms || per_sm_smem[even] != smem) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[even], kern, WPB * 32, smem);
-            if (per_sm[even] < 1) per_sm[even] = 1;
-            per_sm_smem[even] = smem;
-        }
+        cudaError_t e = ensure_dyn_smem((const void *)kern, smem);
+        if (e != cudaSuccess) return e;
         const long long need = (a.frames + WPB - 1) / WPB;
-        const long long cap = (long long)sms * per_sm[even];
+        const long long cap = (long long)device_sms() * occupancy_ctas((const void *)kern, WPB * 32, smem);
         const int grid = (int)(need < cap ? need : cap);
         kern<<<grid, WPB * 32, smem, st>>>(a);
         return cudaGetLastError();
@@ -857,11 +827,9 @@ cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st) {
     const size_t per_warp = (((size_t)SN * 8 + 15) & ~size_t(15)) + (((size_t)SN * 4 + 15) & ~size_t(15)) +
                             (((size_t)32 * a.K * 4 + 15) & ~size_t(15));
     const size_t smem = per_warp * WPB;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && attr < smem) {
-        cudaError_t e = cudaFuncSetAttribute(dirichlet_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_dyn_smem((const void *)dirichlet_kernel, smem);
         if (e != cudaSuccess) return e;
-        attr = smem;
     }
     dirichlet_kernel<<<(a.frames + WPB - 1) / WPB, WPB * 32, smem, st>>>(a);
     return cudaGetLastError();

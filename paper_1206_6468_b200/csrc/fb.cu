@@ -786,27 +786,19 @@ cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
     const size_t smem = ((size_t)2 * NMAX * NMAX + (size_t)C::WPB * (2 * NMAX + 2 * C::CH * N)) * sizeof(float);
     const bool chunked = a.nchunk > 1;
     auto kern = chunked ? fb_kernel<NMAX, true> : fb_kernel<NMAX, false>;
-    static size_t attr[2] = {0, 0};
-    if (smem > 48 * 1024 && attr[chunked] < smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_dyn_smem((const void *)kern, smem);
         if (e != cudaSuccess) return e;
-        attr[chunked] = smem;
     }
     if (chunked) {   // phases 1 and 2 of the parallel-in-time path (NMAX <= 64)
         if (NMAX > 64 || !a.P || !a.PT || !a.PE) return cudaErrorInvalidValue;
         const size_t sm1 = ((size_t)NMAX * NMAX + (size_t)a.chunk_len * NMAX + FBP_ROWS * 2 * NMAX) * sizeof(float);
         const size_t sm2 = ((size_t)2 * NMAX * NMAX +
                             2 * ((size_t)a.nchunk * NMAX + (size_t)FBP_RING * ScanSlot<NMAX>::FLOATS + 2 * NMAX)) * sizeof(float);
-        static size_t attr1 = 0, attr2 = 0;
-        if (sm1 > 48 * 1024 && attr1 < sm1) {
-            cudaError_t e = cudaFuncSetAttribute(fbp_transfer_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        {
+            cudaError_t e = ensure_dyn_smem((const void *)fbp_transfer_kernel<NMAX>, sm1);
+            if (e == cudaSuccess) e = ensure_dyn_smem((const void *)fbp_scan_kernel<NMAX>, sm2);
             if (e != cudaSuccess) return e;
-            attr1 = sm1;
-        }
-        if (sm2 > 48 * 1024 && attr2 < sm2) {
-            cudaError_t e = cudaFuncSetAttribute(fbp_scan_kernel<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-            if (e != cudaSuccess) return e;
-            attr2 = sm2;
         }
         const int rows_blocks = (NMAX + FBP_ROWS - 1) / FBP_ROWS;
         fbp_transfer_kernel<NMAX><<<dim3(a.nchunk * rows_blocks, a.M * a.S), FBP_ROWS * 32, sm1, st>>>(a, a.P, a.PT, a.PE);
@@ -831,6 +823,17 @@ int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len) {
     if (chains > 32 || N > 64 || T < 96) return 0;
     int L = 32;
     while (L * L < T / 2 && L < 128) L *= 2;
+    // phase 2 keeps every chunk's row scales in shared memory: grow the chunks until it fits (the
+    // template bucket NMAX of N as in launch_fb); past L = 4096 keep the sequential kernel
+    const int NMAX = N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : N <= 24 ? 24 : N <= 32 ? 32 : N <= 40 ? 40 : N <= 48 ? 48 : 64;
+    auto scan_smem = [&](int64_t nc) {
+        return ((int64_t)2 * NMAX * NMAX + 2 * (nc * NMAX + (int64_t)FBP_RING * (NMAX * NMAX + 2 * NMAX) + 2 * NMAX)) * 4;
+    };
+    // phase 1 stages one chunk of emissions: (NMAX^2 + L NMAX + 8 NMAX) floats
+    auto transfer_smem = [&](int64_t l) { return ((int64_t)NMAX * NMAX + l * NMAX + (int64_t)FBP_ROWS * 2 * NMAX) * 4; };
+    const int64_t limit = 227 * 1024;
+    while (scan_smem((T + L - 1) / L) > limit && L < 4096) L *= 2;
+    if (scan_smem((T + L - 1) / L) > limit || transfer_smem(L) > limit) return 0;
     *chunk_len = L;
     return (int)((T + L - 1) / L);
 }

@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(Cfg<NTC>::NT, Cfg<NTC>::MINB) recon_kernel(Rec
                         if (vv[j] > 0.f) {
                             if (vh > 0.f) {
                                 rr[j] = vv[j] / vh;
-                                part += (double)vv[j] * (double)logf(vh);
+                                part += rint((double)vv[j] * (double)logf(vh) * 1048576.0);   // 2^-20 nats (tc path)
                             } else {
                                 rr[j] = 0.f;
                                 bad |= FLAG_ZERO_SUPPORT;

@@ -661,7 +661,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             }
                             *px = make_float4(y[0], y[1], y[2], y[3]);
                         }
-                        part += 0.69314718055994530942 * (double)lsum;
+                        // fixed point (2^-20 nats, an integer-valued double): the per-row sums across
+                        // sub-tiles, warps and column tiles are then exact, so the data term of the bound
+                        // does not depend on the tile width (sharding invariance of L)
+                        part += rint(0.69314718055994530942 * 1048576.0 * (double)lsum);
                         fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
@@ -725,7 +728,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
 }
 
-int g_num_sms = 0;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 int stages_for(int bn, int ring_off = RING_OFF) {
@@ -757,22 +759,16 @@ cudaError_t make_map(CUtensorMap *m, const float *base, int64_t cols, int64_t ro
 // A [M][lda] (cols = lda); epilogue in / out [M][ldc]
 cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, float *eout, cudaStream_t st,
                       const float *dvT = nullptr) {
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int g_num_sms = device_sms();
     if (p.bn < 16 || p.bn > TC_MAX_BN || p.bn % 16 || p.stages < 2) return cudaErrorInvalidValue;
     if (p.ring_off == 0) p.ring_off = RING_OFF;
     const size_t smem = (size_t)p.ring_off + (size_t)p.stages * stage_bytes_of(p.bn);
     if (smem > SMEM_MAX) return cudaErrorInvalidValue;
     const bool fused = p.mode == TC_DIRICHLET;
     auto kern = fused ? tc_gemm_kernel<true> : tc_gemm_kernel<false>;
-    static bool attr[2] = {false, false};
-    if (!attr[fused]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    {
+        cudaError_t e = ensure_dyn_smem((const void *)kern, SMEM_MAX);
         if (e != cudaSuccess) return e;
-        attr[fused] = true;
     }
     CUtensorMap mA, mIn, mOut, mDv;
     cudaError_t e = make_map(&mA, A, lda, p.M, lda, TC_KB, TC_BM, CU_TENSOR_MAP_SWIZZLE_64B);

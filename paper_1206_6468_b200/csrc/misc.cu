@@ -3,6 +3,10 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "nfhmm_internal.cuh"
 
 namespace nfk {
@@ -22,15 +26,16 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 __global__ void __launch_bounds__(256) elbo_kernel(ElboArgs p) {
     __shared__ double scratch[8];
     __shared__ bool last_m;
-    const int m = blockIdx.y, nb = gridDim.x, b = blockIdx.x;
+    const int m = blockIdx.x, nb = gridDim.y, b = blockIdx.y;   // mixtures on x (no 65535 cap)
     const int iter = *p.iter_ctr;
     const int chunk = (p.T + nb - 1) / nb, t0 = b * chunk, t1 = min(p.T, t0 + chunk);
     double acc = 0.0;
     for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
         const size_t f = (size_t)m * p.T + t;
-        double v = p.hdir[f];
-        for (int c = 0; c < p.n_tiles; ++c) v += p.data_part[f * p.n_tiles + c];
-        acc += v;
+        // data term: integer-valued partials in units of 2^-20 nats (exact sum, any tiling)
+        double q = 0.0;
+        for (int c = 0; c < p.n_tiles; ++c) q += p.data_part[f * p.n_tiles + c];
+        acc += p.hdir[f] + q * (1.0 / 1048576.0);
     }
     acc = warp_sum_d(acc);
     if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = acc;
@@ -53,7 +58,7 @@ __global__ void __launch_bounds__(256) elbo_kernel(ElboArgs p) {
     if (iter < p.max_iters) p.fe[(size_t)m * p.max_iters + iter] = s;
     p.mix_ctr[m] = 0u;
     __threadfence();
-    if (atomicAdd(p.done_ctr, 1u) == gridDim.y - 1) {   // the last mixture advances the sweep counter
+    if (atomicAdd(p.done_ctr, 1u) == gridDim.x - 1) {   // the last mixture advances the sweep counter
         *p.done_ctr = 0u;
         *p.iter_ctr = iter + 1;
         __threadfence();
@@ -105,7 +110,8 @@ __global__ void transpose_kernel(const float *__restrict__ src, int rows, int co
 
 // v_t = sum_l V_lt (FP64 accumulation) and input checks (V >= 0, finite) -- one warp per frame.
 __global__ void obs_stats_kernel(const float *__restrict__ V, int frames, int F, int ld, float *vt, unsigned *flags) {
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (w >= frames) return;
     double s = 0.0;
     unsigned bad = 0;
@@ -146,7 +152,8 @@ __global__ void frame_consts_kernel(const float *__restrict__ vt, int frames, in
 }
 
 __global__ void sep_scale_kernel(const float *__restrict__ alpha, int frames, int Kt, int ld, const float *vt, float *scale) {
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (w >= frames) return;
     double s = 0.0;
     for (int k = lane; k < Kt; k += 32) s += (double)alpha[(size_t)w * ld + k];
@@ -184,7 +191,7 @@ int grid_for(size_t n, int block) {
 cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st) {
     int nb = (a.T + 255) / 256;
     nb = nb < 1 ? 1 : (nb > ELBO_MAX_BLOCKS ? ELBO_MAX_BLOCKS : nb);
-    elbo_kernel<<<dim3(nb, a.M), 256, 0, st>>>(a);
+    elbo_kernel<<<dim3(a.M, nb), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -213,7 +220,7 @@ cudaError_t launch_transpose(const float *src, int rows, int cols, int ld_src, f
 }
 
 cudaError_t launch_obs_stats(const float *V, int frames, int F, int ld, float *vt, unsigned *flags, cudaStream_t st) {
-    obs_stats_kernel<<<(frames * 32 + 255) / 256, 256, 0, st>>>(V, frames, F, ld, vt, flags);
+    obs_stats_kernel<<<(unsigned)(((long long)frames * 32 + 255) / 256), 256, 0, st>>>(V, frames, F, ld, vt, flags);
     return cudaGetLastError();
 }
 
@@ -225,7 +232,7 @@ cudaError_t launch_frame_consts(const float *vt, int frames, int Kt, double gamm
 
 cudaError_t launch_sep_scale(const float *alpha, int frames, int Kt, int ld, const float *vt, float *scale,
                              cudaStream_t st) {
-    sep_scale_kernel<<<(frames * 32 + 255) / 256, 256, 0, st>>>(alpha, frames, Kt, ld, vt, scale);
+    sep_scale_kernel<<<(unsigned)(((long long)frames * 32 + 255) / 256), 256, 0, st>>>(alpha, frames, Kt, ld, vt, scale);
     return cudaGetLastError();
 }
 
@@ -233,6 +240,51 @@ cudaError_t launch_wiener(const float *V, int ldv, const float *vsrc, float *vst
                           cudaStream_t st) {
     wiener_kernel<<<grid_for((size_t)M * T * F, 256), 256, 0, st>>>(V, ldv, vsrc, vstar, M, S, T, F);
     return cudaGetLastError();
+}
+
+namespace {
+std::mutex g_launch_mu;
+std::map<std::pair<const void *, int>, size_t> g_smem_attr;
+std::map<int, int> g_sms;
+std::map<std::tuple<const void *, int, int, size_t>, int> g_occ;
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+}  // namespace
+
+cudaError_t ensure_dyn_smem(const void *func, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    size_t &done = g_smem_attr[{func, dev}];
+    if (done >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done = bytes;
+    return e;
+}
+
+int device_sms() {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    int &n = g_sms[dev];
+    if (!n) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n < 1) n = 1;
+    }
+    return n;
+}
+
+int occupancy_ctas(const void *func, int threads, size_t smem) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    int &n = g_occ[std::make_tuple(func, dev, threads, smem)];
+    if (!n) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, func, threads, smem);
+        if (n < 1) n = 1;
+    }
+    return n;
 }
 
 }  // namespace nfk

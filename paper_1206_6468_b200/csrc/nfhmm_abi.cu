@@ -559,7 +559,7 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         h->nt_tc_b = (int)((Kt + h->bn_tc_b - 1) / h->bn_tc_b);
         h->ldf = (int)((frames + 31) / 32 * 32);
         const char *ed = getenv("NFHMM_DIRICHLET");
-        h->dir_variant = (ed && strcmp(ed, "tile") == 0) ? 1 : 0;
+        h->dir_variant = (ed && strcmp(ed, "tile") == 0) ? 1 : (ed && strcmp(ed, "pipe") == 0) ? 2 : 0;
         const char *ew = getenv("NFHMM_FB_WIDE");
         h->fb_wide = (ew && atoi(ew) == 0) ? 0 : 1;
         // Large batches (> 65,536 frames, sequential forward-backward): the reconstruction GEMM leaves 32

@@ -31,7 +31,8 @@ struct ReconArgs {
     int ldv;
     float *R;                 // [M][ldv] ratio out (RATIO)
     float *Vhat;              // optional [..][F] V_hat out (RATIO/STORE), row-major ld = F
-    double *data_part;        // [M][n_tiles] FP64 sum_l V log V_hat per (row, column tile) (RATIO)
+    double *data_part;        // [M][n_tiles] sum_l V log V_hat per (row, column tile) (RATIO), integer-valued
+                              // FP64 in units of 2^-20 nats (exact, tiling-independent sums)
     int n_tiles;
     const float *row_scale;   // SEPARATE: per-row v_t / alpha_0
     float *out_src;           // SEPARATE: V_src base for this source
@@ -100,10 +101,14 @@ struct DirichletArgs {
     double *eoff;             // [M][S][T]     out: gamma * max_n phi (FP64)
     double *hdir;             // [frames]      out: Dirichlet entropy terms of the bound (or NULL)
     int ldf;                  // fused path: frame pitch of the block-major arrays
-    int variant;              // 0: per-warp pipelined kernel; 1: frame-tile kernel (NFHMM_DIRICHLET=tile)
+    int variant;              // 0: ring kernel (dirichlet_ring.cu) where supported, else the per-warp pipelined
+                              // kernel; 1: frame-tile kernel (NFHMM_DIRICHLET=tile); 2: per-warp kernel (=pipe)
     unsigned *flags;
 };
 cudaError_t launch_dirichlet(const DirichletArgs &a, cudaStream_t st);
+// Round-2 default (dirichlet_ring.cu): persistent frame tiles with a two-stage bulk-copy ring
+bool dirichlet_ring_supported(const DirichletArgs &a);
+cudaError_t launch_dirichlet_ring(const DirichletArgs &a, cudaStream_t st);
 // Fused path: pseudo-counts before the back-projection GEMM, Eq. 8 / bound terms after it (dirichlet.cu)
 cudaError_t launch_dv(const DirichletArgs &a, float *dvT, cudaStream_t st);
 cudaError_t launch_eq8(const DirichletArgs &a, const double *spsT, const double *sps2T, const double *hpartT,
@@ -170,5 +175,13 @@ cudaError_t launch_sep_scale(const float *alpha, int frames, int Kt, int ld, con
 // V*^(s) = V V_src^(s) / sum_s' V_src^(s'), V_src layout [M][S][T][F]; writes V_star.
 cudaError_t launch_wiener(const float *V, int ldv, const float *vsrc, float *vstar, int M, int S, int T,
                           int F, cudaStream_t st);
+
+// Per-device launch state (the kernel attributes and SM counts are properties of a device, so a process
+// with handles on several devices must not share one cache): raise `func`'s dynamic shared-memory limit
+// to `bytes` on the current device (once per (kernel, device)); SM count and occupancy of the current
+// device (cached per (kernel, device, block size, smem)).
+cudaError_t ensure_dyn_smem(const void *func, size_t bytes);
+int device_sms();
+int occupancy_ctas(const void *func, int threads, size_t smem);
 
 }  // namespace nfk

@@ -299,11 +299,9 @@ cudaError_t launch_estep(int F, int T, int N, int K, int M, const float *V, cons
                          double *LL, float *C, cudaStream_t st) {
     const size_t smem = (size_t)K * F * 4;
     if (smem > 220 * 1024) return cudaErrorInvalidValue;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && attr < smem) {
-        cudaError_t e = cudaFuncSetAttribute(estep_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_dyn_smem((const void *)estep_kernel<KM>, smem);
         if (e != cudaSuccess) return e;
-        attr = smem;
     }
     estep_kernel<KM><<<dim3((T + ES_FT - 1) / ES_FT, N, M), 256, smem, st>>>(F, T, N, K, V, beta, theta, LL, C);
     return cudaGetLastError();
