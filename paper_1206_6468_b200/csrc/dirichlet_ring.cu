@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "dirichlet_math.cuh"
 #include "nfhmm_internal.cuh"
@@ -94,13 +96,22 @@ struct RingLayout {
 };
 
 // Element work of one (frame, block) item: KC = K at compile time (0: runtime K, any parity).
-// Returns the Eq. 8 sum of psi in FP64 and the item's g~ sum (without its exponent part, added here).
+// psi(a) = E ln 2 + ln m - r,  a = m 2^E (m in [1, 2)),  u = 1/a,  r = u/2 + u^2 G(u)  (G as a polynomial in
+// u, digamma_u_poly.cuh);  with w = u (-G) - 1/2:  -r = u w,
+//   theta = a e^{-psi_0} exp(-r),
+//   g~(a) = lnG(a) - (a-1) psi(a) + a = (E ln 2 + ln m)/2 + (ln(2 pi) + 1)/2 + u (H(u) + G - u G)
+//         = (E ln 2 + ln m)/2 + (ln(2 pi) + 1)/2 + u (H(u) - (-G) + w + 1/2)   [H(u) - 1/2 + (1 - u) G].
+// The item accumulates sum E (integer), sum log2 m, sum (-r) and sum u (H + G + w + 1/2 ...) in packed
+// FP32 and assembles the Eq. 8 block sum of psi in FP64 once.  Per element pair: LDS.64, exponent
+// (SHF + LEA.HI), mantissa (LOP3 x2), six SFU ops (lg2, rcp, ex2 per element), ~17 packed FP32 ops.
 template <int KC>
 __device__ __forceinline__ void item_elements(float *pn, int K, float dv, uint64_t e0_2, bool want_h, float *arow,
                                               double &psum, float &gsum) {
     const int KK = KC ? KC : K;
     const uint64_t dv2 = f2c(dv);
-    uint64_t q2 = 0ull, E2 = 0ull, g2 = 0ull;
+    const float gcoef[9] = DIG_GNU_COEF, hcoef[4] = LNG_HU_COEF;
+    uint64_t L2 = 0ull, Q2 = 0ull, Gs2 = 0ull;   // sum log2 m, sum (-r), sum of the u-terms of g~
+    int ebias = 0;                                // sum of the biased exponents (b >> 23)
 #pragma unroll
     for (int j = 0; j < KK; j += 2) {
         const bool two = KC ? true : (j + 1 < KK);
@@ -116,42 +127,35 @@ __device__ __forceinline__ void item_elements(float *pn, int K, float dv, uint64
         const uint64_t a2 = f2add(f2pack(n0, n1), dv2);
         float a0, a1;
         f2unpack(a2, a0, a1);
-        if (!two) a1 = 1.f;   // padding element: psi(1) etc. are discarded below
-        // psi(a) = E ln 2 + ln m - r,  r = u/2 + u^2 G(2u - 1),  u = 1/a,  a = m 2^E, m in [1, 2)
+        if (!two) a1 = 1.f;   // padding element: exponent 127, log2 m = 0, u = 1 -- its terms are masked below
         const uint32_t b0 = __float_as_uint(a0), b1 = __float_as_uint(a1);
-        float l0, l1;
+        ebias += (int)(b0 >> 23) + (int)(b1 >> 23);
+        float l0, l1;   // log2 of the mantissas
         asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0) : "f"(__uint_as_float((b0 & 0x007FFFFFu) | 0x3F800000u)));
         asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1) : "f"(__uint_as_float((b1 & 0x007FFFFFu) | 0x3F800000u)));
-        const uint64_t e2 = f2pack((float)((int)(b0 >> 23) - 127), two ? (float)((int)(b1 >> 23) - 127) : 0.f);
-        const uint64_t lm2 = f2mul(f2pack(l0, l1), f2c(0.693147180559945309f));   // ln m
-        const uint64_t u2 = f2pack(rcp_sfu(a0), rcp_sfu(a1));
-        const uint64_t t2 = f2fma(u2, f2c(2.f), f2c(-1.f));
-        const uint64_t G2 = dig_G2(t2);
-        const uint64_t uu2 = f2mul(u2, u2);
-        const uint64_t r2 = f2fma(uu2, G2, f2mul(u2, f2c(0.5f)));
-        uint64_t qd = f2sub(lm2, r2);                                                // ln m - r
+        float u0 = rcp_sfu(a0), u1 = rcp_sfu(a1);
+        if (!KC && !two) u1 = 0.f;                 // masks the padding element's -r and g~ terms
+        const uint64_t u2 = f2pack(u0, u1);
+        uint64_t Gn2 = f2c(gcoef[0]);              // -G(u), Horner in u
+#pragma unroll
+        for (int i = 1; i < 9; ++i) Gn2 = f2fma(Gn2, u2, f2c(gcoef[i]));
+        const uint64_t w2 = f2fma(u2, Gn2, f2c(-0.5f));                           // w = -u G - 1/2
+        const uint64_t rn2 = f2mul(u2, w2);                                       // -r
         float th0, th1;
-        {
+        {   // theta = a e^{-psi_0} exp(-r)
             float r0, r1;
-            f2unpack(f2mul(r2, f2c(-1.44269504088896341f)), r0, r1);
+            f2unpack(f2mul(rn2, f2c(1.44269504088896341f)), r0, r1);
             f2unpack(f2mul(f2mul(a2, e0_2), f2pack(ex2_sfu(r0), ex2_sfu(r1))), th0, th1);
         }
-        uint64_t gd = 0ull;
-        if (want_h) {   // g~ - (E ln 2)/2 = ln(m)/2 + ln(2 pi)/2 + 1/2 + u (H - 1/2) + (u - u^2) G
-            const uint64_t H2 = lng_H2(t2);
-            const uint64_t g0 = f2fma(f2c(0.5f), lm2, f2c(1.41893853320467274f));
-            gd = f2add(g0, f2fma(u2, f2sub(H2, f2c(0.5f)), f2mul(f2sub(u2, uu2), G2)));
+        Q2 = f2add(Q2, rn2);
+        L2 = f2add(L2, f2pack(l0, l1));            // (padding: log2 1 = 0)
+        if (want_h) {   // u (H(u) - 1/2 + (1 - u) G) = u (H + (-G)(u - 1) - 1/2) = u (H - (-G) + w + 1/2 ... )
+            uint64_t H2 = f2c(hcoef[0]);
+#pragma unroll
+            for (int i = 1; i < 4; ++i) H2 = f2fma(H2, u2, f2c(hcoef[i]));
+            const uint64_t d2 = f2add(f2sub(H2, Gn2), w2);                       // H - 1/2 + (1 - u) G
+            Gs2 = f2fma(u2, d2, Gs2);
         }
-        if (!two) {   // drop the padding element's share
-            float x0, x1;
-            f2unpack(qd, x0, x1);
-            qd = f2pack(x0, 0.f);
-            f2unpack(gd, x0, x1);
-            gd = f2pack(x0, 0.f);
-        }
-        q2 = f2add(q2, qd);
-        E2 = f2add(E2, e2);
-        g2 = f2add(g2, gd);
         if (KC) {
             *reinterpret_cast<float2 *>(pn + j) = make_float2(th0, th1);
             if (arow) *reinterpret_cast<float2 *>(arow + j) = make_float2(a0, a1);
@@ -164,32 +168,67 @@ __device__ __forceinline__ void item_elements(float *pn, int K, float dv, uint64
             }
         }
     }
-    float qx, qy, ex, ey, gx, gy;
-    f2unpack(q2, qx, qy);
-    f2unpack(E2, ex, ey);
-    f2unpack(g2, gx, gy);
-    const float esum = ex + ey;   // exact (integers < 2^24)
-    psum = (double)esum * 0.69314718055994530942 + (double)(qx + qy);
-    gsum = (gx + gy) + esum * 0.346573590279972655f;
+    // exponent part: sum E = sum (b >> 23) - 127 x (elements + padding element, whose E is 0)
+    const int npad = KC ? 0 : (KK & 1);
+    const float esum = (float)(ebias - 127 * (KK + npad));
+    float lx, ly, qx, qy, gx, gy;
+    f2unpack(L2, lx, ly);
+    f2unpack(Q2, qx, qy);
+    f2unpack(Gs2, gx, gy);
+    const float lsum = lx + ly;                    // sum log2 m
+    // sum psi = ln 2 (sum E + sum log2 m) + sum (-r)
+    psum = ((double)esum + (double)lsum) * 0.69314718055994530942 + (double)(qx + qy);
+    // sum g~ = (ln 2 / 2)(sum E + sum log2 m) + K (ln(2 pi) + 1)/2 + sum u (...)
+    gsum = (gx + gy) + (esum + lsum) * 0.346573590279972655f + (float)KK * 1.41893853320467274f;
 }
 
+constexpr int RING_IPT = 8;   // max (frame, block) items per thread and tile
+constexpr int RING_G = 8;     // lanes per (frame, source) group in the small-vector phases
+#ifndef RING_MAXREG
+#define RING_MAXREG 128   // register cap: ptxas otherwise settles at 64 registers and serialises the element
+                           // chains (config 3, 6-frame tiles: 0.98 -> 0.88 ms per launch with 112 registers)
+#endif
+
 template <int KC, int NT>
-__global__ void __launch_bounds__(NT) dirichlet_ring_kernel(DirichletArgs p, int FT) {
+__global__ void __maxnreg__(RING_MAXREG) dirichlet_ring_kernel(DirichletArgs p, int FT) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int S = p.S, N = p.N, SN = S * N, K = p.K, Kt = p.Kt, T = p.T;
+    constexpr int NW = NT / 32;
+    const int S = p.S, N = p.N, SN = S * N, K = KC ? KC : p.K, Kt = p.Kt, T = p.T, ld = p.ld;
+    const int frames = p.frames;
+    const float *__restrict__ n_in = p.n_in;
+    const float *__restrict__ u_fwd = p.u_fwd;
+    const float *__restrict__ b_bwd = p.b_bwd;
+    const double *__restrict__ fconst = p.fconst;
+    float *__restrict__ theta = p.theta;
+    float *__restrict__ alpha = p.alpha;
+    float *__restrict__ ec = p.ec;
+    double *__restrict__ eoffp = p.eoff;
+    double *__restrict__ hdir = p.hdir;
     const RingLayout L(S, N, Kt, FT);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + L.bars);
     double *sps = reinterpret_cast<double *>(smem_raw + L.sps);   // [FT][SN]
     float *hs = reinterpret_cast<float *>(smem_raw + L.hs);       // [FT][SN]
     float *gq = reinterpret_cast<float *>(smem_raw + L.gq);       // [FT][S] gamma / sum_n u b
-    float *mxs = reinterpret_cast<float *>(smem_raw + L.mx);      // [FT][S] Eq. 8 maxima
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int grp = lane / RING_G, g = lane % RING_G;             // (frame, source) group of 8 lanes
     const float gamma = p.gamma;
-    const bool want_h = p.hdir != nullptr, want_a = p.write_alpha != 0;
-    const float invSN = 1.f / (float)SN, invN = 1.f / (float)N, invS = 1.f / (float)S;
-    const int ntiles = (p.frames + FT - 1) / FT;
-    const bool contiguous = p.ld == Kt;
+    const bool want_h = hdir != nullptr, want_a = p.write_alpha != 0;
+    const int ntiles = (frames + FT - 1) / FT;
+    const bool contiguous = ld == Kt;
     unsigned bad = 0;
+    // this thread's first item (frame f, source s, state n) and the per-item stride NT in those digits
+    int f_1st, s_1st, n_1st, df, ds, dn;
+    {
+        const float invSN = 1.f / (float)SN, invN = 1.f / (float)N;
+        f_1st = divq(tid, SN, invSN);
+        const int b = tid - f_1st * SN;
+        s_1st = divq(b, N, invN);
+        n_1st = b - s_1st * N;
+        df = NT / SN;
+        const int db = NT - df * SN;
+        ds = db / N;
+        dn = db - ds * N;
+    }
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -202,24 +241,24 @@ __global__ void __launch_bounds__(NT) dirichlet_ring_kernel(DirichletArgs p, int
         float *nb = reinterpret_cast<float *>(sb + L.n);
         float *ub = reinterpret_cast<float *>(sb + L.u);
         float *bb = reinterpret_cast<float *>(sb + L.b);
-        const int f0 = tile * FT, nf = min(FT, p.frames - f0);
+        const int f0 = tile * FT, nf = min(FT, frames - f0);
         mbar_expect_tx(&bars[st], (uint32_t)nf * ((uint32_t)Kt * 4 + 8u * (uint32_t)SN + 32u));
         if (contiguous) {
-            bulk_g2s(nb, p.n_in + (size_t)f0 * Kt, (uint32_t)nf * Kt * 4, &bars[st]);
+            bulk_g2s(nb, n_in + (size_t)f0 * Kt, (uint32_t)nf * Kt * 4, &bars[st]);
         } else {
-            for (int f = 0; f < nf; ++f) bulk_g2s(nb + (size_t)f * Kt, p.n_in + (size_t)(f0 + f) * p.ld, Kt * 4, &bars[st]);
+            for (int f = 0; f < nf; ++f) bulk_g2s(nb + (size_t)f * Kt, n_in + (size_t)(f0 + f) * ld, Kt * 4, &bars[st]);
         }
         for (int f = f0; f < f0 + nf;) {   // runs of consecutive t inside one mixture
             const int m = f / T, t = f - m * T, len = min(f0 + nf - f, T - t);
             for (int s = 0; s < S; ++s) {
                 const size_t row = ((size_t)(m * S + s) * T + t) * N;
                 const size_t dst = ((size_t)s * FT + (f - f0)) * N;
-                bulk_g2s(ub + dst, p.u_fwd + row, (uint32_t)len * N * 4, &bars[st]);
-                bulk_g2s(bb + dst, p.b_bwd + row, (uint32_t)len * N * 4, &bars[st]);
+                bulk_g2s(ub + dst, u_fwd + row, (uint32_t)len * N * 4, &bars[st]);
+                bulk_g2s(bb + dst, b_bwd + row, (uint32_t)len * N * 4, &bars[st]);
             }
             f += len;
         }
-        bulk_g2s(sb + L.fc, p.fconst + 4 * (size_t)f0, (uint32_t)nf * 32, &bars[st]);
+        bulk_g2s(sb + L.fc, fconst + 4 * (size_t)f0, (uint32_t)nf * 32, &bars[st]);
     };
 
     int it = 0;
@@ -227,7 +266,7 @@ __global__ void __launch_bounds__(NT) dirichlet_ring_kernel(DirichletArgs p, int
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = it & 1;
         const uint32_t parity = (it >> 1) & 1;
-        const int f0 = tile * FT, nf = min(FT, p.frames - f0);
+        const int f0 = tile * FT, nf = min(FT, frames - f0), nitems = nf * SN, npairs = nf * S;
         unsigned char *sb = smem_raw + st * L.stage;
         float *nb = reinterpret_cast<float *>(sb + L.n);
         const float *ub = reinterpret_cast<const float *>(sb + L.u);
@@ -246,83 +285,97 @@ __global__ void __launch_bounds__(NT) dirichlet_ring_kernel(DirichletArgs p, int
         }
         mbar_wait(&bars[st], parity);
 
-        // Eq. 6 normalisers: gq[f][s] = gamma / sum_n u b  (one thread per (frame, source))
-        for (int k = tid; k < nf * S; k += NT) {
-            const int f = divq(k, S, invS), s = k - f * S;
-            const float *u = ub + ((size_t)s * FT + f) * N, *b = bb + ((size_t)s * FT + f) * N;
-            float q0 = 0.f, q1 = 0.f;
-            int n = 0;
-            for (; n + 1 < N; n += 2) {
-                q0 = fmaf(u[n], b[n], q0);
-                q1 = fmaf(u[n + 1], b[n + 1], q1);
+        // Eq. 6 normalisers gq[f][s] = gamma / sum_n u b: 8 lanes per (frame, source), fixed-order sums
+        for (int pb = warp * (32 / RING_G); pb < npairs; pb += NW * (32 / RING_G)) {
+            const int pr = pb + grp;
+            float q = 0.f;
+            if (pr < npairs) {
+                const int f = pr / S, s = pr - f * S;
+                const float *u = ub + ((size_t)s * FT + f) * N, *b = bb + ((size_t)s * FT + f) * N;
+                for (int n = g; n < N; n += RING_G) q = fmaf(u[n], b[n], q);
             }
-            if (n < N) q0 = fmaf(u[n], b[n], q0);
-            const float q = q0 + q1;
-            if (!(q > 0.f) || !(q < INFINITY)) bad |= FLAG_NONFINITE;
-            gq[k] = gamma * __frcp_rn(q);
+            q += __shfl_xor_sync(0xffffffffu, q, 4);
+            q += __shfl_xor_sync(0xffffffffu, q, 2);
+            q += __shfl_xor_sync(0xffffffffu, q, 1);
+            if (pr < npairs && g == 0) {
+                if (!(q > 0.f) || !(q < INFINITY)) bad |= FLAG_NONFINITE;
+                gq[pr] = gamma * __frcp_rn(q);
+            }
         }
         __syncthreads();
 
         // element pass: one thread per (frame, block) item; theta replaces n in the stage buffer
-        for (int i = tid; i < nf * SN; i += NT) {
-            const int f = divq(i, SN, invSN), b = i - f * SN;
-            const int s = divq(b, N, invN), n = b - s * N;
-            const size_t ui = ((size_t)s * FT + f) * N + n;
-            const float dv = fmaf(gq[f * S + s], ub[ui] * bb[ui], 1.f);
-            const uint64_t e0_2 = f2c((float)fc[4 * f + 3]);
-            float *arow = want_a ? p.alpha + (size_t)(f0 + f) * p.ld + b * K : nullptr;
-            double ps;
-            float gs;
-            item_elements<KC>(nb + (size_t)f * Kt + b * K, K, dv, e0_2, want_h, arow, ps, gs);
-            sps[i] = ps;
-            hs[i] = gs;
+        {
+            int f = f_1st, s = s_1st, n = n_1st;
+#pragma unroll 1
+            for (int i = tid; i < nitems; i += NT) {
+                const int b = s * N + n;
+                const int ui = (s * FT + f) * N + n;
+                const float dv = fmaf(gq[f * S + s], ub[ui] * bb[ui], 1.f);
+                const uint64_t e0_2 = f2c((float)fc[4 * f + 3]);
+                float *arow = want_a ? alpha + (size_t)(f0 + f) * ld + b * K : nullptr;
+                double ps;
+                float gs;
+                item_elements<KC>(nb + (size_t)f * Kt + b * K, K, dv, e0_2, want_h, arow, ps, gs);
+                sps[i] = ps;
+                hs[i] = gs;
+                // next item i + NT in (frame, source, state) digits
+                n += dn;
+                const int cn = n >= N;
+                n -= cn ? N : 0;
+                s += ds + cn;
+                const int cs = s >= S;
+                s -= cs ? S : 0;
+                f += df + cs;
+            }
         }
         fence_async_smem();   // theta (generic writes) before the bulk store (async proxy) reads it
         __syncthreads();
         if (tid == 0) {
             if (contiguous) {
-                bulk_s2g(p.theta + (size_t)f0 * Kt, nb, (uint32_t)nf * Kt * 4);
+                bulk_s2g(theta + (size_t)f0 * Kt, nb, (uint32_t)nf * Kt * 4);
             } else {
-                for (int f = 0; f < nf; ++f) bulk_s2g(p.theta + (size_t)(f0 + f) * p.ld, nb + (size_t)f * Kt, Kt * 4);
+                for (int f = 0; f < nf; ++f) bulk_s2g(theta + (size_t)(f0 + f) * ld, nb + (size_t)f * Kt, Kt * 4);
             }
             bulk_commit();
         }
-        // Eq. 8 maxima and offsets, one thread per (frame, source); the bound term, one warp per frame
-        for (int k = tid; k < nf * S; k += NT) {
-            const int f = divq(k, S, invS), s = k - f * S;
+        // Eq. 8 per (frame, source), 8 lanes each: max over n (FP32 of the FP64 sums), offset eoff, and the
+        // centred emissions e = exp(gamma (phi - max)) in (0, 1]
+        for (int pb = warp * (32 / RING_G); pb < npairs; pb += NW * (32 / RING_G)) {
+            const int pr = pb + grp;
+            const bool ok = pr < npairs;
+            const int f = ok ? pr / S : 0, s = pr - f * S;
             const double *v = sps + (size_t)f * SN + s * N;
-            float m0 = -INFINITY, m1 = -INFINITY;
-            int n = 0;
-            for (; n + 1 < N; n += 2) {
-                m0 = fmaxf(m0, (float)v[n]);
-                m1 = fmaxf(m1, (float)v[n + 1]);
+            float mxf = -INFINITY;
+            if (ok)
+                for (int n = g; n < N; n += RING_G) mxf = fmaxf(mxf, (float)v[n]);
+            mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, 4));
+            mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, 2));
+            mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, 1));
+            if (ok) {
+                const int fg = f0 + f, m = fg / T, t = fg - m * T;
+                const double mx = (double)mxf;
+                float *dst = ec + ((size_t)(m * S + s) * T + t) * N;
+                for (int n = g; n < N; n += RING_G)
+                    dst[n] = ex2_sfu((float)((double)gamma * (v[n] - mx)) * 1.44269504088896341f);
+                if (g == 0) {
+                    const double off = (double)gamma * (mx - (double)K * fc[4 * f + 1]);
+                    eoffp[(size_t)(m * S + s) * T + t] = off;
+                    if (!isfinite(off)) bad |= FLAG_NONFINITE;
+                }
             }
-            if (n < N) m0 = fmaxf(m0, (float)v[n]);
-            const float mxf = fmaxf(m0, m1);
-            mxs[k] = mxf;
-            const int fg = f0 + f, m = fg / T, t = fg - m * T;
-            const double off = (double)gamma * ((double)mxf - (double)K * fc[4 * f + 1]);
-            p.eoff[(size_t)(m * S + s) * T + t] = off;
-            if (!isfinite(off)) bad |= FLAG_NONFINITE;
         }
-        if (want_h) {
-            for (int f = warp; f < nf; f += NT / 32) {
+        if (want_h) {   // bound term per frame, 8 lanes each (fixed order)
+            for (int fb = warp * (32 / RING_G); fb < nf; fb += NW * (32 / RING_G)) {
+                const int f = fb + grp;
                 float h = 0.f;
-                for (int b = lane; b < SN; b += 32) h += hs[(size_t)f * SN + b];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-                if (lane == 0) p.hdir[f0 + f] = (double)h + fc[4 * f + 2];
+                if (f < nf)
+                    for (int b = g; b < SN; b += RING_G) h += hs[(size_t)f * SN + b];
+                h += __shfl_xor_sync(0xffffffffu, h, 4);
+                h += __shfl_xor_sync(0xffffffffu, h, 2);
+                h += __shfl_xor_sync(0xffffffffu, h, 1);
+                if (f < nf && g == 0) hdir[f0 + f] = (double)h + fc[4 * f + 2];
             }
-        }
-        __syncthreads();
-        // emissions e = exp(gamma (phi - max)) in (0, 1], one thread per (frame, block)
-        for (int i = tid; i < nf * SN; i += NT) {
-            const int f = divq(i, SN, invSN), b = i - f * SN;
-            const int s = divq(b, N, invN), n = b - s * N;
-            const int fg = f0 + f, m = fg / T, t = fg - m * T;
-            const double mx = (double)mxs[f * S + s];
-            p.ec[((size_t)(m * S + s) * T + t) * N + n] =
-                ex2_sfu((float)((double)gamma * (sps[i] - mx)) * 1.44269504088896341f);
         }
     }
     if (tid == 0) bulk_wait0();   // the last theta store has landed before the kernel retires
@@ -336,24 +389,30 @@ struct RingPick {
 // Tile shape: FT frames x (threads) with FT*S*N a multiple of the thread count (equal items per thread),
 // a stage of at most ~40 KB (two stages + sums: three CTAs per SM) or, for long rows, one frame per stage.
 RingPick ring_pick(int S, int N, int Kt) {
+    // model (fitted to the round-2 tile sweep at config 3): throughput ~ lane utilisation of the element
+    // pass x resident warps (up to 16 per SM; ~112 registers per thread, so registers cap the CTAs too)
+    // (measured at config 3, ms per launch: 6 frames x 128 threads 0.88, 8 x 128 0.89, 8 x 160 0.92,
+    // 4 x 128 1.06, 6 x 192 1.28)
     const int SN = S * N;
     RingPick best{0, 0};
     double best_score = -1.0;
-    for (int nt = 128; nt <= 256; nt += 32) {
-        for (int FT = 1; FT <= 64; ++FT) {
+    if (S > 255 || N > 65535) return best;
+    for (int nt = 128; nt <= 160; nt += 32) {   // (192+ threads measured slower at every tile size)
+        for (int FT = 1; FT <= 255; ++FT) {
             const RingLayout L(S, N, Kt, FT);
-            if (L.total > 110 * 1024) break;
+            if (L.total > 200 * 1024) break;
             const int items = FT * SN;
             const int per = (items + nt - 1) / nt;
-            const double eff = (double)items / ((double)per * nt);   // lane utilisation of the element pass
-            const int ctas = (int)((227 * 1024) / (L.total + 1024));
-            const int warps = ctas * nt / 32 > 64 ? 64 : ctas * nt / 32;
+            if (per > RING_IPT) break;
+            const double eff = (double)items / ((double)per * nt);
+            int ctas = (int)((227 * 1024) / (L.total + 1024));
+            const int ctas_reg = 65536 / (RING_MAXREG * nt);
+            if (ctas > ctas_reg) ctas = ctas_reg;
             if (ctas < 1) continue;
-            // prefer full lanes, then resident warps per SM (latency hiding of the element chains), then
-            // bigger tiles (fewer barriers per frame)
-            const double score = eff * 100.0 + 0.5 * (warps < 24 ? warps : 24) + (FT >= 4 ? 1.0 : 0.25 * FT) +
-                                 (ctas >= 2 ? 2.0 : 0.0);
-            if (score > best_score + 1e-9) {
+            const int warps = ctas * nt / 32;
+            // (1 + 0.15 / FT): the per-tile phases, barriers and copy issue amortised over the tile's frames
+            const double score = eff * (warps >= 16 ? 1.0 : warps / 16.0) / (1.0 + 0.15 / FT) * (nt == 128 ? 1.0 : 0.97);
+            if (score > best_score + 1e-9) {   // ties: the first (fewest threads)
                 best_score = score;
                 best = {FT, nt};
             }
@@ -396,7 +455,13 @@ bool dirichlet_ring_supported(const DirichletArgs &a) {
 }
 
 cudaError_t launch_dirichlet_ring(const DirichletArgs &a, cudaStream_t st) {
-    const RingPick pk = ring_pick(a.S, a.N, a.Kt);
+    RingPick pk = ring_pick(a.S, a.N, a.Kt);
+    if (const char *e = getenv("NFHMM_DIR_RING")) {   // "FT,threads": tile-shape experiments
+        int ft = 0, nt = 0;
+        if (sscanf(e, "%d,%d", &ft, &nt) == 2 && ft >= 1 && ft <= 255 && nt >= 128 && nt <= 256 && nt % 32 == 0 &&
+            RingLayout(a.S, a.N, a.Kt, ft).total <= 200 * 1024 && (ft * a.S * a.N + nt - 1) / nt <= RING_IPT)
+            pk = {ft, nt};
+    }
     if (pk.FT < 1) return cudaErrorInvalidValue;
     if (a.K == 10) return launch_ring_k<10>(a, pk.FT, pk.nt, st);
     if (a.K == 20) return launch_ring_k<20>(a, pk.FT, pk.nt, st);

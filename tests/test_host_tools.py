@@ -62,3 +62,27 @@ def test_lngamma_remainder_and_gtilde():
     gt = 0.5 * np.log(x) + 0.5 * np.log(2 * np.pi) + 0.5 + u * (Hv - 0.5) + (u - u * u) * Gv
     ref = gammaln(x) - (x - 1) * digamma(x) + x
     assert np.max(np.abs(gt - ref)) < 1e-6
+
+
+def _table(name, text):
+    import re
+    line = next(l for l in text.splitlines() if l.startswith(f"#define {name} "))
+    return np.array([float(v.rstrip("f")) for v in re.findall(r"[-+]?\d\.\d+e[-+]\d+f", line)], dtype=np.float32)
+
+
+def test_psi_u_form_float32_accuracy():
+    """The round-2 Dirichlet kernel's form: psi(x) = E ln 2 + ln m - r, r = u/2 + u^2 G(u) with G as a
+    polynomial in u (DIG_GNU_COEF = -G, highest degree first), evaluated in float32."""
+    txt = open(HDR).read()
+    Gn = _table("DIG_GNU_COEF", txt)
+    x = np.concatenate([np.linspace(1, 20, 100001), np.geomspace(20, 1e6, 100001)]).astype(np.float32)
+    u = (np.float32(1) / x).astype(np.float32)
+    r = np.float32(Gn[0]) * np.ones_like(u)
+    for c in Gn[1:]:
+        r = (r * u + np.float32(c)).astype(np.float32)
+    w = (u * r + np.float32(-0.5)).astype(np.float32)          # w' = u (-G) - 1/2
+    rn = (u * w).astype(np.float32)                             # -r
+    m, e = np.frexp(x.astype(np.float64))                       # x = m 2^e, m in [0.5, 1)
+    lnm = np.log((2 * m).astype(np.float32)).astype(np.float32)
+    psi = (e - 1) * np.log(2.0) + lnm.astype(np.float64) + rn.astype(np.float64)
+    assert np.max(np.abs(psi - digamma(x.astype(np.float64)))) <= 4e-7
