@@ -816,6 +816,228 @@ cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------------------------
+// Many chains per source (batched configurations): C chains of ONE source and ONE direction per warp,
+// sharing that source's A in registers.  For N = 32 Q + R (R = 32 / C, e.g. N = 40 = 32 + 8 with C = 4):
+// lane l owns state l of every chain in each full round q < Q, and state 32 Q + l % R of chain l / R in
+// the remainder round, so the remainder's lanes are not idle (the one-chain kernel leaves 24 of 32 lanes
+// idle in its second round at N = 40).  A step: the C previous messages are broadcast through shared
+// memory (LDS.128), each lane forms its Q C + 1 dot products with packed FFMA2 (C Q + 1 independent
+// chains -- the latency is hidden by the other chains instead of by split accumulators), the scale
+// 2^-E of each chain comes from the sum of that chain's broadcast vector (computed by its remainder lane
+// group, shared by a shuffle), and the outputs are multiplied by the emissions (forward) or turned into
+// the next step's e .* b (backward).  Same recursions and scaling as fb_kernel:
+//   u_0 = pi .* e_0,  u_t = ((u_{t-1} A) .* e_t) 2^-E(sum u_{t-1});
+//   b_{T-1} = 1,  b_t = (A (e_{t+1} .* b_{t+1})) 2^-E(sum e_{t+1} .* b_{t+1});
+//   log Z = ln(sum u_{T-1}) + ln 2 sum_t E_t + sum_t eoff_t.
+// The emissions of the next FBM_D steps (all C chains) are staged in a per-warp cp.async ring.
+constexpr int FBM_D = 8;   // emission ring depth (steps)
+
+template <int Q, int R>
+struct FBMCfg {
+    static constexpr int C = 32 / R;          // chains per warp
+    static constexpr int NM = 32 * Q + R;     // states
+    static constexpr int SLOT = C * NM;       // floats per emission slot (one step, all chains)
+    static constexpr int SMEM = (2 * C * NM + FBM_D * SLOT) * 4;   // per warp: 2 broadcast buffers + ring
+    static_assert(NM % 4 == 0, "states must be a multiple of 4");
+};
+
+template <int Q, int R>
+__global__ void __launch_bounds__(32) fb_multi_kernel(FBArgs p) {
+    using C_ = FBMCfg<Q, R>;
+    constexpr int C = C_::C, NM = C_::NM, SLOT = C_::SLOT;
+    constexpr int CHUNKS = SLOT / 4, CPL = (CHUNKS + 31) / 32;   // 16-byte emission chunks per step, per lane
+    extern __shared__ __align__(16) float sm[];
+    float *xb = sm;                          // [2][C][NM] broadcast messages
+    float *ring = sm + 2 * C * NM;           // [FBM_D][C][NM] emissions
+    const int lane = threadIdx.x;
+    const int groups = (p.M + C - 1) / C;
+    const int s = blockIdx.x / (2 * groups), rem = blockIdx.x - s * 2 * groups;
+    const bool backward = rem >= groups;
+    const int grp0 = backward ? rem - groups : rem;
+    const int m0 = grp0 * C;
+    const int T = p.T, N = NM;
+    const int g = lane / R, jr = 32 * Q + lane % R;   // remainder round: chain g, state jr
+    const float *Ag = p.trans + (size_t)s * N * N;
+    // A in registers: forward u A -> column j; backward A x -> row j (pairs over the input index)
+    uint64_t Mq[Q > 0 ? Q : 1][NM / 2], Mr[NM / 2];
+#pragma unroll
+    for (int i = 0; i < NM; i += 2) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int j = 32 * q + lane;
+            Mq[q][i / 2] = backward ? pk2(Ag[j * N + i], Ag[j * N + i + 1]) : pk2(Ag[i * N + j], Ag[(i + 1) * N + j]);
+        }
+        Mr[i / 2] = backward ? pk2(Ag[jr * N + i], Ag[jr * N + i + 1]) : pk2(Ag[i * N + jr], Ag[(i + 1) * N + jr]);
+    }
+    // per-chain message rows (chains past M write nothing; they compute on a valid chain's emissions)
+    const int cm = p.M - 1 - m0;             // last valid chain index in the group
+    float *outp = backward ? p.bwd : p.fwd;
+    float *orow[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) orow[c] = outp + ((size_t)(m0 + (c <= cm ? c : cm)) * p.S + s) * T * N;
+    const bool gv = g <= cm;
+    float *grow = orow[0];   // chain g's row (selected without indexing the register array)
+#pragma unroll
+    for (int c = 1; c < C; ++c)
+        if (c == g) grow = orow[c];
+    // emission staging: this lane's chunks (chain, 16-byte offset), source rows advanced by one step each
+    const float *esrc[CPL];
+    unsigned edst[CPL];
+    bool eok[CPL];
+#pragma unroll
+    for (int u = 0; u < CPL; ++u) {
+        const int k = lane + 32 * u;
+        eok[u] = k < CHUNKS;
+        const int c = eok[u] ? k / (NM / 4) : 0, o = eok[u] ? k - c * (NM / 4) : 0;
+        const int cc = c <= cm ? c : cm;
+        esrc[u] = p.ec + ((size_t)(m0 + cc) * p.S + s) * T * N + 4 * o;
+        edst[u] = (unsigned)__cvta_generic_to_shared(ring + c * NM + 4 * o);
+    }
+    auto stage = [&](int t) {
+        const unsigned slot = (unsigned)((t % FBM_D) * SLOT * 4);
+#pragma unroll
+        for (int u = 0; u < CPL; ++u)
+            if (eok[u]) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(edst[u] + slot), "l"(esrc[u] + (size_t)t * N));
+        cp_async_commit();
+    };
+    unsigned bad = 0;
+    const int t_first = backward ? T - 1 : 0, dt = backward ? -1 : 1;
+    for (int k = 0; k < FBM_D - 1; ++k) {
+        const int t = t_first + dt * k;
+        if (t >= 0 && t < T) stage(t);
+        else cp_async_commit();
+    }
+    int esum = 0;            // (forward) exponent sum of chain g (the remainder group's chain)
+    float vq[Q > 0 ? Q : 1][C], vr = 0.f;   // this lane's current outputs
+    int t = t_first;
+    for (int k = 0; k < T; ++k, t += dt) {
+        {   // keep FBM_D - 1 steps in flight
+            const int tn = t + dt * (FBM_D - 1);
+            if (tn >= 0 && tn < T) stage(tn);
+            else cp_async_commit();
+        }
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(FBM_D - 1));
+        __syncwarp();
+        const float *et = ring + (t % FBM_D) * SLOT;
+        float *xo = xb + (k & 1) * C * NM;          // this step's outputs (broadcast for the next step)
+        float eq[Q > 0 ? Q : 1][C], er;
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) eq[q][c] = et[c * NM + 32 * q + lane];
+        er = et[g * NM + jr];
+        if (k == 0) {
+            if (!backward) {   // u_0 = pi .* e_0 (unscaled)
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) vq[q][c] = p.prior[s * N + 32 * q + lane] * eq[q][c];
+                vr = p.prior[s * N + jr] * er;
+            } else {           // b_{T-1} = 1
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) vq[q][c] = 1.f;
+                vr = 1.f;
+            }
+        } else {
+            const float *xi = xb + ((k - 1) & 1) * C * NM;   // previous step's broadcast vectors
+            uint64_t aq[Q > 0 ? Q : 1][C], ar = 0ull, xs2[2] = {0ull, 0ull};
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) aq[q][c] = 0ull;
+#pragma unroll
+            for (int i4 = 0; i4 < NM / 4; ++i4) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    if (Q == 0) break;
+                    const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(xi + c * NM)[i4];
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        fma2(aq[q][c], v.x, Mq[q][2 * i4]);
+                        fma2(aq[q][c], v.y, Mq[q][2 * i4 + 1]);
+                    }
+                }
+                const ulonglong2 w = reinterpret_cast<const ulonglong2 *>(xi + g * NM)[i4];
+                fma2(ar, w.x, Mr[2 * i4]);
+                fma2(ar, w.y, Mr[2 * i4 + 1]);
+                add2(xs2[0], w.x);
+                add2(xs2[1], w.y);
+            }
+            add2(xs2[0], xs2[1]);
+            const float xsum = hsum2(xs2[0]);          // sum of chain g's broadcast vector
+            if (gv && (!(xsum > 0.f) || !(xsum < INFINITY))) bad |= FLAG_NONFINITE;
+            const int E = exponent_of(xsum);
+            if (!backward) esum += E;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if (Q == 0) break;
+                const float sc = pow2_neg(__shfl_sync(0xffffffffu, E, c * R));
+#pragma unroll
+                for (int q = 0; q < Q; ++q) vq[q][c] = hsum2(aq[q][c]) * sc;
+            }
+            vr = hsum2(ar) * pow2_neg(E);
+            if (!backward) {   // u_t = (u_{t-1} A) .* e_t  2^-E
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) vq[q][c] *= eq[q][c];
+                vr *= er;
+            }
+        }
+        // store the messages (u_t or b_t) and publish the next broadcast vector (u_t, or e_t .* b_t)
+        const int to = t * N;
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if (c <= cm) orow[c][to + 32 * q + lane] = vq[q][c];
+                xo[c * NM + 32 * q + lane] = backward ? vq[q][c] * eq[q][c] : vq[q][c];
+            }
+        if (gv) grow[to + jr] = vr;
+        xo[g * NM + jr] = backward ? vr * er : vr;
+        __syncwarp();
+    }
+    cp_async_wait_all();
+    if (!backward) {   // log Z of chain g (its R lanes agree): ln(sum u_{T-1}) + ln 2 sum E + sum eoff
+        const float *xl = xb + ((T - 1) & 1) * C * NM + g * NM;
+        float us = 0.f;
+        for (int i = lane % R; i < NM; i += R) us += xl[i];
+        double off = 0.0;
+        const size_t chain = (size_t)(m0 + (gv ? g : 0)) * p.S + s;
+        if (gv)
+            for (int tt = lane % R; tt < T; tt += R) off += p.eoff[chain * T + tt];
+#pragma unroll
+        for (int o = R / 2; o > 0; o >>= 1) {
+            us += __shfl_xor_sync(0xffffffffu, us, o);
+            off += __shfl_xor_sync(0xffffffffu, off, o);
+        }
+        if (gv && lane % R == 0) {
+            if (!(us > 0.f) || !(us < INFINITY)) bad |= FLAG_NONFINITE;
+            const double lz = log((double)us) + (double)esum * 0.69314718055994530942 + off;
+            p.logZ[chain] = lz;
+            if (!isfinite(lz)) bad |= FLAG_NONFINITE;
+        }
+    }
+    if (bad) atomicOr(p.flags, bad);
+}
+
+template <int Q, int R>
+cudaError_t launch_fb_multi(const FBArgs &a, cudaStream_t st) {
+    using C_ = FBMCfg<Q, R>;
+    const int groups = (a.M + C_::C - 1) / C_::C;
+    cudaError_t e = ensure_dyn_smem((const void *)fb_multi_kernel<Q, R>, C_::SMEM);
+    if (e != cudaSuccess) return e;
+    fb_multi_kernel<Q, R><<<a.S * 2 * groups, 32, C_::SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+
+bool fb_multi_supported(int N, int64_t M, int nchunk) {
+    return nchunk <= 1 && M >= 2 && (N == 40 || N == 36 || N == 48 || N == 8 || N == 4 || N == 16);
+}
+
 int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len) {
     // Parallel in time only while the sequential recursion would leave most of the GPU idle (at most
     // 32 chains -- e.g. single-mixture configurations), for N <= 64 (phase-2 smem) and long enough sequences.  Chunk length ~ sqrt(T): phase 1
@@ -840,6 +1062,15 @@ int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len) {
 
 cudaError_t launch_fb(const FBArgs &a, cudaStream_t st) {
     const int N = a.N;
+    // many chains per source: C chains per warp with the remainder states spread over the lanes
+    if (a.multi && fb_multi_supported(N, a.M, a.nchunk)) {
+        if (N == 40) return launch_fb_multi<1, 8>(a, st);
+        if (N == 36) return launch_fb_multi<1, 4>(a, st);
+        if (N == 48) return launch_fb_multi<1, 16>(a, st);
+        if (N == 8) return launch_fb_multi<0, 8>(a, st);
+        if (N == 4) return launch_fb_multi<0, 4>(a, st);
+        if (N == 16) return launch_fb_multi<0, 16>(a, st);
+    }
     if (a.wide == 2 && a.nchunk <= 1 && N > 32 && N <= 64) {   // experiment: multi-warp kernel for few chains
         if (N <= 40) return launch_fb_wide<40>(a, st);
         if (N <= 64) return launch_fb_wide<64>(a, st);

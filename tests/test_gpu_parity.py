@@ -260,3 +260,24 @@ def test_fb_overlap_is_bitwise_neutral(graphs, monkeypatch):
     seq = run_gpu(cfg, model, V, 3, separate=False)
     for key in ("d_hat", "alpha_hat", "V_hat", "free_energy"):
         assert np.array_equal(ov[key], seq[key]), key
+
+
+@pytest.mark.parametrize("c,over", [(3, dict(T=40, M=21)), (0, dict(T=60, M=20)), (2, dict(T=30, M=13))])
+def test_multi_chain_forward_backward(c, over, monkeypatch):
+    """> 32 chains: the multi-chain forward-backward (C chains of one source per warp, the N = 32 Q + R
+    remainder states spread over the lanes; M not a multiple of C leaves a partly empty group) agrees
+    with the one-chain-per-warp kernel and with the oracle."""
+    cfg, model, V = make_inputs(c, **over)
+    multi = run_gpu(cfg, model, V, 4)
+    monkeypatch.setenv("NFHMM_FB_MULTI", "0")
+    one = run_gpu(cfg, model, V, 4)
+    for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
+        assert rel_l2(multi[key], one[key]) <= 2e-6, key
+    assert np.all(np.abs(multi["free_energy"] - one["free_energy"]) <= 1e-7 * np.abs(one["free_energy"]))
+    for m in (0, V.shape[0] - 1):
+        o1 = run_oracle(cfg, model, V[m], 1, separate=False)
+        g1 = run_gpu(cfg, model, V, 1, separate=False) if m == 0 else g1
+        compare(f"multi-fb:{cfg.name}:M{V.shape[0]}/m{m}/sweep1", "d_hat", g1["d_hat"][m], o1["d_hat"], TOL1)
+        o = run_oracle(cfg, model, V[m], 4)
+        assert rel_l2(multi["V_star"][m], o["V_star"]) <= TOL_VSTAR
+        assert np.all(np.abs(multi["free_energy"][m] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
