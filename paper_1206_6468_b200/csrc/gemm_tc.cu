@@ -65,7 +65,7 @@ constexpr int A_STAGE_COLS = 2 * TC_KB;    // TMEM columns of one A stage: [hi 1
 constexpr int A_TILE_BYTES = TC_BM * TC_KB * 4;   // 8 KB smem copy of one A stage (TMA, 64-byte swizzle)
 constexpr int EPI_SUB_BYTES = 32 * 16 * 4;        // 2 KB epilogue sub-tile: 32 rows x 16 columns (TMA, 64-byte swizzle)
 constexpr int EPI_TILE_BYTES = 2 * EPI_SUB_BYTES; // per 32-column chunk
-constexpr int MAX_STAGES = 8;
+constexpr int MAX_STAGES = 16;            // ring depth cap (narrow tiles: more stages in flight, see stages_for)
 constexpr int A_PREFETCH = 16;             // stages ahead at which the producer pulls A tiles into L2
 constexpr int XCH_OFF = 1024;                                      // [3][128] FP64 row partials
 constexpr int EPI_OFF = 4096;                                      // epilogue tiles [12][4 KB]
@@ -235,7 +235,7 @@ __device__ __forceinline__ void tmem_add16(uint32_t taddr, float (&acc)[32]) {
     for (int i = 0; i < 16; ++i) acc[i] += __uint_as_float(r[i]);
 }
 
-enum TcMode : int { TC_RATIO = 0, TC_STORE = 1, TC_SEPARATE = 2, TC_BACKPROJ = 3, TC_DIRICHLET = 4 };
+enum TcMode : int { TC_RATIO = 0, TC_STORE = 1, TC_SEPARATE = 2, TC_BACKPROJ = 3, TC_DIRICHLET = 4, TC_PARTIAL = 5 };
 
 struct TcParams {
     int mode;
@@ -264,6 +264,13 @@ struct TcParams {
     const double *fconst;
     double *spsT, *sps2T, *hpartT;
     float *alpha_out;
+    // PARTIAL (split-K for few row tiles): every work unit is (row tile, column tile, k-split) with ONE
+    // accumulation chunk of chunk_kb k-blocks; its raw sums go to part[split][M][ldp] and tc_split_reduce
+    // adds the splits in chunk order (the same FP32 additions as the single-CTA drain) and applies the
+    // RATIO / BACKPROJ epilogue
+    int splits;             // k-splits (1: no split)
+    float *part;
+    int ldp;
     int dbg;                // performance experiments only (NFHMM_TC_DEBUG): 1 no A loads, 2 no MMAs, 4 no epilogue
                             // I/O, 8 no A TMEM stores, 32 no B loads, 64 no drains, 128 no converter work
 };
@@ -290,12 +297,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mtiles = (p.M + TC_BM - 1) / TC_BM;
-    const int n_total = n_mtiles * p.n_tiles;
+    const int splits = p.splits > 1 ? p.splits : 1;
+    const int n_total = n_mtiles * p.n_tiles * splits;
     const int kstart = p.k_begin & ~(TC_KB - 1);          // k-blocks on the global 16-element grid of Bsplit
     const int kb0 = kstart / TC_KB;
     const int n_kb = (p.k_end - kstart + TC_KB - 1) / TC_KB;
     const int chunk_kb = p.chunk_kb;
-    const int n_chunks = (n_kb + chunk_kb - 1) / chunk_kb;
+    // work unit -> (row tile, column tile) and its k-blocks [kb_lo, kb_hi) (all of them unless split)
+    auto unit_of = [&](int tile, int &mt, int &nt, int &ks, int &kb_lo, int &kb_hi) {
+        ks = tile % splits;
+        const int t2 = tile / splits;
+        mt = t2 / p.n_tiles;
+        nt = t2 - mt * p.n_tiles;
+        kb_lo = splits > 1 ? ks * chunk_kb : 0;
+        kb_hi = splits > 1 ? min(n_kb, kb_lo + chunk_kb) : n_kb;
+    };
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.stages; ++i) {
@@ -334,7 +350,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         RingPos rp;
         const uint32_t nst = (uint32_t)p.stages;
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
-            for (int kb = 0; kb < n_kb; ++kb, rp.next(nst)) {
+            int mt_, nt_, ks_, kb_lo, kb_hi;
+            unit_of(tile, mt_, nt_, ks_, kb_lo, kb_hi);
+            for (int kb = kb_lo; kb < kb_hi; ++kb, rp.next(nst)) {
                 const uint32_t st = rp.st;
                 mbar_wait(&S.loaded[st], rp.ph);
                 tc_fence_after();
@@ -382,23 +400,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {
             RingPos rp;
             const uint32_t nst = (uint32_t)p.stages;
-            int pf_tile = blockIdx.x, pf_kb = 0;
+            int pf_tile = blockIdx.x, pf_kb = 0, pf_mt = 0, pf_hi = 0;
+            {
+                int a_, b_, c_;
+                unit_of(pf_tile, pf_mt, a_, b_, pf_kb, pf_hi);
+                (void)c_;
+            }
             auto pf_advance = [&]() {
-                if (++pf_kb == n_kb) {
-                    pf_kb = 0;
+                if (++pf_kb == pf_hi) {
                     pf_tile += gridDim.x;
+                    int a_, b_;
+                    if (pf_tile < n_total) unit_of(pf_tile, pf_mt, a_, b_, pf_kb, pf_hi);
                 }
             };
             auto pf_issue = [&]() {
                 if (pf_tile < n_total && !(p.dbg & 1))
-                    tma_prefetch_2d(&tmA, kstart + pf_kb * TC_KB, (pf_tile / p.n_tiles) * TC_BM);
-                pf_advance();
+                    tma_prefetch_2d(&tmA, kstart + pf_kb * TC_KB, pf_mt * TC_BM);
+                if (pf_tile < n_total) pf_advance();
             };
             for (int i = 0; i < A_PREFETCH; ++i) pf_issue();
             for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
-                const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+                int mt, nt, ks_, kb_lo, kb_hi;
+                unit_of(tile, mt, nt, ks_, kb_lo, kb_hi);
                 const float *bt = p.Bsplit + (size_t)nt * p.nkb_total * (2 * (size_t)BN * TC_KB);
-                for (int kb = 0; kb < n_kb; ++kb, rp.next(nst)) {
+                for (int kb = kb_lo; kb < kb_hi; ++kb, rp.next(nst)) {
                     const uint32_t st = rp.st;
                     mbar_wait_sleep(&S.empty[st], rp.ph ^ 1);
                     unsigned char *sa = ring + (size_t)st * stage_bytes;
@@ -423,13 +448,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t nst = (uint32_t)p.stages;
         uint32_t ch_it = 0;
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
-            for (int c = 0; c < n_chunks; ++c, ++ch_it) {
+            int mt_, nt_, ks_, kb_lo, kb_hi;
+            unit_of(tile, mt_, nt_, ks_, kb_lo, kb_hi);
+            for (int cb = kb_lo; cb < kb_hi; cb += chunk_kb, ++ch_it) {
                 const uint32_t slot = ch_it & 1, sph = (ch_it >> 1) & 1;
                 mbar_wait(&S.pempty[slot], sph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + slot * (uint32_t)BN;
-                const int kb_end = min(n_kb, (c + 1) * chunk_kb);
-                for (int kb = c * chunk_kb; kb < kb_end; ++kb, rp.next(nst)) {
+                const int kb_end = min(kb_hi, cb + chunk_kb);
+                for (int kb = cb; kb < kb_end; ++kb, rp.next(nst)) {
                     const uint32_t st = rp.st;
                     mbar_wait(&S.loaded[st], rp.ph);   // B image landed (async proxy)
                     mbar_wait(&S.full[st], rp.ph);     // A split into TMEM
@@ -445,7 +472,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             const uint32_t bo = (uint32_t)kk * 2 * ((uint32_t)BN * 16);
                             const uint64_t dbh = umma_desc(b_hi + bo, (uint32_t)BN * 16, 128);
                             const uint64_t dbl = umma_desc(b_lo + bo, (uint32_t)BN * 16, 128);
-                            const uint32_t first = (kb == c * chunk_kb && kk == 0) ? 0u : 1u;
+                            const uint32_t first = (kb == cb && kk == 0) ? 0u : 1u;
                             if (p.dbg & 2) continue;
                             tc_mma_tf32_ts(d, a_lo + 8 * kk, dbh, idesc, first);   // small terms first
                             tc_mma_tf32_ts(d, a_hi + 8 * kk, dbl, idesc, 1u);
@@ -581,7 +608,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (!((endm >> (w - 1)) & 1) && rok && rel <= nb_last) (rel == 0 ? dst0 : dstn)[(size_t)(bq + rel) * ldf + row] = sp;
         };
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
-            const int mt = tile / p.n_tiles, nt = tile - mt * p.n_tiles;
+            int mt, nt, ks, kb_lo, kb_hi;
+            unit_of(tile, mt, nt, ks, kb_lo, kb_hi);
             const int m0 = mt * TC_BM, n0 = nt * BN;
             const int r0 = m0 + 32 * q;            // first row of this warp's 32-row slice
             // chunk 0's operand lands while the tile accumulates; chunk 1's is fetched after chunk 0 left
@@ -594,7 +622,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int j = 0; j < EPI_CH; ++j)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) acc[j][i] = 0.f;
-            for (int c = 0; c < n_chunks; ++c, ++ch_it) {
+            for (int cb = kb_lo; cb < kb_hi; cb += chunk_kb, ++ch_it) {
                 const uint32_t slot = ch_it & 1, sph = (ch_it >> 1) & 1;
                 mbar_wait_sleep(&S.pfull[slot], sph);
                 tc_fence_after();
@@ -684,6 +712,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     const int w = min(32, BN - c0);
                     if (p.dbg & 4) {
                         part += (double)acc[j][0];
+                    } else if (p.mode == TC_PARTIAL) {   // raw split sums, row-contiguous float4 stores
+                        float *dst = p.part + ((size_t)ks * p.M + row) * p.ldp + colb;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4)
+                            if (i < w) *reinterpret_cast<float4 *>(dst + i) = make_float4(acc[j][i], acc[j][i + 1], acc[j][i + 2], acc[j][i + 3]);
                     } else if (p.mode == TC_STORE) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
@@ -731,9 +764,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 int stages_for(int bn, int ring_off = RING_OFF) {
+    // as many stages as shared memory and the TMEM A columns allow: with few row tiles the per-stage load
+    // latency bounds a CTA (round 2, config 1: ~0.9k cycles per k-block at 8 stages whatever the width)
+    static int cap = -1;
+    if (cap < 0) {
+        const char *e = getenv("NFHMM_TC_STAGES");   // A/B experiments
+        cap = (e && atoi(e) >= 2 && atoi(e) <= MAX_STAGES) ? atoi(e) : MAX_STAGES;
+    }
     int s = (SMEM_MAX - ring_off) / stage_bytes_of(bn);
     if (s > tmem_a_stages(bn)) s = tmem_a_stages(bn);
-    return s > MAX_STAGES ? MAX_STAGES : s;
+    return s > cap ? cap : s;
 }
 
 // 2-D FP32 tensor map over rows x cols (row pitch ld floats), box box_c x box_r
@@ -785,7 +825,7 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
         if (e == cudaSuccess) e = make_map(&mOut, eout, p.ldc, p.M, p.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (e != cudaSuccess) return e;
     }
-    const int n_total = ((p.M + TC_BM - 1) / TC_BM) * p.n_tiles;
+    const int n_total = ((p.M + TC_BM - 1) / TC_BM) * p.n_tiles * (p.splits > 1 ? p.splits : 1);
     const int sms = (p.max_ctas > 0 && p.max_ctas < g_num_sms) ? p.max_ctas : g_num_sms;
     const int grid = n_total < sms ? n_total : sms;
     static int dbg = -1, chunk = CHUNK_KB;
@@ -798,6 +838,87 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
     p.dbg = dbg;
     p.chunk_kb = chunk;
     kern<<<grid, TC_THREADS, smem, st>>>(mA, mIn, mOut, mDv, p);
+    return cudaGetLastError();
+}
+
+// Split-K epilogue: C[row][c] = ((0 + part_0) + part_1) + ... (the chunk order of the single-CTA drain,
+// so C is bitwise the unsplit kernel's), then the RATIO epilogue (R = V / C, 0 where V = 0, zero-support
+// flag, the data term of the bound per 16-column sub-tile in the same fixed point) or BACKPROJ
+// (n = theta .* C; supported, not used: see nfhmm_abi.cu).  One thread per (row, 16-column sub-tile).
+__global__ void __launch_bounds__(256) tc_split_reduce_kernel(int mode, int splits, const float *__restrict__ part,
+                                                              int ldp, int M, int ldc, const float *__restrict__ ein,
+                                                              float *__restrict__ eout, double *data_part, int n_sub,
+                                                              unsigned *flags) {
+    const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int row = (int)(id / n_sub), sub = (int)(id - (long long)row * n_sub);
+    if (row >= M) return;
+    const int c0 = 16 * sub;
+    float acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+    for (int s = 0; s < splits; ++s) {
+        const float4 *src = reinterpret_cast<const float4 *>(part + ((size_t)s * M + row) * ldp + c0);
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4) {
+            const float4 v = src[i4];
+            acc[4 * i4] += v.x;
+            acc[4 * i4 + 1] += v.y;
+            acc[4 * i4 + 2] += v.z;
+            acc[4 * i4 + 3] += v.w;
+        }
+    }
+    const float *x = ein + (size_t)row * ldc + c0;
+    float *y = eout + (size_t)row * ldc + c0;
+    const int w = min(16, ldc - c0);   // ldc is a multiple of 8
+    if (mode == TC_BACKPROJ) {
+#pragma unroll
+        for (int i4 = 0; i4 < 4; ++i4) {
+            if (4 * i4 >= w) break;
+            const float4 t = reinterpret_cast<const float4 *>(x)[i4];
+            reinterpret_cast<float4 *>(y)[i4] =
+                make_float4(t.x * acc[4 * i4], t.y * acc[4 * i4 + 1], t.z * acc[4 * i4 + 2], t.w * acc[4 * i4 + 3]);
+        }
+        return;
+    }
+    float lsum = 0.f;
+    unsigned bad = 0;
+#pragma unroll
+    for (int i4 = 0; i4 < 4; ++i4) {
+        if (4 * i4 >= w) break;
+        const float4 v4 = reinterpret_cast<const float4 *>(x)[i4];
+        const float xv[4] = {v4.x, v4.y, v4.z, v4.w};
+        float r[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float vh = acc[4 * i4 + e];
+            const float rc = __frcp_rn(vh);
+            r[e] = 0.f;
+            if (xv[e] > 0.f) {
+                if (vh > 0.f) {
+                    r[e] = xv[e] * rc;
+                    lsum = fmaf(xv[e], __log2f(vh), lsum);
+                } else {
+                    bad |= FLAG_ZERO_SUPPORT;
+                }
+            }
+        }
+        reinterpret_cast<float4 *>(y)[i4] = make_float4(r[0], r[1], r[2], r[3]);
+    }
+    if (data_part) data_part[(size_t)row * n_sub + sub] = rint(0.69314718055994530942 * 1048576.0 * (double)lsum);
+    if (bad) atomicOr(flags, bad);
+}
+
+cudaError_t launch_split(TcParams p, const float *A, int lda, const float *ein, float *eout, int ldc, double *data_part,
+                         cudaStream_t st) {
+    const int mode = p.mode;
+    p.mode = TC_PARTIAL;
+    p.tma_epi = 0;
+    cudaError_t e = launch_tc(p, A, lda, nullptr, nullptr, st);
+    if (e != cudaSuccess) return e;
+    const int n_sub = (ldc + 15) / 16;
+    const long long threads = (long long)p.M * n_sub;
+    tc_split_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(mode, p.splits, p.part, p.ldp, p.M, ldc,
+                                                                            ein, eout, data_part, n_sub, p.flags);
     return cudaGetLastError();
 }
 
@@ -894,6 +1015,53 @@ cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaS
     p.nkb_total = a.nkb_total;
     p.ldc = a.ldb;
     return launch_tc(p, a.A, a.lda, a.theta, a.n_out, st);
+}
+
+int tc_split_count(int64_t k_len) {
+    const int n_kb = (int)((k_len + TC_KB - 1) / TC_KB);
+    return (n_kb + CHUNK_KB - 1) / CHUNK_KB;
+}
+
+int tc_pick_bn_split(int64_t n, int64_t rows, int splits, int sms) {
+    if (const char *e = getenv("NFHMM_SPLIT_BN")) {   // A/B experiments: one width for both contractions
+        const int b = atoi(e);
+        if (b >= 16 && b <= TC_MAX_BN && b % 16 == 0) return b;
+    }
+    // split-K units all carry one accumulation chunk: time ~ waves of units (the per-k-block step time
+    // measured ~0.6 us from BN = 32 to 176), then the widest tile
+    const int64_t mt = (rows + TC_BM - 1) / TC_BM;
+    int best = 16;
+    int64_t best_waves = INT64_MAX;
+    for (int bn = 16; bn <= TC_MAX_BN; bn += 16) {
+        const int64_t nt = (n + bn - 1) / bn;
+        const int64_t waves = (mt * nt * splits + sms - 1) / sms;
+        if (waves < best_waves || (waves == best_waves && bn < best)) {
+            best_waves = waves;
+            best = bn;
+        }
+    }
+    return best;
+}
+
+cudaError_t launch_recon_tc_split(int bn, const ReconArgs &a, float *part, cudaStream_t st) {
+    TcParams p{};
+    p.mode = TC_RATIO;
+    p.M = a.M;
+    p.bn = bn;
+    p.n_tiles = (a.F + bn - 1) / bn;
+    p.k_begin = a.k_begin;
+    p.k_end = a.k_end;
+    p.stages = stages_for(bn);
+    p.Bsplit = a.Bsplit;
+    p.nkb_total = a.nkb_total;
+    p.ldc = a.ldv;
+    p.F = a.F;
+    p.flags = a.flags;
+    p.splits = tc_split_count(a.k_end - (a.k_begin & ~(TC_KB - 1)));
+    p.part = part;
+    p.ldp = p.n_tiles * bn;
+    if (!a.R || a.Vhat || p.ldp < a.ldv) return cudaErrorInvalidValue;
+    return launch_split(p, a.A, a.lda, a.V, a.R, a.ldv, a.data_part, st);
 }
 
 int tc_fused_blocks_per_chunk(int K) { return (2 * K - 2 + 32) / K; }

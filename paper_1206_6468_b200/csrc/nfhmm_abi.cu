@@ -47,6 +47,9 @@ struct nfhmm {
     cudaStream_t fbst = nullptr;
     cudaEvent_t fev[2] = {nullptr, nullptr};
     int ldf = 0, nt_tc_b = 0;
+    // split-K reconstruction for few row tiles (single mixtures): units of one accumulation chunk + reduce
+    int split = 0;
+    float *tcpart = nullptr;
     float *dvT = nullptr;
     double *spsT = nullptr, *sps2T = nullptr, *hpartT = nullptr;
     // parallel-in-time forward-backward (few chains): chunks, their transfer matrices and start messages
@@ -173,7 +176,11 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take(chainTN * 4);                       h->fwd = (float *)p;
     p = take(chainT * 8);                        h->eoff = (double *)p;
     p = take((size_t)h->M * h->S * 8);           h->logZ = (double *)p;
-    p = take(fr * (size_t)(h->nt_a > h->nt_tc_a ? h->nt_a : h->nt_tc_a) * 8); h->data_part = (double *)p;
+    {
+        size_t nt = (size_t)(h->nt_a > h->nt_tc_a ? h->nt_a : h->nt_tc_a);
+        if (h->split && (size_t)(h->Fa + 15) / 16 > nt) nt = (size_t)(h->Fa + 15) / 16;   // split: 16-col sub-tiles
+        p = take(fr * nt * 8);                   h->data_part = (double *)p;
+    }
     p = take(fr * 8);                            h->hdir = (double *)p;
     p = take(fr * 4 * 8);                        h->fconst = (double *)p;
     p = take((size_t)h->M * ELBO_MAX_BLOCKS * 8); h->elbo_part = (double *)p;
@@ -198,6 +205,10 @@ size_t carve(nfhmm_t *h, char *base) {
         p = take(sn * ldf * 8);                  h->spsT = (double *)p;
         p = take(sn * ldf * 8);                  h->sps2T = (double *)p;
         p = take((size_t)h->nt_tc_b * ldf * 8);  h->hpartT = (double *)p;
+    }
+    if (h->split) {   // split-K partial sums (the larger of the two contractions)
+        const size_t pa = (size_t)tc_split_count(h->Kt) * fr * (size_t)h->nt_tc_a * h->bn_tc_a;
+        p = take(pa * 4);                        h->tcpart = (float *)p;
     }
     p = take(256);                               h->flags = (unsigned *)p;
     return o;
@@ -227,7 +238,11 @@ int run_recon(nfhmm_t *h, int cls, ReconArgs a) {
         a.nkb_total = (h->Kt + 15) / 16;
         a.ldb = h->Kb;
         a.n_tiles = h->nt_tc_a;
-        LAUNCH(h, cls, launch_recon_tc(h->bn_tc_a, a, h->st));
+        if (h->split && a.R && !a.Vhat) {
+            LAUNCH(h, cls, launch_recon_tc_split(h->bn_tc_a, a, h->tcpart, h->st));
+        } else {
+            LAUNCH(h, cls, launch_recon_tc(h->bn_tc_a, a, h->st));
+        }
     } else {
         a.B = h->betaT;     // [Kt_pad][F_pad]
         a.ldb = h->Fa;
@@ -237,7 +252,10 @@ int run_recon(nfhmm_t *h, int cls, ReconArgs a) {
     return NFHMM_OK;
 }
 
-int data_tiles(const nfhmm_t *h) { return h->math == NFHMM_MATH_TC ? h->nt_tc_a : h->nt_a; }
+int data_tiles(const nfhmm_t *h) {
+    if (h->math == NFHMM_MATH_TC) return h->split ? (int)((h->Fa + 15) / 16) : h->nt_tc_a;
+    return h->nt_a;
+}
 
 int recon_ratio(nfhmm_t *h, int max_ctas = 0) {
     ReconArgs a{};
@@ -575,6 +593,19 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         h->overlap_sms = (h->math == NFHMM_MATH_TC && frames > 65536 && h->fb_nchunk == 0) ? ((h->fb_multi && fb_multi_supported(h->N, h->M, 0)) ? 24 : 32) : 0;
         if (eo) h->overlap_sms = h->math == NFHMM_MATH_TC ? atoi(eo) : 0;
         if (h->overlap_sms < 0 || h->overlap_sms > 64) h->overlap_sms = 0;
+    }
+    {   // split-K for few row tiles: measured per k-block step ~0.6 us whatever the tile width, so
+        // single-mixture contractions (8-16 row tiles, 50-75 k-blocks per CTA) are latency-bound; units of
+        // one accumulation chunk cut the k-blocks per CTA 3-5x.  NFHMM_SPLITK=0 / 1 forces it off / on.
+        const char *e = getenv("NFHMM_SPLITK");
+        const int64_t mt = (frames + 127) / 128;
+        // Measured (round 2, ms per 100 sweeps, split / unsplit): config 1 reconstruction 2.93 / 3.47,
+        // back-projection 2.77 / 2.51; config 2 4.41 / 4.60 and 4.66 / 2.72 -- the back-projection's
+        // contraction (F_pad = 520: chunks of 16, 16 and 1 k-blocks) splits unevenly and its unsplit narrow
+        // tiles already fill the SMs, so only the reconstruction (Kt = 800 / 1200) is split.
+        const bool want = h->math == NFHMM_MATH_TC && !h->fused && mt <= 16 && tc_split_count(Kt) >= 3;
+        h->split = e ? (atoi(e) != 0 && h->math == NFHMM_MATH_TC && !h->fused) : want;
+        if (h->split) h->bn_tc_a = tc_pick_bn_split(F, frames, tc_split_count(Kt));
     }
     h->nt_tc_a = (int)((F + h->bn_tc_a - 1) / h->bn_tc_a);
     // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)

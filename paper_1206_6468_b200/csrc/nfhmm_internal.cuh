@@ -72,6 +72,13 @@ void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t
                       float *dst, int64_t k_pad = 0);
 cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st);
 cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st);
+// Split-K reconstruction for few row tiles (single mixtures): tc_split_count(k) units of one TMEM accumulation chunk per
+// (row tile, column tile); raw sums in part [splits][M][n_tiles * bn], then a fixed-order reduction with the
+// RATIO / BACKPROJ epilogue (results bitwise equal to the unsplit kernel; the RATIO data term goes to
+// data_part[row][ceil(ldv / 16)] -- 16-column sub-tiles -- in the same fixed point)
+int tc_split_count(int64_t k_len);
+int tc_pick_bn_split(int64_t n, int64_t rows, int splits, int sms = 148);
+cudaError_t launch_recon_tc_split(int bn, const ReconArgs &a, float *part, cudaStream_t st);
 
 // Back-projection with the Dirichlet element step fused into its epilogue (bn % K == 0, K <= 32):
 // theta is updated in place; Eq. 8 block sums and g~ partials leave block-major ([block][ldf]).

@@ -1,0 +1,12 @@
+#!/bin/bash
+mkdir -p gpurun_out
+run() { echo "== $*" >> gpurun_out/s2_bench.log; timeout 300 env "$@" python bench.py --config $CFG --steps 5 --warmup 3 --no-e2e --no-bound-off --no-cpu-baseline 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']/1e6,3), round(d['ms_per_step'],3), {k:round(v['ms_per_step'],2) for k,v in d['kernels'].items() if k in ('recon','backproj','fb')})" >> gpurun_out/s2_bench.log 2>&1; }
+for CFG in 1 2; do
+  run NFHMM_SPLITK=0 NFHMM_TC_STAGES=8
+  run NFHMM_SPLITK=0
+  run NFHMM_SPLITK=1
+  run NFHMM_SPLITK=1 NFHMM_SPLIT_BN=32
+  run NFHMM_SPLITK=1 NFHMM_SPLIT_BN=64
+  run NFHMM_SPLITK=1 NFHMM_SPLIT_BN=96
+done
+CFG=3; run NFHMM_TC_STAGES=8; run NFHMM_SPLITK=0
