@@ -1043,8 +1043,16 @@ int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len) {
     // 32 chains -- e.g. single-mixture configurations), for N <= 64 (phase-2 smem) and long enough sequences.  Chunk length ~ sqrt(T): phase 1
     // costs ~L matrix products per chunk, phase 2 ~T/L vector-matrix products per chain.
     if (chains > 32 || N > 64 || T < 96) return 0;
-    int L = 32;
-    while (L * L < T / 2 && L < 128) L *= 2;
+    // chunk length ~ sqrt(2.3 T) in multiples of 16 (round 2 sweep, frame-iterations/s: config 1 (T = 1000)
+    // L = 24 / 32 / 48 / 64 / 96 -> 7.3 / 7.6 / 8.2 / 7.9 / 7.4 M; config 2 (T = 2000) 32 / 48 / 64 / 96 ->
+    // 9.5 / 10.2 / 10.3 / 10.2 M): the transfer and re-run phases cost ~L steps, the scan ~T / L chunks
+    int L = 16 * (int)lround(sqrt(2.3 * (double)T) / 16.0);
+    if (L < 32) L = 32;
+    if (L > 256) L = 256;
+    if (const char *e = getenv("NFHMM_FB_CHUNK")) {   // experiments (chunk length)
+        const int l = atoi(e);
+        if (l >= 8 && l <= 1024) L = l;
+    }
     // phase 2 keeps every chunk's row scales in shared memory: grow the chunks until it fits (the
     // template bucket NMAX of N as in launch_fb); past L = 4096 keep the sequential kernel
     const int NMAX = N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : N <= 24 ? 24 : N <= 32 ? 32 : N <= 40 ? 40 : N <= 48 ? 48 : 64;
