@@ -20,10 +20,14 @@
  *   M-step  theta_t(d)_z  ∝ sum_l V_lt P(z | l, t, d);
  *           beta_l(d,z)   ∝ sum_t gamma_t(d) V_lt P(z | l, t, d);
  *           rho(i -> j)   ∝ sum_{t>=1} xi_t(i,j);  pi = gamma_0;
- *           rho rows and pi floored at 1e-15 and renormalised (DESIGN R21, see floor_renorm);
- *           a state whose posterior mass sum_t gamma_t(d) is below 1e-8 T keeps its dictionary, a row of
- *           rho whose mass sum_{t<T-1} gamma_t(i) is below 1e-8 T keeps its values (DESIGN R22: their
- *           ML updates are set by underflow-level weights, which FP64 and FP32 resolve differently).
+ *           beta and rho floored at 1e-12, then renormalised (SPEC's decision S:214: "Floor of 1e-12
+ *           applied to beta and rho after each M-step, then renormalize ... prevents absorbing zeros that
+ *           would freeze EM"), and pi likewise (DESIGN R21: pi = gamma_0 puts all its mass on one state
+ *           after a few iterations; if that state's emission ratio at frame 0 underflows, the evidence is
+ *           exactly 0 and EM stops -- the absorbing zero S:214 guards against, on the chain's other
+ *           parameter).  A sum with no weight at all (an element no frame, or a chain
+ *           row no transition, gave any posterior mass to -- exactly 0 in FP64) keeps its previous value:
+ *           0/0 has no ML solution.
  * (theta's update carries no gamma: gamma_t(d) is constant in z for fixed (t, d) and cancels in the
  * normalisation.)  Every step is the exact maximiser of the expected complete-data log-likelihood,
  * so the returned log evidence is non-decreasing across iterations.
@@ -131,18 +135,11 @@ int or_nhmm_loglik(int F, int T, int N, int K, const double *V, const double *be
     return OR_OK;
 }
 
-/* DESIGN R21: chain probabilities are floored at 1e-15 after each M-step (then renormalised).  At 10^4-10^5
- * counts per frame the per-state log-likelihoods of a frame differ by thousands of nats, so most
- * emission ratios exp(loglik - max) underflow to exactly 0; transitions that no posterior path used
- * then come out exactly 0 and, one iteration later, a frame whose only explaining state is unreachable
- * has zero evidence in floating point.  The floor keeps every path feasible.  Its size is set by the
- * GPU's FP32 recursion, which rescales each message by the PREVIOUS step's sum: along the best path a
- * product of two floored steps must stay normal, (f/N)^2 >= 2^-126, i.e. f >= N 2^-63 (1.4e-17 at
- * N = 128); 1e-15 moves the evidence by O(1e-15) relative. */
+/* S:214 (DESIGN R21): floor at 1e-12, then renormalise. */
 static void floor_renorm(double *p, int n) {
     double s = 0.0;
     for (int i = 0; i < n; ++i) {
-        if (p[i] < 1e-15) p[i] = 1e-15;
+        if (p[i] < 1e-12) p[i] = 1e-12;
         s += p[i];
     }
     for (int i = 0; i < n; ++i) p[i] /= s;
@@ -191,22 +188,21 @@ int or_nhmm_em_step(int F, int T, int N, int K, const double *V, double *beta, d
                 for (int z = 0; z < K; ++z) theta[(size_t)(t * N + d) * K + z] = nt[(size_t)(t * N + d) * K + z] / s;
         }
     for (int dz = 0; dz < N * K; ++dz) {
-        const int d = dz / K;
-        double mass = 0.0, s = 0.0;   /* DESIGN R22: a state with negligible posterior mass keeps beta */
-        for (int t = 0; t < T; ++t) mass += g[t * N + d];
+        double s = 0.0;
         for (int l = 0; l < F; ++l) s += nb[dz * F + l];
-        if (s > 0.0 && mass >= 1e-8 * T)
+        if (s > 0.0)
             for (int l = 0; l < F; ++l) beta[dz * F + l] = nb[dz * F + l] / s;
+        floor_renorm(beta + (size_t)dz * F, F);
     }
     for (int i = 0; i < N; ++i) {
         double s = 0.0;
         for (int j = 0; j < N; ++j) s += xi[i * N + j];
-        if (s >= 1e-8 * T)   /* DESIGN R22: s = sum_{t < T-1} gamma_t(i), the row's posterior mass */
+        if (s > 0.0)
             for (int j = 0; j < N; ++j) A[i * N + j] = xi[i * N + j] / s;
         floor_renorm(A + (size_t)i * N, N);
     }
     for (int d = 0; d < N; ++d) pi[d] = g[d];
-    floor_renorm(pi, N);
+    floor_renorm(pi, N);   /* pi is the chain's other parameter: the same floor (DESIGN R21) */
 done:
     free(ll); free(g); free(xi); free(nb); free(nt);
     return st;

@@ -8,22 +8,27 @@
 //   M-step  theta_t(d)_z ∝ theta_t(d)_z C_{t,d,z},  C_{t,d,z} = sum_l beta_l(d,z) V_lt / lhat_{t,d}(l);
 //           beta_l(d,z)  ∝ beta_l(d,z) sum_t gamma_t(d) theta_t(d)_z V_lt / lhat_{t,d}(l);
 //           rho(i -> j)  ∝ sum_{t>=1} xi_t(i,j),  xi_t(i,j) = u_{t-1}(i) A_ij e_t(j) b_t(j) / Z_t;  pi = gamma_0;
-//           rho rows and pi floored at 1e-15 and renormalised (DESIGN R21: keeps every path feasible when
-//           the emission ratios of a 1e5-count frame underflow; large enough that two floored steps in a
-//           row stay normal in the FP32 recursion); states / rows with posterior mass below 1e-8 T keep
-//           their dictionary / row (DESIGN R22).
+//           beta and rho floored at 1e-12 and renormalised (SPEC's decision S:214), pi likewise (DESIGN R21).
+// The posterior weights span hundreds of orders of magnitude (at 1e4-1e5 counts per frame the per-state
+// log-likelihoods of a frame differ by thousands of nats): a state the posterior barely visits has
+// gamma_t(d) ~ 1e-289, and its ML dictionary update is a ratio of such weights.  Everything that carries
+// posterior weight therefore runs in FP64 -- the emissions e, the chain recursion (train_fb_kernel), gamma,
+// xi and the beta sums -- so the GPU reaches the same plain ML update as the FP64 oracle (round 1 ran the
+// FP32 VB recursion here and had to skip the updates of such states).
 // Kernels, per EM iteration (n_src independent sources batched in every launch):
 //   estep_kernel<KM>     CTA per (source, state d, tile of frames): beta(d) [K][F] staged in shared memory,
 //                        a warp per frame, lanes over l; loglik in FP64 (per-bin terms v log lhat are
 //                        ~1e3 and the frame totals ~1e5: FP32 sums would move e = exp(loglik - max) by
 //                        ~1e-3), C_{t,d,:} by warp reductions;
-//   emission_kernel      e_t(d) = exp(loglik - max_d loglik), eoff_t = max (FP64) -> launch_fb;
+//   emission_kernel      e_t(d) = exp(loglik - max_d loglik) (FP64), eoff_t = max;
+//   train_fb_kernel      FP64 scaled forward-backward per source (forward and backward warps concurrently),
+//                        log evidence;
 //   posterior_kernel     gamma_t = u_t .* b_t / sum and the pairwise normaliser Z_t = u_{t-1} A (e_t .* b_t);
 //   xi_kernel            sum_{t>=1} xi_t(i,j), thread per (i, j), FP64 accumulation over t;
 //   beta_kernel<KM>      thread per (source, d, l): beta_l(d,:) in registers, FP64 accumulation over t;
-//   beta_norm_kernel / mstep_kernel  normalisations, theta, rho, pi.
-// The forward-backward messages are power-of-two scaled per step (fb.cu); every consumer normalises
-// per frame, so the scales cancel exactly.
+//   beta_norm_kernel / mstep_kernel  normalisations, floors, theta, rho, pi.
+// The messages are normalised per step (forward by its sum, whose logs give the evidence; backward by its
+// sum); every consumer normalises per frame, so the scales cancel.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
@@ -103,7 +108,7 @@ __global__ void __launch_bounds__(256) estep_kernel(int F, int T, int N, int K, 
 }
 
 // one warp per (source, frame): e = exp(loglik - max_d), eoff = max_d (FP64)
-__global__ void emission_kernel(int T, int N, int MT, const double *LL, float *ec, double *eoff, unsigned *flags) {
+__global__ void emission_kernel(int T, int N, int MT, const double *LL, double *ec, double *eoff, unsigned *flags) {
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (w >= MT) return;
     const double *l = LL + (size_t)w * N;
@@ -115,26 +120,137 @@ __global__ void emission_kernel(int T, int N, int MT, const double *LL, float *e
         if (lane == 0) atomicOr(flags, FLAG_ZERO_SUPPORT);
         mx = 0.0;
     }
-    for (int d = lane; d < N; d += 32) ec[(size_t)w * N + d] = (float)exp(l[d] - mx);
+    for (int d = lane; d < N; d += 32) ec[(size_t)w * N + d] = exp(l[d] - mx);
     if (lane == 0) eoff[w] = mx;
+}
+
+// FP64 scaled forward-backward, one warp per (source, direction), lanes over states, A in shared memory:
+//   u_0 = pi .* e_0 / c_0,  u_t = (u_{t-1} A) .* e_t / c_t  (c_t = the sum; log Z = sum_t ln c_t + eoff_t);
+//   b_{T-1} = 1,  b_t = A (e_{t+1} .* b_{t+1}) / (its sum).
+__global__ void __launch_bounds__(64) train_fb_kernel(int T, int N, const double *ec, const double *eoff,
+                                                      const float *A, const float *prior, double *fw, double *bw,
+                                                      double *logZ, unsigned *flags) {
+    extern __shared__ __align__(16) double tsm[];
+    double *As = tsm;                 // [N][N]
+    const int m = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *xb = tsm + (size_t)N * N + warp * 2 * N;   // [2][N] broadcast buffers of this warp
+    const float *Ag = A + (size_t)m * N * N;
+    for (int i = threadIdx.x; i < N * N; i += blockDim.x) As[i] = (double)Ag[i];
+    __syncthreads();
+    const double *e = ec + (size_t)m * T * N;
+    unsigned bad = 0;
+    auto wsum = [&](double v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+    if (warp == 0) {   // forward
+        double *f = fw + (size_t)m * T * N;
+        double lz = 0.0, part = 0.0;
+        for (int j = lane; j < N; j += 32) {
+            const double v = (double)prior[(size_t)m * N + j] * e[j];
+            xb[j] = v;
+            part += v;
+        }
+        double c = wsum(part);
+        if (!(c > 0.0)) bad |= FLAG_NONFINITE;
+        double ic = 1.0 / c;
+        __syncwarp();
+        for (int j = lane; j < N; j += 32) {
+            xb[j] *= ic;
+            f[j] = xb[j];
+        }
+        lz += log(c) + eoff[(size_t)m * T];
+        __syncwarp();
+        for (int t = 1; t < T; ++t) {
+            const double *prev = xb + ((t - 1) & 1) * N;
+            double *cur = xb + (t & 1) * N;
+            part = 0.0;
+            for (int j = lane; j < N; j += 32) {
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four chains: latency
+                int i = 0;
+                for (; i + 3 < N; i += 4) {
+                    a0 = fma(prev[i], As[i * N + j], a0);
+                    a1 = fma(prev[i + 1], As[(i + 1) * N + j], a1);
+                    a2 = fma(prev[i + 2], As[(i + 2) * N + j], a2);
+                    a3 = fma(prev[i + 3], As[(i + 3) * N + j], a3);
+                }
+                for (; i < N; ++i) a0 = fma(prev[i], As[i * N + j], a0);
+                const double v = ((a0 + a1) + (a2 + a3)) * e[(size_t)t * N + j];
+                cur[j] = v;
+                part += v;
+            }
+            c = wsum(part);
+            if (!(c > 0.0)) bad |= FLAG_NONFINITE;
+            ic = 1.0 / c;
+            __syncwarp();
+            for (int j = lane; j < N; j += 32) {
+                cur[j] *= ic;
+                f[(size_t)t * N + j] = cur[j];
+            }
+            lz += log(c) + eoff[(size_t)m * T + t];
+            __syncwarp();
+        }
+        if (lane == 0) {
+            logZ[m] = lz;
+            if (!isfinite(lz)) bad |= FLAG_NONFINITE;
+        }
+    } else {           // backward
+        double *b = bw + (size_t)m * T * N;
+        for (int j = lane; j < N; j += 32) {
+            b[(size_t)(T - 1) * N + j] = 1.0;
+            xb[((T - 1) & 1) * N + j] = e[(size_t)(T - 1) * N + j];   // x_{T-1} = e_{T-1} .* b_{T-1}
+        }
+        __syncwarp();
+        for (int t = T - 2; t >= 0; --t) {
+            const double *x = xb + ((t + 1) & 1) * N;
+            double *cur = xb + (t & 1) * N;
+            double part = 0.0;
+            double bv[4];
+            int q = 0;
+            for (int i = lane; i < N; i += 32, ++q) {
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                int j = 0;
+                for (; j + 3 < N; j += 4) {
+                    a0 = fma(As[i * N + j], x[j], a0);
+                    a1 = fma(As[i * N + j + 1], x[j + 1], a1);
+                    a2 = fma(As[i * N + j + 2], x[j + 2], a2);
+                    a3 = fma(As[i * N + j + 3], x[j + 3], a3);
+                }
+                for (; j < N; ++j) a0 = fma(As[i * N + j], x[j], a0);
+                bv[q] = (a0 + a1) + (a2 + a3);
+                part += bv[q];
+            }
+            const double sum = wsum(part);
+            if (!(sum > 0.0)) bad |= FLAG_NONFINITE;
+            const double is = 1.0 / sum;
+            __syncwarp();
+            q = 0;
+            for (int i = lane; i < N; i += 32, ++q) {
+                const double v = bv[q] * is;
+                b[(size_t)t * N + i] = v;
+                cur[i] = v * e[(size_t)t * N + i];
+            }
+            __syncwarp();
+        }
+    }
+    if (bad) atomicOr(flags, bad);
 }
 
 // one warp per (source, frame): gamma_t = u .* b / sum; for t >= 1, 1 / Z_t with
 // Z_t = sum_i u_{t-1}(i) sum_j A_ij e_t(j) b_t(j) (the pairwise normaliser; reciprocal once per frame)
-__global__ void posterior_kernel(int T, int N, int MT, const float *u, const float *b, const float *ec, const float *A,
-                                 float *gamma, double *Zt) {
+__global__ void posterior_kernel(int T, int N, int MT, const double *u, const double *b, const double *ec,
+                                 const float *A, double *gamma, double *Zt) {
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (w >= MT) return;
     const int m = w / T, t = w - m * T;
     const size_t row = (size_t)w * N;
-    // FP64 products: the messages carry the scale of the PREVIOUS step (fb.cu), so u_t and b_t can each be
-    // ~1e-15 when the chain passes a floored transition and their FP32 product would underflow
     double s = 0.0;
-    for (int d = lane; d < N; d += 32) s += (double)u[row + d] * (double)b[row + d];
+    for (int d = lane; d < N; d += 32) s += u[row + d] * b[row + d];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const double is = 1.0 / s;
-    for (int d = lane; d < N; d += 32) gamma[row + d] = (float)((double)u[row + d] * (double)b[row + d] * is);
+    for (int d = lane; d < N; d += 32) gamma[row + d] = u[row + d] * b[row + d] * is;
     if (t == 0) {
         if (lane == 0) Zt[w] = 0.0;
         return;
@@ -143,8 +259,8 @@ __global__ void posterior_kernel(int T, int N, int MT, const float *u, const flo
     double z = 0.0;
     for (int i = lane; i < N; i += 32) {
         double y = 0.0;
-        for (int j = 0; j < N; ++j) y = fma((double)Am[i * N + j], (double)ec[row + j] * (double)b[row + j], y);
-        z += (double)u[row - N + i] * y;
+        for (int j = 0; j < N; ++j) y = fma((double)Am[i * N + j], ec[row + j] * b[row + j], y);
+        z += u[row - N + i] * y;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
@@ -153,35 +269,35 @@ __global__ void posterior_kernel(int T, int N, int MT, const float *u, const flo
 
 // thread per (source, i, j) and chunk of frames: partial xi sums A_ij sum_{t in chunk, t>=1}
 // u_{t-1}(i) e_t(j) b_t(j) / Z_t (FP64); mstep_kernel adds the chunks in a fixed order
-__global__ void xi_kernel(int T, int N, int M, int tchunk, const float *u, const float *b, const float *ec,
-                          const double *invZ, const float *A, float *xi_part) {
+__global__ void xi_kernel(int T, int N, int M, int tchunk, const double *u, const double *b, const double *ec,
+                          const double *invZ, const float *A, double *xi_part) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
     if (idx >= M * N * N) return;
     const int m = idx / (N * N), ij = idx - m * N * N, i = ij / N, j = ij - i * N;
     const size_t base = (size_t)m * T * N;
     double acc = 0.0;
     for (int t = max(1, c * tchunk); t < min(T, (c + 1) * tchunk); ++t)
-        acc += (double)u[base + (size_t)(t - 1) * N + i] * ((double)ec[base + (size_t)t * N + j] * (double)b[base + (size_t)t * N + j]) *
+        acc += u[base + (size_t)(t - 1) * N + i] * (ec[base + (size_t)t * N + j] * b[base + (size_t)t * N + j]) *
                invZ[(size_t)m * T + t];
-    xi_part[(size_t)c * M * N * N + idx] = (float)(acc * (double)A[(size_t)m * N * N + ij]);
+    xi_part[(size_t)c * M * N * N + idx] = acc * (double)A[(size_t)m * N * N + ij];
 }
 
 // thread per (source, d, l) and chunk of frames: partial nb_l(d, z) = beta_l(d,z) sum_{t in chunk}
-// gamma_t(d) theta_t(d)_z V_lt / lhat_{t,d}(l), compensated FP32 accumulation; beta_norm_kernel adds the chunks
+// gamma_t(d) theta_t(d)_z V_lt / lhat_{t,d}(l) in FP64 (gamma may be ~1e-289); beta_norm_kernel adds the chunks
 template <int KM>
 __global__ void __launch_bounds__(BK_THREADS) beta_kernel(int F, int T, int N, int K, int tchunk, const float *V,
-                                                          const float *beta, const float *theta, const float *gamma,
-                                                          float *nb_part) {
+                                                          const float *beta, const float *theta, const double *gamma,
+                                                          double *nb_part) {
     const int M = gridDim.z / ((T + tchunk - 1) / tchunk);
     const int c = blockIdx.z / M, m = blockIdx.z - c * M, d = blockIdx.y, l = blockIdx.x * BK_THREADS + threadIdx.x;
     const bool lv = l < F;
     const float *bg = beta + ((size_t)m * N + d) * K * F;
-    float bz[KM], acc[KM], cmp[KM];   // compensated (Kahan) FP32 sums over the chunk's frames
+    float bz[KM];
+    double acc[KM];
 #pragma unroll
     for (int z = 0; z < KM; ++z) {
         bz[z] = (lv && z < K) ? bg[z * F + l] : 0.f;
-        acc[z] = 0.f;
-        cmp[z] = 0.f;
+        acc[z] = 0.0;
     }
     const int t1 = min(T, (c + 1) * tchunk);
     // branch-free body (a zero weight where V = 0 or lhat = 0) so the loads of the next frames issue
@@ -190,42 +306,33 @@ __global__ void __launch_bounds__(BK_THREADS) beta_kernel(int F, int T, int N, i
     for (int t = c * tchunk; t < t1; ++t) {
         const float v = lv ? V[((size_t)m * T + t) * F + l] : 0.f;
         const float *th = theta + (((size_t)m * T + t) * N + d) * K;
-        const float gm = gamma[((size_t)m * T + t) * N + d];
+        const double gm = gamma[((size_t)m * T + t) * N + d];
         float tz[KM];
-        float lh = 0.f;   // the weights need FP32 only (the log-likelihood's lhat is FP64, estep_kernel)
+        float lh = 0.f;   // V / lhat needs FP32 only (the log-likelihood's lhat is FP64, estep_kernel)
 #pragma unroll
         for (int z = 0; z < KM; ++z) {
             tz[z] = z < K ? th[z] : 0.f;
             lh = fmaf(tz[z], bz[z], lh);
         }
-        const float g = (v > 0.f && lh > 0.f) ? gm * __fdiv_rn(v, lh) : 0.f;
+        const double g = (v > 0.f && lh > 0.f) ? gm * (double)__fdiv_rn(v, lh) : 0.0;
 #pragma unroll
         for (int z = 0; z < KM; ++z)
-            if (z < K) {
-                const float y = __fsub_rn(g * tz[z], cmp[z]);
-                const float t2 = __fadd_rn(acc[z], y);
-                cmp[z] = __fsub_rn(__fsub_rn(t2, acc[z]), y);
-                acc[z] = t2;
-            }
+            if (z < K) acc[z] = fma(g, (double)tz[z], acc[z]);
     }
     if (lv) {
-        float *dst = nb_part + (size_t)c * gridDim.y * M * K * F;   // [chunk][M][N][K][F]
+        double *dst = nb_part + (size_t)c * gridDim.y * M * K * F;   // [chunk][M][N][K][F]
 #pragma unroll
         for (int z = 0; z < KM; ++z)
-            if (z < K) dst[(((size_t)m * N + d) * K + z) * F + l] = (float)(((double)acc[z] - (double)cmp[z]) * (double)bz[z]);
+            if (z < K) dst[(((size_t)m * N + d) * K + z) * F + l] = acc[z] * (double)bz[z];
     }
 }
 
-// warp per (source, d, z): nb = sum over frame chunks of the partials (fixed order), beta <- nb / sum_l nb;
-// kept when the element saw no data or the state's posterior mass sum_t gamma_t(d) is below 1e-8 T
-// (DESIGN R22)
-__global__ void beta_norm_kernel(int F, int T, int N, int K, int rows, int nchunk, const float *nb_part,
-                                 const float *gamma, float *beta) {
+// warp per (source, d, z): nb = sum over frame chunks of the partials (fixed order), beta <- nb / sum_l nb
+// (kept when the element got no weight at all: 0/0), then the 1e-12 floor and renormalisation
+__global__ void beta_norm_kernel(int F, int T, int N, int K, int rows, int nchunk, const double *nb_part,
+                                 float *beta) {
     const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (w >= rows) return;
-    const int m = w / (N * K), d = (w / K) % N;
-    double mass = 0.0;
-    for (int t = lane; t < T; t += 32) mass += gamma[((size_t)m * T + t) * N + d];
     const size_t stride = (size_t)rows * F;
     double s = 0.0;
     for (int l = lane; l < F; l += 32) {
@@ -234,22 +341,39 @@ __global__ void beta_norm_kernel(int F, int T, int N, int K, int rows, int nchun
         s += v;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, o);
-        mass += __shfl_xor_sync(0xffffffffu, mass, o);
-    }
-    if (s > 0.0 && mass >= 1e-8 * T)
-        for (int l = lane; l < F; l += 32) {
-            double v = 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    float *bt = beta + (size_t)w * F;
+    double s2 = 0.0;   // sum of the floored values
+    for (int l = lane; l < F; l += 32) {
+        double v;
+        if (s > 0.0) {
+            v = 0.0;
             for (int c = 0; c < nchunk; ++c) v += nb_part[c * stride + (size_t)w * F + l];
-            beta[(size_t)w * F + l] = (float)(v / s);
+            v /= s;
+        } else {
+            v = (double)bt[l];
         }
+        s2 += fmax(v, 1e-12);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    for (int l = lane; l < F; l += 32) {
+        double v;
+        if (s > 0.0) {
+            v = 0.0;
+            for (int c = 0; c < nchunk; ++c) v += nb_part[c * stride + (size_t)w * F + l];
+            v /= s;
+        } else {
+            v = (double)bt[l];
+        }
+        bt[l] = (float)(fmax(v, 1e-12) / s2);
+    }
 }
 
 // theta_t(d) <- theta .* C / sum (thread per (source, t, d)); rho rows from xi, pi = gamma_0 (threads of
 // the first blocks)
-__global__ void mstep_kernel(int T, int N, int K, int M, int nchunk, float *theta, const float *C, const float *xi_part,
-                             float *A, float *prior, const float *gamma) {
+__global__ void mstep_kernel(int T, int N, int K, int M, int nchunk, float *theta, const float *C, const double *xi_part,
+                             float *A, float *prior, const double *gamma) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx < M * T * N) {
         float *th = theta + (size_t)idx * K;
@@ -259,28 +383,38 @@ __global__ void mstep_kernel(int T, int N, int K, int M, int nchunk, float *thet
         if (s > 0.0)
             for (int z = 0; z < K; ++z) th[z] = (float)((double)th[z] * (double)c[z] / s);
     }
-    if (idx < M * N) {   // rho row i of source m; rows and pi floored at 1e-15 and renormalised (DESIGN R21)
+    if (idx < M * N) {   // rho row i of source m: ML row (kept on 0/0), 1e-12 floor, renormalised
         const int m = idx / N, i = idx - m * N;
         const size_t row = (size_t)m * N * N + (size_t)i * N, cs = (size_t)M * N * N;
         float *a = A + row;
         double s = 0.0;
         for (int j = 0; j < N; ++j)
             for (int c = 0; c < nchunk; ++c) s += xi_part[c * cs + row + j];
-        if (s >= 1e-8 * T)   // s = sum_{t < T-1} gamma_t(i), the row's posterior mass (DESIGN R22)
-            for (int j = 0; j < N; ++j) {
-                double x = 0.0;
-                for (int c = 0; c < nchunk; ++c) x += xi_part[c * cs + row + j];
-                a[j] = (float)(x / s);
-            }
         double s2 = 0.0;
-        for (int j = 0; j < N; ++j) s2 += fmax((double)a[j], 1e-15);
-        for (int j = 0; j < N; ++j) a[j] = (float)(fmax((double)a[j], 1e-15) / s2);
+        for (int j = 0; j < N; ++j) {
+            double x = (double)a[j];
+            if (s > 0.0) {
+                x = 0.0;
+                for (int c = 0; c < nchunk; ++c) x += xi_part[c * cs + row + j];
+                x /= s;
+            }
+            s2 += fmax(x, 1e-12);
+        }
+        for (int j = 0; j < N; ++j) {
+            double x = (double)a[j];
+            if (s > 0.0) {
+                x = 0.0;
+                for (int c = 0; c < nchunk; ++c) x += xi_part[c * cs + row + j];
+                x /= s;
+            }
+            a[j] = (float)(fmax(x, 1e-12) / s2);
+        }
     }
-    if (idx < M) {
-        const float *g = gamma + (size_t)idx * T * N;
+    if (idx < M) {   // pi = gamma_0, floored at 1e-12 and renormalised like rho (DESIGN R21)
+        const double *g = gamma + (size_t)idx * T * N;
         double s = 0.0;
-        for (int d = 0; d < N; ++d) s += fmax((double)g[d], 1e-15);
-        for (int d = 0; d < N; ++d) prior[(size_t)idx * N + d] = (float)(fmax((double)g[d], 1e-15) / s);
+        for (int d = 0; d < N; ++d) s += fmax(g[d], 1e-12);
+        for (int d = 0; d < N; ++d) prior[(size_t)idx * N + d] = (float)(fmax(g[d], 1e-12) / s);
     }
 }
 
@@ -309,7 +443,7 @@ cudaError_t launch_estep(int F, int T, int N, int K, int M, const float *V, cons
 
 template <int KM>
 cudaError_t launch_beta(int F, int T, int N, int K, int M, int tchunk, const float *V, const float *beta,
-                        const float *theta, const float *gamma, float *nb, cudaStream_t st) {
+                        const float *theta, const double *gamma, double *nb, cudaStream_t st) {
     const int nc = (T + tchunk - 1) / tchunk;
     beta_kernel<KM><<<dim3((F + BK_THREADS - 1) / BK_THREADS, N, M * nc), BK_THREADS, 0, st>>>(F, T, N, K, tchunk, V, beta,
                                                                                               theta, gamma, nb);
@@ -326,8 +460,8 @@ struct nhmm_train {
     int N = 0, K = 0, max_iters = 0, device = 0, iters = 0;
     cudaStream_t st = nullptr;
     void *mem = nullptr;
-    float *V = nullptr, *beta = nullptr, *nb = nullptr, *theta = nullptr, *A = nullptr, *prior = nullptr;
-    float *C = nullptr, *ec = nullptr, *fwd = nullptr, *bwd = nullptr, *gamma = nullptr, *xi = nullptr;
+    float *V = nullptr, *beta = nullptr, *theta = nullptr, *A = nullptr, *prior = nullptr, *C = nullptr;
+    double *nb = nullptr, *ec = nullptr, *fwd = nullptr, *bwd = nullptr, *gamma = nullptr, *xi = nullptr;
     double *Zt = nullptr, *LL = nullptr, *eoff = nullptr, *logZ = nullptr, *trace = nullptr;
     unsigned *flags = nullptr;
     bool have_data = false, have_params = false;
@@ -400,10 +534,10 @@ int nhmm_train_create(int64_t F, int64_t T, int32_t N, int32_t K, int64_t n_src,
         off += (bytes + 255) & ~size_t(255);
         return o;
     };
-    const size_t oV = take(MT * F * 4), oB = take(MN * K * F * 4), oNB = take(nchunk * MN * K * F * 4), oTh = take(MT * N * K * 4),
-                 oA = take(MN * N * 4), oP = take(MN * 4), oC = take(MT * N * K * 4), oE = take(MT * N * 4),
-                 oF = take(MT * N * 4), oBw = take(MT * N * 4), oG = take(MT * N * 4), oZ = take(MT * 8),
-                 oX = take(nchunk * MN * N * 4), oLL = take(MT * N * 8), oEo = take(MT * 8), oLZ = take(n_src * 8),
+    const size_t oV = take(MT * F * 4), oB = take(MN * K * F * 4), oNB = take(nchunk * MN * K * F * 8), oTh = take(MT * N * K * 4),
+                 oA = take(MN * N * 4), oP = take(MN * 4), oC = take(MT * N * K * 4), oE = take(MT * N * 8),
+                 oF = take(MT * N * 8), oBw = take(MT * N * 8), oG = take(MT * N * 8), oZ = take(MT * 8),
+                 oX = take(nchunk * MN * N * 8), oLL = take(MT * N * 8), oEo = take(MT * 8), oLZ = take(n_src * 8),
                  oTr = take((size_t)n_src * max_iters * 8), oFl = take(256);
 
     if (cudaMalloc(&h->mem, off) != cudaSuccess) {
@@ -413,17 +547,17 @@ int nhmm_train_create(int64_t F, int64_t T, int32_t N, int32_t K, int64_t n_src,
     char *b = (char *)h->mem;
     h->V = (float *)(b + oV);
     h->beta = (float *)(b + oB);
-    h->nb = (float *)(b + oNB);
+    h->nb = (double *)(b + oNB);
     h->theta = (float *)(b + oTh);
     h->A = (float *)(b + oA);
     h->prior = (float *)(b + oP);
     h->C = (float *)(b + oC);
-    h->ec = (float *)(b + oE);
-    h->fwd = (float *)(b + oF);
-    h->bwd = (float *)(b + oBw);
-    h->gamma = (float *)(b + oG);
+    h->ec = (double *)(b + oE);
+    h->fwd = (double *)(b + oF);
+    h->bwd = (double *)(b + oBw);
+    h->gamma = (double *)(b + oG);
     h->Zt = (double *)(b + oZ);
-    h->xi = (float *)(b + oX);
+    h->xi = (double *)(b + oX);
     h->LL = (double *)(b + oLL);
     h->eoff = (double *)(b + oEo);
     h->logZ = (double *)(b + oLZ);
@@ -502,25 +636,12 @@ int nhmm_train_em(nhmm_train_t *h, int32_t n_iters) {
         TCU(h, e);
         emission_kernel<<<(MT + 7) / 8, 256, 0, h->st>>>(T, N, MT, h->LL, h->ec, h->eoff, h->flags);
         TCU(h, cudaGetLastError());
-        FBArgs f{};   // each source is its own chain: M = 1 mixture, S = n_src sources
-        f.M = 1;
-        f.S = M;
-        f.T = T;
-        f.N = N;
-        f.ec = h->ec;
-        f.eoff = h->eoff;
-        f.trans = h->A;
-        f.prior = h->prior;
-        f.fwd = h->fwd;
-        f.bwd = h->bwd;
-        f.logZ = h->logZ;
-        f.flags = h->flags;
-        // Sequential recursion (the chunked, parallel-in-time variant multiplies emission ratios of ~1e-30
-        // along 32-64 steps in FP32 and loses whole rows -- measured).  Few chains: the multi-warp kernel
-        // also for 32 < N <= 64 (one output per lane: 0.46 -> 0.38 ms for 2 chains of 2000 steps at
-        // N = 40; with ~1000 chains it measured 3 % slower).
-        f.wide = M <= 64 ? 2 : 1;
-        TCU(h, launch_fb(f, h->st));
+        {   // FP64 chain recursion per source (forward and backward warps), A in shared memory
+            const size_t smem = ((size_t)N * N + 4 * (size_t)N) * 8;
+            TCU(h, ensure_dyn_smem((const void *)train_fb_kernel, smem));
+            train_fb_kernel<<<M, 64, smem, h->st>>>(T, N, h->ec, h->eoff, h->A, h->prior, h->fwd, h->bwd, h->logZ, h->flags);
+            TCU(h, cudaGetLastError());
+        }
         trace_kernel<<<(M + 127) / 128, 128, 0, h->st>>>(M, h->iters, h->max_iters, h->logZ, h->trace);
         posterior_kernel<<<(MT + 7) / 8, 256, 0, h->st>>>(T, N, MT, h->fwd, h->bwd, h->ec, h->A, h->gamma, h->Zt);
         xi_kernel<<<dim3((M * N * N + 255) / 256, nch), 256, 0, h->st>>>(T, N, M, TCHUNK, h->fwd, h->bwd, h->ec, h->Zt, h->A,
@@ -534,11 +655,11 @@ int nhmm_train_em(nhmm_train_t *h, int32_t n_iters) {
             default: e = launch_beta<32>(F, T, N, K, M, TCHUNK, h->V, h->beta, h->theta, h->gamma, h->nb, h->st); break;
         }
         TCU(h, e);
-        beta_norm_kernel<<<(M * N * K + 7) / 8, 256, 0, h->st>>>(F, T, N, K, M * N * K, nch, h->nb, h->gamma, h->beta);
+        beta_norm_kernel<<<(M * N * K + 7) / 8, 256, 0, h->st>>>(F, T, N, K, M * N * K, nch, h->nb, h->beta);
         mstep_kernel<<<(MT * N + 255) / 256, 256, 0, h->st>>>(T, N, K, M, nch, h->theta, h->C, h->xi, h->A, h->prior,
                                                               h->gamma);
         TCU(h, cudaGetLastError());
-        h->launches += 10;
+        h->launches += 9;
         h->iters++;
     }
     return t_flags(h);
