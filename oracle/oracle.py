@@ -17,7 +17,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "nfhmm_oracle.c")
-_SRCS = [_SRC, os.path.join(_HERE, "nhmm_em_oracle.c")]   # VB iteration; N-HMM EM training (NEXT-3)
+_SRCS = [_SRC, os.path.join(_HERE, "nhmm_em_oracle.c"),   # VB iteration; N-HMM EM training (NEXT-3)
+         os.path.join(_HERE, "stft_oracle.c")]                   # STFT front end / resynthesis (NEXT-4)
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 OR_OK, OR_EINVAL, OR_EZEROSUPPORT, OR_ENUMERIC = 0, -1, -5, -6
@@ -56,6 +57,8 @@ def lib():
         L.or_fb_pairwise.argtypes = [i, i, P, P, P, P, P, P]
         L.or_nhmm_loglik.argtypes = [i, i, i, i, P, P, P, P]
         L.or_nhmm_em_step.argtypes = [i, i, i, i, P, P, P, P, P, P]
+        L.or_stft.argtypes = [P, i, i, i, d, P, P]
+        L.or_istft.argtypes = [P, P, i, i, i, P, i]
         _lib = L
     return _lib
 
@@ -218,3 +221,28 @@ def nhmm_em(V, beta, theta, A, pi, n_iters):
         _check(lib().or_nhmm_em_step(F, T, N, K, _p(v), _p(b), _p(th), _p(a), _p(p), ctypes.byref(lz)))
         ll[i] = lz.value
     return dict(beta=b, theta=th, A=a, pi=p, loglik=ll)
+
+
+# ---- STFT front end and resynthesis (stft_oracle.c) -------------------------------------
+
+def stft(x, win, hop, gain=1.0):
+    """x [n_samples] (one signal) -> (X [T][F] complex128, V [T][F] = gain |X|)."""
+    xs = _f32(x)
+    n = xs.shape[0]
+    T = 1 + (n - win) // hop
+    F = win // 2 + 1
+    X = np.empty((T, F, 2))
+    V = np.empty((T, F))
+    _check(lib().or_stft(_p(xs), n, win, hop, float(gain), _p(X), _p(V)))
+    return X[..., 0] + 1j * X[..., 1], V
+
+
+def istft(X, M, win, hop, n_samples):
+    """X [T][F] complex mixture STFT, M [T][F] magnitudes -> y [n_samples] (mixture phase, weighted OLA)."""
+    Xc = np.asarray(X)
+    Xr = np.ascontiguousarray(np.stack([Xc.real, Xc.imag], -1), dtype=np.float64)
+    Mm = _f64(M)
+    T = Xr.shape[0]
+    y = np.empty(n_samples)
+    _check(lib().or_istft(_p(Xr), _p(Mm), T, win, hop, _p(y), n_samples))
+    return y
