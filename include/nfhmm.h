@@ -177,6 +177,31 @@ int nfhmm_profile_read(nfhmm_t *h, double *ms, int64_t *launches);
 int nfhmm_bench_kernel(nfhmm_t *h, int cls, int32_t reps, double *ms_per_launch);
 
 /* ---------------------------------------------------------------------------------------------------
+ * Spectrogram front end and resynthesis back end.  Stateless calls on `device`
+ * and `stream` (cudaStream_t or NULL); arrays may be host or device pointers (host ones are staged);
+ * both synchronise the stream before returning.  Window: periodic Hann w[n] = 1/2 - 1/2 cos(2 pi n / win),
+ * DFT length = win (a power of two, 2 .. 4096), hop <= win (DESIGN R23); the paper's analysis is
+ * win = 1024, hop = 256 at 16 kHz ("a window size of 64ms and a hop size of 16ms").
+ *
+ * nfhmm_stft ("A spectrogram is the magnitude of the short-time Fourier transform"):
+ *   x [n_sig][n_samples] FP32 waveforms (n_samples >= win, n_sig <= 65535);
+ *   T = 1 + (n_samples - win) / hop frames, F = win / 2 + 1 bins;
+ *   X [n_sig][T][F] complex64 as interleaved (re, im) FP32 pairs:  X_t[k] = sum_n w[n] x[t hop + n] e^{-2 pi i k n / win}
+ *   V [n_sig][T][F] FP32 quanta  V = gain |X|  (the observations of nfhmm_set_observations);
+ *   either output may be NULL (not both); gain > 0.
+ * nfhmm_istft ("go back to the time domain ... using the phase of the original mixture"):
+ *   X [n_mix][T][F] complex64 mixture STFT (from nfhmm_stft), M [n_mix][S][T][F] per-source magnitudes in
+ *   quanta (e.g. V* of nfhmm_separate; divided by gain), y [n_mix][S][n_samples] out:
+ *   Y = (M / gain) X / |X| (0 where X = 0), y_t = real inverse DFT / win, and the weighted overlap-add
+ *   y[n] = sum_t w[n - t hop] y_t[n - t hop] / sum_t w[n - t hop]^2 (0 where no frame covers n).
+ *   With M = V of nfhmm_stft, y = x wherever the windows cover x.
+ * Errors: NFHMM_EINVAL (sizes, NULL, gain <= 0, win not a power of two), NFHMM_ECUDA. */
+int nfhmm_stft(const float *x, int64_t n_sig, int64_t n_samples, int32_t win, int32_t hop, float gain, float *X, float *V,
+               int32_t device, void *stream);
+int nfhmm_istft(const float *X, const float *M, int64_t n_mix, int32_t S, int64_t T, int32_t win, int32_t hop,
+                float gain, float *y, int64_t n_samples, int32_t device, void *stream);
+
+/* ---------------------------------------------------------------------------------------------------
  * N-HMM maximum-likelihood EM training: learns each source's dictionaries,
  * transition matrix and initial distribution from an isolated-source spectrogram, the step before the
  * separation path.  The paper gives only "maximum-likelihood (ML) values of all these parameters may be

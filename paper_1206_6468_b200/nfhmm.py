@@ -62,6 +62,9 @@ SIGNATURES = {
     "nfhmm_bench_kernel": (ctypes.c_int, [_P, ctypes.c_int, _I32, ctypes.POINTER(_D)]),
     "nfhmm_layout": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32),
                                     ctypes.POINTER(_I32)]),
+    # spectrogram front end / resynthesis
+    "nfhmm_stft": (ctypes.c_int, [_P, _I64, _I64, _I32, _I32, ctypes.c_float, _P, _P, _I32, _P]),
+    "nfhmm_istft": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I32, _I32, ctypes.c_float, _P, _I64, _I32, _P]),
     # N-HMM EM training
     "nhmm_train_create": (ctypes.c_int, [_I64, _I64, _I32, _I32, _I64, _I32, _I32, _P, ctypes.POINTER(_P)]),
     "nhmm_train_set_data": (ctypes.c_int, [_P, _P]),
@@ -320,6 +323,46 @@ class NFHMM:
         vs = np.empty((M, S, T, F), np.float32) if V_src else None
         nfhmm_separate(self.h, vst, vs)
         return (vst, vs) if V_src else vst
+
+
+# ---- spectrogram front end / resynthesis (include/nfhmm.h nfhmm_stft / nfhmm_istft) ------
+
+def _stream_ptr(stream, device):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream(device).cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+
+
+def stft(x, win=1024, hop=256, gain=1.0, device=0, stream=None, want_X=True, want_V=True):
+    """x [n_sig][n_samples] float32 (numpy or torch) -> dict(X [n_sig][T][F] complex64, V [n_sig][T][F]),
+    computed by libnfhmm's kernels (nfhmm_stft); outputs are host numpy arrays."""
+    x = np.ascontiguousarray(x, np.float32) if isinstance(x, np.ndarray) else x
+    if x.ndim == 1:
+        x = x[None]
+    n_sig, n = x.shape
+    T, F = 1 + (n - win) // hop, win // 2 + 1
+    X = np.empty((n_sig, T, F), np.complex64) if want_X else None
+    V = np.empty((n_sig, T, F), np.float32) if want_V else None
+    st = _lib.nfhmm_stft(_ptr(x), n_sig, n, win, hop, gain, _ptr(X), _ptr(V), device, _stream_ptr(stream, device))
+    if st != NFHMM_OK:
+        raise NFHMMError(st, _lib.nfhmm_strerror(st).decode())
+    return dict(X=X, V=V)
+
+
+def istft(X, M, n_samples, win=1024, hop=256, gain=1.0, device=0, stream=None):
+    """X [n_mix][T][F] complex64 mixture STFT, M [n_mix][S][T][F] magnitudes in quanta -> y [n_mix][S][n_samples]
+    (nfhmm_istft: the mixture's phase, weighted overlap-add)."""
+    X = np.ascontiguousarray(X, np.complex64)
+    M = np.ascontiguousarray(M, np.float32)
+    n_mix, T, F = X.shape
+    S = M.shape[1]
+    y = np.empty((n_mix, S, n_samples), np.float32)
+    st = _lib.nfhmm_istft(_ptr(X), _ptr(M), n_mix, S, T, win, hop, gain, _ptr(y), n_samples, device,
+                          _stream_ptr(stream, device))
+    if st != NFHMM_OK:
+        raise NFHMMError(st, _lib.nfhmm_strerror(st).decode())
+    return y
 
 
 # ---- N-HMM EM training (SURVEY NEXT-3; include/nfhmm.h nhmm_train_*) --------------------------------
