@@ -1034,6 +1034,223 @@ cudaError_t launch_fb_multi(const FBArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------------
+// Tensor-core forward-backward for many chains per source (round 2): the chains of one source share A_s,
+// so one step of 16 chains is a [16 x N] x [N x N] matrix product -- warp-level mma.sync m16n8k8 TF32 with
+// the 3xTF32 split (a_lo b_hi + a_hi b_lo + a_hi b_hi, as the GEMMs; FP32 accumulation).  One CTA per
+// (source, direction, 16 chains) with one warp per 8-state column tile (N = 8 NT: NT warps); each warp
+// keeps its column tile of A (hi / lo fragments) in registers for the whole recursion, reads the previous
+// messages of all 16 chains from a shared tile as A-operand fragments, and publishes its 8 columns of the
+// new messages and their row-sum partials; one named barrier per step.  The three products accumulate
+// separately (mma.sync's latency on sm_100 is long: NT-deep chains).  Same recursions and scaling as
+// fb_kernel (power-of-two scale from the previous message's row sum):
+//   forward u_t = ((u_{t-1} A) 2^-E) .* e_t;  backward b_t = (x_{t+1} A^T) 2^-E, x_t = e_t .* b_t.
+constexpr int FBT_D = 8;   // emission ring depth (steps)
+
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// hi = x rounded to TF32 (nearest, ties away: two integer ops); lo = x - hi exactly (the MMA reads its top
+// 19 bits -- a truncation 2^-11 below lo, i.e. 2^-22 of x)
+__device__ __forceinline__ uint32_t tf32_hi_bits(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
+
+template <int NT>   // N = 8 NT states, NT warps
+struct FBTCfg {
+    static constexpr int N = 8 * NT, LD = N + 4;   // operand tile row pitch (floats; +4 staggers the banks)
+    static constexpr int OP = 16 * LD;
+    static constexpr int RING = 16 * 8;            // one warp's emission slot: 16 rows x its 8 columns
+    static constexpr int FLOATS = 4 * OP + 2 * NT * 16 + NT * FBT_D * RING;   // op tiles (hi, lo) x 2 | row sums | rings
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT * 32) fb_mma_kernel(FBArgs p) {
+    using C_ = FBTCfg<NT>;
+    constexpr int N = C_::N, LD = C_::LD, OP = C_::OP, RING = C_::RING;
+    extern __shared__ __align__(16) float sm[];
+    uint32_t *opb = reinterpret_cast<uint32_t *>(sm);   // [2][hi, lo][16][LD] operand tiles, already split
+    float *rsp = sm + 4 * OP;                     // [2][NT][16] row-sum partials
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float *ring = rsp + 2 * NT * 16 + warp * FBT_D * RING;   // this warp's [FBT_D][16][8] emissions
+    const int groups = (p.M + 15) / 16;
+    const int s = blockIdx.x / (2 * groups), rem = blockIdx.x - s * 2 * groups;
+    const bool backward = rem >= groups;
+    const int m0 = (backward ? rem - groups : rem) * 16;
+    const int T = p.T;
+    const int g = lane >> 2, tq = lane & 3;
+    const int rows_valid = min(16, p.M - m0);
+    const int col = 8 * warp + 2 * tq;            // this thread's two columns
+    const float *Ag = p.trans + (size_t)s * N * N;
+    // B fragments of column tile `warp`: forward B[k][n] = A[k][n]; backward B[k][n] = A[n][k];
+    // b0 = (k = 8j + tq, n = 8 warp + g), b1 = (k = 8j + tq + 4, n = 8 warp + g)
+    uint32_t bh[NT][2], bl[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k = 8 * j + tq + 4 * h, n = 8 * warp + g;
+            const float v = backward ? Ag[n * N + k] : Ag[k * N + n];
+            const uint32_t hi = tf32_hi_bits(v);
+            bh[j][h] = hi;
+            bl[j][h] = __float_as_uint(v - __uint_as_float(hi));
+        }
+    const int rA = g, rB = g + 8;
+    const bool vA = rA < rows_valid, vB = rB < rows_valid;
+    const size_t chA = (size_t)(m0 + (vA ? rA : 0)) * p.S + s, chB = (size_t)(m0 + (vB ? rB : 0)) * p.S + s;
+    float *outp = backward ? p.bwd : p.fwd;
+    const int dtN = backward ? -N : N;   // message pointers advance one row per step
+    float *oA = outp + chA * T * N + col + (size_t)(backward ? T - 1 : 0) * N;
+    float *oB = outp + chB * T * N + col + (size_t)(backward ? T - 1 : 0) * N;
+    const float pr0 = backward ? 0.f : p.prior[s * N + col], pr1 = backward ? 0.f : p.prior[s * N + col + 1];
+    // emission ring: lane = (row lane / 2, half lane % 2) -> one 16-byte chunk of its row's 8 columns
+    const int er = lane >> 1;
+    const int err = er < rows_valid ? er : 0;
+    // step kk's emission row e_t (t = t_first + dt kk) goes to ring slot kk % FBT_D
+    const int t_first = backward ? T - 1 : 0;
+    const float *esrc = p.ec + ((size_t)(m0 + err) * p.S + s) * T * N + 8 * warp + 4 * (lane & 1) + (size_t)t_first * N;
+    const unsigned edst = (unsigned)__cvta_generic_to_shared(ring + er * 8 + 4 * (lane & 1));
+    auto stage = [&](int kk) {
+        if (kk < T)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(edst + (unsigned)((kk & (FBT_D - 1)) * RING * 4)),
+                         "l"(esrc + (ptrdiff_t)kk * dtN));
+        cp_async_commit();
+    };
+    for (int kk = 0; kk < FBT_D - 1; ++kk) stage(kk);
+    unsigned bad = 0;
+    int EA = 0, EB = 0;              // exponents of the operand rows' sums (applied at the next step)
+    int esumA = 0, esumB = 0;        // forward: applied exponents (log Z)
+    float sumA = 0.f, sumB = 0.f;    // the last operand row sums (forward: sum u_{T-1})
+    const unsigned bar_n = NT * 32;
+    for (int k = 0; k < T; ++k) {
+        stage(k + FBT_D - 1);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(FBT_D - 1));
+        __syncwarp();
+        const float *et = ring + (k & (FBT_D - 1)) * RING;
+        const float2 ea = *reinterpret_cast<const float2 *>(et + rA * 8 + 2 * tq);
+        const float2 eb = *reinterpret_cast<const float2 *>(et + rB * 8 + 2 * tq);
+        float c[4];   // (rA, col), (rA, col+1), (rB, col), (rB, col+1)
+        if (k == 0) {
+            if (backward) {
+                c[0] = c[1] = c[2] = c[3] = 1.f;
+            } else {   // u_0 = pi .* e_0 (unscaled)
+                c[0] = pr0 * ea.x;
+                c[1] = pr1 * ea.y;
+                c[2] = pr0 * eb.x;
+                c[3] = pr1 * eb.y;
+            }
+        } else {
+            const uint32_t *oph = opb + ((k - 1) & 1) * 2 * OP, *opl = oph + OP;
+            float ch[4] = {0.f, 0.f, 0.f, 0.f}, cl[4] = {0.f, 0.f, 0.f, 0.f}, cm[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                const int o0 = rA * LD + 8 * j + tq, o1 = rB * LD + 8 * j + tq;
+                const uint32_t ah[4] = {oph[o0], oph[o1], oph[o0 + 4], oph[o1 + 4]};
+                const uint32_t al[4] = {opl[o0], opl[o1], opl[o0 + 4], opl[o1 + 4]};
+                mma_tf32(cl, al, bh[j][0], bh[j][1]);
+                mma_tf32(cm, ah, bl[j][0], bl[j][1]);
+                mma_tf32(ch, ah, bh[j][0], bh[j][1]);
+            }
+            const float scA = pow2_neg(EA), scB = pow2_neg(EB);
+            if (!backward) {
+                esumA += EA;
+                esumB += EB;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) c[r] = (ch[r] + (cl[r] + cm[r])) * (r < 2 ? scA : scB);
+            if (!backward) {   // u_t = (u_{t-1} A) 2^-E .* e_t
+                c[0] *= ea.x;
+                c[1] *= ea.y;
+                c[2] *= eb.x;
+                c[3] *= eb.y;
+            }
+        }
+        // messages out; the next operand (u_t, or x_t = e_t .* b_t) into the tile; row-sum partials
+        if (vA) *reinterpret_cast<float2 *>(oA) = make_float2(c[0], c[1]);
+        if (vB) *reinterpret_cast<float2 *>(oB) = make_float2(c[2], c[3]);
+        oA += dtN;
+        oB += dtN;
+        if (backward) {
+            c[0] *= ea.x;
+            c[1] *= ea.y;
+            c[2] *= eb.x;
+            c[3] *= eb.y;
+        }
+        {   // the producer splits its own values: the consumers read hi and lo fragments directly
+            uint32_t *oh = opb + (k & 1) * 2 * OP, *ol = oh + OP;
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                h[r] = tf32_hi_bits(c[r]);
+                l[r] = __float_as_uint(c[r] - __uint_as_float(h[r]));
+            }
+            *reinterpret_cast<uint2 *>(oh + rA * LD + col) = make_uint2(h[0], h[1]);
+            *reinterpret_cast<uint2 *>(oh + rB * LD + col) = make_uint2(h[2], h[3]);
+            *reinterpret_cast<uint2 *>(ol + rA * LD + col) = make_uint2(l[0], l[1]);
+            *reinterpret_cast<uint2 *>(ol + rB * LD + col) = make_uint2(l[2], l[3]);
+        }
+        float pa = c[0] + c[1], pb = c[2] + c[3];
+        pa += __shfl_xor_sync(0xffffffffu, pa, 1);
+        pa += __shfl_xor_sync(0xffffffffu, pa, 2);
+        pb += __shfl_xor_sync(0xffffffffu, pb, 1);
+        pb += __shfl_xor_sync(0xffffffffu, pb, 2);
+        float *rp = rsp + (k & 1) * NT * 16;
+        if (tq == 0) {
+            rp[warp * 16 + rA] = pa;
+            rp[warp * 16 + rB] = pb;
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"r"(bar_n) : "memory");
+        float ta = 0.f, tb = 0.f;   // the rows' full sums, column tiles in a fixed order
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            ta += rp[i * 16 + rA];
+            tb += rp[i * 16 + rB];
+        }
+        if ((vA && (!(ta > 0.f) || !(ta < INFINITY))) || (vB && (!(tb > 0.f) || !(tb < INFINITY)))) bad |= FLAG_NONFINITE;
+        EA = ta > 0.f ? exponent_of(ta) : 0;
+        EB = tb > 0.f ? exponent_of(tb) : 0;
+        sumA = ta;
+        sumB = tb;
+    }
+    cp_async_wait_all();
+    if (!backward && warp == 0) {   // log Z = ln(sum u_{T-1}) + ln 2 sum E + sum_t eoff_t, per row
+        double oa = 0.0, ob = 0.0;
+        for (int tt = tq; tt < T; tt += 4) {
+            if (vA) oa += p.eoff[chA * T + tt];
+            if (vB) ob += p.eoff[chB * T + tt];
+        }
+        oa += __shfl_xor_sync(0xffffffffu, oa, 1);
+        oa += __shfl_xor_sync(0xffffffffu, oa, 2);
+        ob += __shfl_xor_sync(0xffffffffu, ob, 1);
+        ob += __shfl_xor_sync(0xffffffffu, ob, 2);
+        if (tq == 0) {
+            if (vA) {
+                const double lz = log((double)sumA) + (double)esumA * 0.69314718055994530942 + oa;
+                p.logZ[chA] = lz;
+                if (!isfinite(lz)) bad |= FLAG_NONFINITE;
+            }
+            if (vB) {
+                const double lz = log((double)sumB) + (double)esumB * 0.69314718055994530942 + ob;
+                p.logZ[chB] = lz;
+                if (!isfinite(lz)) bad |= FLAG_NONFINITE;
+            }
+        }
+    }
+    if (bad) atomicOr(p.flags, bad);
+}
+
+template <int NT>
+cudaError_t launch_fb_mma(const FBArgs &a, cudaStream_t st) {
+    using C_ = FBTCfg<NT>;
+    const size_t smem = (size_t)C_::FLOATS * 4;
+    cudaError_t e = ensure_dyn_smem((const void *)fb_mma_kernel<NT>, smem);
+    if (e != cudaSuccess) return e;
+    fb_mma_kernel<NT><<<a.S * 2 * ((a.M + 15) / 16), NT * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+bool fb_mma_supported(int N, int64_t M, int nchunk) { return nchunk <= 1 && M >= 16 && (N == 40 || N == 48 || N == 32 || N == 64 || N == 24 || N == 16); }
+
 bool fb_multi_supported(int N, int64_t M, int nchunk) {
     return nchunk <= 1 && M >= 2 && (N == 40 || N == 36 || N == 48 || N == 8 || N == 4 || N == 16);
 }
@@ -1070,7 +1287,16 @@ int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len) {
 
 cudaError_t launch_fb(const FBArgs &a, cudaStream_t st) {
     const int N = a.N;
-    // many chains per source: C chains per warp with the remainder states spread over the lanes
+    // many chains per source: 16 chains per warp on the tensor cores (multi == 2, default), or C chains per
+    // warp with the remainder states spread over the lanes (multi == 1)
+    if (a.multi == 2 && fb_mma_supported(N, a.M, a.nchunk)) {
+        if (N == 40) return launch_fb_mma<5>(a, st);
+        if (N == 48) return launch_fb_mma<6>(a, st);
+        if (N == 32) return launch_fb_mma<4>(a, st);
+        if (N == 64) return launch_fb_mma<8>(a, st);
+        if (N == 24) return launch_fb_mma<3>(a, st);
+        if (N == 16) return launch_fb_mma<2>(a, st);
+    }
     if (a.multi && fb_multi_supported(N, a.M, a.nchunk)) {
         if (N == 40) return launch_fb_multi<1, 8>(a, st);
         if (N == 36) return launch_fb_multi<1, 4>(a, st);

@@ -54,7 +54,7 @@ struct nfhmm {
     double *spsT = nullptr, *sps2T = nullptr, *hpartT = nullptr;
     // parallel-in-time forward-backward (few chains): chunks, their transfer matrices and start messages
     int fb_nchunk = 0, fb_len = 0;
-    int fb_multi = 1;   // several chains per warp (fb_multi_kernel) where N allows it (NFHMM_FB_MULTI=0: off)
+    int fb_multi = 1;   // chains per warp: 1 FFMA2 multi-chain (default), 2 tensor-core kernel, 0 one (NFHMM_FB_MULTI)
     float *fbP = nullptr, *fbPT = nullptr, *fbF = nullptr, *fbB = nullptr;
     int *fbE = nullptr;
     // CUDA graphs of one sweep (mid: alpha not stored; last: alpha stored), replayed on an internal stream
@@ -583,14 +583,17 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         const char *ew = getenv("NFHMM_FB_WIDE");
         h->fb_wide = (ew && atoi(ew) == 0) ? 0 : 1;
         const char *em = getenv("NFHMM_FB_MULTI");
-        h->fb_multi = (em && atoi(em) == 0) ? 0 : 1;
+        // (the tensor-core kernel, NFHMM_FB_MULTI=2, measured 68 vs 90 ms per step alone but needs >= 16 SMs
+        // beside the reconstruction GEMM and measured no faster there: 77.9 vs 80.1 M frame-iterations/s)
+        h->fb_multi = em ? atoi(em) : 1;
+        if (h->fb_multi < 0 || h->fb_multi > 2) h->fb_multi = 1;
         // Large batches (> 65,536 frames, sequential forward-backward): the reconstruction GEMM leaves 32
         // SMs to the forward-backward running beside it (measured at config 3: 16 / 24 / 32 / 40 / 48 / 64
         // reserved SMs -> -5 / -6 / +1.9 / +1.6 / -0.2 / -4.7 %).  NFHMM_OVERLAP=n overrides (0 = off).
         const char *eo = getenv("NFHMM_OVERLAP");
         // (with the multi-chain forward-backward, round 2: 0 / 20 / 24 / 32 / 40 SMs -> 72.8 / 78.8 / 82.6 /
         // 81.8 / 79.9 M frame-iterations/s; the one-chain kernel keeps 32)
-        h->overlap_sms = (h->math == NFHMM_MATH_TC && frames > 65536 && h->fb_nchunk == 0) ? ((h->fb_multi && fb_multi_supported(h->N, h->M, 0)) ? 24 : 32) : 0;
+        h->overlap_sms = (h->math == NFHMM_MATH_TC && frames > 65536 && h->fb_nchunk == 0) ? ((h->fb_multi == 2 && fb_mma_supported(h->N, h->M, 0)) ? 16 : (h->fb_multi && fb_multi_supported(h->N, h->M, 0)) ? 24 : 32) : 0;
         if (eo) h->overlap_sms = h->math == NFHMM_MATH_TC ? atoi(eo) : 0;
         if (h->overlap_sms < 0 || h->overlap_sms > 64) h->overlap_sms = 0;
     }

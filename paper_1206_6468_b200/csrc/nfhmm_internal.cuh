@@ -133,7 +133,8 @@ struct FBArgs {
     unsigned *flags;
     int wide;                 // multi-warp kernel per chain and direction: 1 for N > 64 (default), 2 also for
                               // 32 < N <= 64 (few chains), 0 never
-    int multi;                // 1: several chains of one source per warp (fb_multi_kernel) where N allows it
+    int multi;                // 2: 16 chains of one source per warp on the tensor cores (fb_mma_kernel),
+                              // 1: several chains per warp with FFMA2 (fb_multi_kernel), 0: one chain per warp
     // parallel-in-time path (fbp_*): nchunk chunks of chunk_len steps; exact chunk-start messages
     int nchunk, chunk_len;    // nchunk <= 1: one sequential pass over [0, T)
     float *fstart;            // [M*S][nchunk][NMAX]  u_{t0} of each chunk (scratch)
@@ -146,6 +147,8 @@ struct FBArgs {
 int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len);
 // multi-chain kernel (fb_multi_kernel) for this shape: N = 32 Q + R with R | 32 among the compiled ones
 bool fb_multi_supported(int N, int64_t M, int nchunk);
+// tensor-core kernel (fb_mma_kernel, 16 chains per warp, mma.sync 3xTF32) for this shape: N = 8 NT
+bool fb_mma_supported(int N, int64_t M, int nchunk);
 cudaError_t launch_fb(const FBArgs &a, cudaStream_t st);
 
 struct ElboArgs {

@@ -262,13 +262,19 @@ def test_fb_overlap_is_bitwise_neutral(graphs, monkeypatch):
         assert np.array_equal(ov[key], seq[key]), key
 
 
-@pytest.mark.parametrize("c,over", [(3, dict(T=40, M=21)), (0, dict(T=60, M=20)), (2, dict(T=30, M=13))])
+@pytest.mark.parametrize("c,over", [(3, dict(T=40, M=21)), (0, dict(T=60, M=20)), (2, dict(T=30, M=13)),
+                                    (3, dict(T=35, M=37, N=24))])
 def test_multi_chain_forward_backward(c, over, monkeypatch):
     """> 32 chains: the multi-chain forward-backward (C chains of one source per warp, the N = 32 Q + R
     remainder states spread over the lanes; M not a multiple of C leaves a partly empty group) agrees
     with the one-chain-per-warp kernel and with the oracle."""
     cfg, model, V = make_inputs(c, **over)
     multi = run_gpu(cfg, model, V, 4)
+    if cfg.N % 8 == 0 and V.shape[0] >= 16:   # tensor-core variant (16 chains per warp, mma.sync 3xTF32)
+        monkeypatch.setenv("NFHMM_FB_MULTI", "2")
+        tcv = run_gpu(cfg, model, V, 4)
+        for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
+            assert rel_l2(tcv[key], multi[key]) <= 2e-6, key
     monkeypatch.setenv("NFHMM_FB_MULTI", "0")
     one = run_gpu(cfg, model, V, 4)
     for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
