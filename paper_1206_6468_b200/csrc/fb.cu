@@ -832,6 +832,9 @@ cudaError_t launch_fb_t(const FBArgs &a, cudaStream_t st) {
 //   log Z = ln(sum u_{T-1}) + ln 2 sum_t E_t + sum_t eoff_t.
 // The emissions of the next FBM_D steps (all C chains) are staged in a per-warp cp.async ring.
 constexpr int FBM_D = 8;   // emission ring depth (steps)
+#ifndef FBM_MINB
+#define FBM_MINB 1   // min resident warps per SM asked of ptxas (16: <= 128 registers)
+#endif
 
 template <int Q, int R>
 struct FBMCfg {
@@ -843,7 +846,7 @@ struct FBMCfg {
 };
 
 template <int Q, int R>
-__global__ void __launch_bounds__(32) fb_multi_kernel(FBArgs p) {
+__global__ void __launch_bounds__(32, FBM_MINB) fb_multi_kernel(FBArgs p) {
     using C_ = FBMCfg<Q, R>;
     constexpr int C = C_::C, NM = C_::NM, SLOT = C_::SLOT;
     constexpr int CHUNKS = SLOT / 4, CPL = (CHUNKS + 31) / 32;   // 16-byte emission chunks per step, per lane
