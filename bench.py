@@ -428,6 +428,8 @@ def run_ours(args):
             elb = pdist.max_over_ranks(elb, device=f"cuda:{dev}")
         value_bound_off = frame_iters / (elb / args.steps / 1000.0)
         hb.close()
+        del hb
+        torch.cuda.empty_cache()
 
     # ---- e2e: public API with host buffers, copies inside the timed region -------------------
     # Every step copies its V from pinned host memory, runs the sweeps and the separation, and reads

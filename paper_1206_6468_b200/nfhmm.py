@@ -252,6 +252,7 @@ class NFHMM:
         if getattr(self, "h", None):
             nfhmm_destroy(self.h)
             self.h = None
+        self.workspace = None   # the device memory goes back to torch's allocator with the handle
 
     def __del__(self):
         try:
