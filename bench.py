@@ -253,8 +253,8 @@ def run_reference(args):
 
 
 def gather_results(h, cfg, iters, M, world, rank, dev, elapsed_ms):
-    """NCCL gathers after the timed region: free-energy traces (all_gather), d_hat (to rank 0, global
-    mixture order) and the per-rank device times.  Returns a summary for the JSON line: sizes, the
+    """NCCL gathers after the timed region: free-energy traces, d_hat (global mixture order) and the
+    per-rank device times (all_gather_into_tensor).  Returns a summary for the JSON line: sizes, the
     gather's device time and digests of the gathered arrays (equal digests across --gpus N = the
     per-mixture results do not depend on the sharding)."""
     import hashlib
@@ -276,19 +276,20 @@ def gather_results(h, cfg, iters, M, world, rank, dev, elapsed_ms):
         pad = lambda x: torch.cat([x, x.new_zeros((rows - x.shape[0],) + tuple(x.shape[1:]))]) if x.shape[0] < rows else x  # noqa: E731
         fe_all = torch.empty((world * rows, iters), dtype=torch.float64, device=f"cuda:{dev}")
         dist.all_gather_into_tensor(fe_all, pad(fe_d))
-        d_all = torch.empty((world * rows, S, T, N), dtype=torch.float32, device=f"cuda:{dev}") if rank == 0 else None
-        dist.gather(pad(d), [d_all[r * rows:(r + 1) * rows] for r in range(world)] if rank == 0 else None, dst=0)
+        # d_hat of every mixture, in global order (all_gather: every rank receives it; rank 0 digests it)
+        d_all = torch.empty((world * rows, S, T, N), dtype=torch.float32, device=f"cuda:{dev}")
+        dist.all_gather_into_tensor(d_all, pad(d))
         times = torch.empty(world, dtype=torch.float64, device=f"cuda:{dev}")
         dist.all_gather_into_tensor(times, torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{dev}"))
         keep = torch.cat([torch.arange(r * rows, r * rows + sizes[r], device=f"cuda:{dev}") for r in range(world)])
         fe_all = fe_all[keep]
-        d_all = d_all[keep] if rank == 0 else None
+        d_all = d_all[keep]
     else:
         fe_all, d_all = fe_d, d
         times = torch.tensor([elapsed_ms], dtype=torch.float64)
     g1.record()
     torch.cuda.synchronize()
-    out = {"collective": "nccl all_gather (free energies, timings) + gather to rank 0 (d_hat)" if world > 1
+    out = {"collective": "nccl all_gather of the free energies, d_hat and the device times" if world > 1
            else "none (1 rank)", "ms": g0.elapsed_time(g1),
            "bytes": int(cfg.M * S * T * N * 4 + cfg.M * iters * 8 + world * 8),
            "rank_ms": [round(float(x), 3) for x in times.cpu().tolist()]}
