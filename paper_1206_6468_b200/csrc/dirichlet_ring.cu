@@ -229,68 +229,63 @@ __global__ void __maxnreg__(RING_MAXREG) dirichlet_ring_kernel(DirichletArgs p, 
         ds = db / N;
         dn = db - ds * N;
     }
-    if (tid == 0) {
+    // one thread of the last warp (whose tail-phase share is the smallest) stores theta; its warp issues
+    // the loads (the store thread first waits until its previous store has read the stage)
+    constexpr int IO_WARP = NW - 1;
+    const bool io_warp = warp == IO_WARP, io_thread = tid == IO_WARP * 32;
+    if (io_thread) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
 
-    auto issue = [&](int tile, int st) {   // thread 0: the tile's inputs into stage st
+    // warp IO_WARP: the tile's inputs into stage st, one bulk copy per lane (n rows | fc rows | u, b rows
+    // per (run of consecutive t inside one mixture, source))
+    auto issue = [&](int tile, int st) {
         unsigned char *sb = smem_raw + st * L.stage;
         float *nb = reinterpret_cast<float *>(sb + L.n);
         float *ub = reinterpret_cast<float *>(sb + L.u);
         float *bb = reinterpret_cast<float *>(sb + L.b);
         const int f0 = tile * FT, nf = min(FT, frames - f0);
-        mbar_expect_tx(&bars[st], (uint32_t)nf * ((uint32_t)Kt * 4 + 8u * (uint32_t)SN + 32u));
-        if (contiguous) {
-            bulk_g2s(nb, n_in + (size_t)f0 * Kt, (uint32_t)nf * Kt * 4, &bars[st]);
-        } else {
-            for (int f = 0; f < nf; ++f) bulk_g2s(nb + (size_t)f * Kt, n_in + (size_t)(f0 + f) * ld, Kt * 4, &bars[st]);
+        if (lane == 0) {
+            bulk_wait_read0();     // the store of the tile that last used this stage has read it
+            fence_async_smem();
+            mbar_expect_tx(&bars[st], (uint32_t)nf * ((uint32_t)Kt * 4 + 8u * (uint32_t)SN + 32u));
         }
-        for (int f = f0; f < f0 + nf;) {   // runs of consecutive t inside one mixture
-            const int m = f / T, t = f - m * T, len = min(f0 + nf - f, T - t);
-            for (int s = 0; s < S; ++s) {
+        __syncwarp();
+        const int m0 = f0 / T, nrun = (f0 + nf - 1) / T - m0 + 1;
+        const int nn = contiguous ? 1 : nf, ncopy = nn + 1 + nrun * S * 2;
+        for (int c = lane; c < ncopy; c += 32) {
+            if (c < nn) {
+                if (contiguous) bulk_g2s(nb, n_in + (size_t)f0 * Kt, (uint32_t)nf * Kt * 4, &bars[st]);
+                else bulk_g2s(nb + (size_t)c * Kt, n_in + (size_t)(f0 + c) * ld, Kt * 4, &bars[st]);
+            } else if (c == nn) {
+                bulk_g2s(sb + L.fc, fconst + 4 * (size_t)f0, (uint32_t)nf * 32, &bars[st]);
+            } else {
+                const int q = c - nn - 1, r = q / (2 * S), s = (q >> 1) - r * S, m = m0 + r;
+                const int fs = max(f0, m * T), fe = min(f0 + nf, (m + 1) * T), t = fs - m * T;
                 const size_t row = ((size_t)(m * S + s) * T + t) * N;
-                const size_t dst = ((size_t)s * FT + (f - f0)) * N;
-                bulk_g2s(ub + dst, u_fwd + row, (uint32_t)len * N * 4, &bars[st]);
-                bulk_g2s(bb + dst, b_bwd + row, (uint32_t)len * N * 4, &bars[st]);
+                const size_t dst = ((size_t)s * FT + (fs - f0)) * N;
+                if (q & 1) bulk_g2s(bb + dst, b_bwd + row, (uint32_t)(fe - fs) * N * 4, &bars[st]);
+                else bulk_g2s(ub + dst, u_fwd + row, (uint32_t)(fe - fs) * N * 4, &bars[st]);
             }
-            f += len;
         }
-        bulk_g2s(sb + L.fc, fconst + 4 * (size_t)f0, (uint32_t)nf * 32, &bars[st]);
     };
-
-    int it = 0;
-    if (tid == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int st = it & 1;
-        const uint32_t parity = (it >> 1) & 1;
-        const int f0 = tile * FT, nf = min(FT, frames - f0), nitems = nf * SN, npairs = nf * S;
-        unsigned char *sb = smem_raw + st * L.stage;
-        float *nb = reinterpret_cast<float *>(sb + L.n);
+    // Eq. 6 normalisers gq[f][s] = gamma / sum_n u b of the tile in stage st: 8 lanes per (frame, source),
+    // fixed-order sums; (frame, source) groups taken from the last warp down (the Eq. 8 phase, which
+    // runs beside it, takes them from warp 0 up)
+    const float invS = 1.f / (float)S;
+    auto normalisers = [&](int tile, int st) {
+        const unsigned char *sb = smem_raw + st * L.stage;
         const float *ub = reinterpret_cast<const float *>(sb + L.u);
         const float *bb = reinterpret_cast<const float *>(sb + L.b);
-        const double *fc = reinterpret_cast<const double *>(sb + L.fc);
-        // every thread is done with the other stage (tile it-1: its fc rows, the theta it stored):
-        // refill it with the next tile once the bulk store out of it has read its bytes
-        __syncthreads();
-        if (tid == 0) {
-            const int nt = tile + gridDim.x;
-            if (nt < ntiles) {
-                bulk_wait_read0();
-                fence_async_smem();
-                issue(nt, st ^ 1);
-            }
-        }
-        mbar_wait(&bars[st], parity);
-
-        // Eq. 6 normalisers gq[f][s] = gamma / sum_n u b: 8 lanes per (frame, source), fixed-order sums
-        for (int pb = warp * (32 / RING_G); pb < npairs; pb += NW * (32 / RING_G)) {
+        const int npairs = min(FT, frames - tile * FT) * S;
+        for (int pb = (NW - 1 - warp) * (32 / RING_G); pb < npairs; pb += NW * (32 / RING_G)) {
             const int pr = pb + grp;
             float q = 0.f;
             if (pr < npairs) {
-                const int f = pr / S, s = pr - f * S;
+                const int f = divq(pr, S, invS), s = pr - f * S;
                 const float *u = ub + ((size_t)s * FT + f) * N, *b = bb + ((size_t)s * FT + f) * N;
                 for (int n = g; n < N; n += RING_G) q = fmaf(u[n], b[n], q);
             }
@@ -302,7 +297,33 @@ __global__ void __maxnreg__(RING_MAXREG) dirichlet_ring_kernel(DirichletArgs p, 
                 gq[pr] = gamma * __frcp_rn(q);
             }
         }
-        __syncthreads();
+    };
+
+    // prologue: the first tile's inputs and normalisers
+    if ((int)blockIdx.x < ntiles) {
+        if (io_warp) issue(blockIdx.x, 0);
+        mbar_wait(&bars[0], 0);
+        normalisers(blockIdx.x, 0);
+    }
+    __syncthreads();
+    // per tile, two CTA barriers: [issue next | element pass] | [store | Eq. 8 | bound | next normalisers]
+    int it = 0;
+    // (mixture, t) of the tile's first frame, advanced incrementally (no division per tile)
+    int m_t0 = (int)((long long)blockIdx.x * FT / T), t_t0 = (int)((long long)blockIdx.x * FT - (long long)m_t0 * T);
+    const long long tstride = (long long)gridDim.x * FT;
+    const int dm = (int)(tstride / T), dt = (int)(tstride - (long long)dm * T);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = it & 1;
+        const int f0 = tile * FT, nf = min(FT, frames - f0), nitems = nf * SN, npairs = nf * S;
+        const int nxt = tile + gridDim.x;
+        unsigned char *sb = smem_raw + st * L.stage;
+        float *nb = reinterpret_cast<float *>(sb + L.n);
+        const float *ub = reinterpret_cast<const float *>(sb + L.u);
+        const float *bb = reinterpret_cast<const float *>(sb + L.b);
+        const double *fc = reinterpret_cast<const double *>(sb + L.fc);
+        // the other stage is free (tile it-1's element pass, Eq. 8 and bound phases read it before the
+        // last barrier; its theta store is awaited inside issue): refill it with the next tile
+        if (io_warp && nxt < ntiles) issue(nxt, st ^ 1);
 
         // element pass: one thread per (frame, block) item; theta replaces n in the stage buffer
         {
@@ -331,7 +352,7 @@ __global__ void __maxnreg__(RING_MAXREG) dirichlet_ring_kernel(DirichletArgs p, 
         }
         fence_async_smem();   // theta (generic writes) before the bulk store (async proxy) reads it
         __syncthreads();
-        if (tid == 0) {
+        if (io_thread) {
             if (contiguous) {
                 bulk_s2g(theta + (size_t)f0 * Kt, nb, (uint32_t)nf * Kt * 4);
             } else {
@@ -344,7 +365,7 @@ __global__ void __maxnreg__(RING_MAXREG) dirichlet_ring_kernel(DirichletArgs p, 
         for (int pb = warp * (32 / RING_G); pb < npairs; pb += NW * (32 / RING_G)) {
             const int pr = pb + grp;
             const bool ok = pr < npairs;
-            const int f = ok ? pr / S : 0, s = pr - f * S;
+            const int f = ok ? divq(pr, S, invS) : 0, s = pr - f * S;
             const double *v = sps + (size_t)f * SN + s * N;
             float mxf = -INFINITY;
             if (ok)
@@ -353,7 +374,8 @@ __global__ void __maxnreg__(RING_MAXREG) dirichlet_ring_kernel(DirichletArgs p, 
             mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, 2));
             mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, 1));
             if (ok) {
-                const int fg = f0 + f, m = fg / T, t = fg - m * T;
+                int m = m_t0, t = t_t0 + f;
+                while (t >= T) t -= T, ++m;
                 const double mx = (double)mxf;
                 float *dst = ec + ((size_t)(m * S + s) * T + t) * N;
                 for (int n = g; n < N; n += RING_G)
@@ -365,8 +387,8 @@ __global__ void __maxnreg__(RING_MAXREG) dirichlet_ring_kernel(DirichletArgs p, 
                 }
             }
         }
-        if (want_h) {   // bound term per frame, 8 lanes each (fixed order)
-            for (int fb = warp * (32 / RING_G); fb < nf; fb += NW * (32 / RING_G)) {
+        if (want_h) {   // bound term per frame, 8 lanes each (fixed order), from the last warp down
+            for (int fb = (NW - 1 - warp) * (32 / RING_G); fb < nf; fb += NW * (32 / RING_G)) {
                 const int f = fb + grp;
                 float h = 0.f;
                 if (f < nf)
@@ -377,8 +399,17 @@ __global__ void __maxnreg__(RING_MAXREG) dirichlet_ring_kernel(DirichletArgs p, 
                 if (f < nf && g == 0) hdir[f0 + f] = (double)h + fc[4 * f + 2];
             }
         }
+        // the next tile's normalisers (its inputs were issued at the top of this tile)
+        if (nxt < ntiles) {
+            mbar_wait(&bars[st ^ 1], ((it + 1) >> 1) & 1);
+            normalisers(nxt, st ^ 1);
+        }
+        m_t0 += dm;
+        t_t0 += dt;
+        while (t_t0 >= T) t_t0 -= T, ++m_t0;
+        __syncthreads();   // gq, sps, hs and this stage are free for the next tile
     }
-    if (tid == 0) bulk_wait0();   // the last theta store has landed before the kernel retires
+    if (io_thread) bulk_wait0();   // the last theta store has landed before the kernel retires
     if (bad) atomicOr(p.flags, bad);
 }
 

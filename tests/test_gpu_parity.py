@@ -287,3 +287,14 @@ def test_multi_chain_forward_backward(c, over, monkeypatch):
         o = run_oracle(cfg, model, V[m], 4)
         assert rel_l2(multi["V_star"][m], o["V_star"]) <= TOL_VSTAR
         assert np.all(np.abs(multi["free_energy"][m] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
+
+
+@pytest.mark.parametrize("chunk", [None, "32"])
+def test_long_single_chain_parallel_scan_fits(chunk, monkeypatch):
+    """One long chain with N = 64 (the parallel-in-time FB's largest state bucket): T = 20,000 frames.
+    With NFHMM_FB_CHUNK=32 the phase-2 scan would need 625 chunks' row scales in shared memory (> 227 KB);
+    fb_pick_chunks grows the chunk length until it fits instead of failing the sweep."""
+    if chunk:
+        monkeypatch.setenv("NFHMM_FB_CHUNK", chunk)
+    cfg, model, V = make_inputs(0, S=1, N=64, K=3, F=33, T=20000, M=1, counts=300)
+    check_parity(cfg, model, V, 3)
