@@ -34,12 +34,15 @@
 // (n = theta .* C) through TMA; STORE (V_hat) and SEPARATE (v_t/alpha_0 scaled V_src^(s)), which run only
 // for posteriors / separation (off the sweep), write directly from registers.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+#include <vector>
 
 #include "dirichlet_math.cuh"
 #include "nfhmm_internal.cuh"
@@ -62,7 +65,13 @@ constexpr int TC_THREADS = 18 * 32;        // 576
 constexpr int TC_MAX_BN = 192;             // 6 x 32-column chunks = 2 per epilogue warp (64 FP32 registers)
 constexpr int EPI_CH = 2;                  // chunks per epilogue warp
 constexpr int A_STAGE_COLS = 2 * TC_KB;    // TMEM columns of one A stage: [hi 16][lo 16]
-constexpr int A_TILE_BYTES = TC_BM * TC_KB * 4;   // 8 KB smem copy of one A stage (TMA, 64-byte swizzle)
+// A stage smem copy: 128 x 16 floats = 8 KB (TMA, 64-byte swizzle); H16: 128 x 32 floats (128-byte swizzle)
+// FP16-split variant of the reconstruction (H16, DESIGN "3xFP16 reconstruction"): 32 k-elements per stage
+// (2 MMAs of K=16 per split product), the A stage's smem copy is 128 x 32 floats (128-byte swizzle) and its
+// TMEM image [hi 16 | lo 16] columns of packed half pairs -- the same 32 TMEM columns and the same B-image
+// bytes per stage as the TF32 kernel
+constexpr int TC_KB16 = 32;
+__host__ __device__ constexpr int a_tile_bytes(bool h16) { return TC_BM * (h16 ? TC_KB16 : TC_KB) * 4; }
 constexpr int EPI_SUB_BYTES = 32 * 16 * 4;        // 2 KB epilogue sub-tile: 32 rows x 16 columns (TMA, 64-byte swizzle)
 constexpr int EPI_TILE_BYTES = 2 * EPI_SUB_BYTES; // per 32-column chunk
 constexpr int MAX_STAGES = 16;            // ring depth cap (narrow tiles: more stages in flight, see stages_for)
@@ -77,7 +86,9 @@ constexpr int SMEM_MAX = 227 * 1024;
 __host__ __device__ constexpr int a_col0(int bn) { return (2 * bn + 31) & ~31; }
 __host__ __device__ constexpr int tmem_a_stages(int bn) { return (512 - a_col0(bn)) / A_STAGE_COLS; }
 // one ring stage = [A copy 8 KB][B hi | B lo], 1 KB aligned (the A swizzle pattern is address-based)
-__host__ __device__ constexpr int stage_bytes_of(int bn) { return (A_TILE_BYTES + 2 * bn * TC_KB * 4 + 1023) & ~1023; }
+__host__ __device__ constexpr int stage_bytes_of(int bn, bool h16 = false) {
+    return (a_tile_bytes(h16) + 2 * bn * TC_KB * 4 + 1023) & ~1023;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -195,6 +206,20 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
 }
+// Same with A/B F16 (kind::f16, K = 16 per instruction)
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {
+    return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 
 __host__ __device__ __forceinline__ float tf32_rn_bits(float x) {
     uint32_t u;
@@ -271,6 +296,7 @@ struct TcParams {
     int splits;             // k-splits (1: no split)
     float *part;
     int ldp;
+    const float *colscale;  // H16: per output column 2^-(15 + s_l) (the B row scale and the A scale undone)
     int dbg;                // performance experiments only (NFHMM_TC_DEBUG): 1 no A loads, 2 no MMAs, 4 no epilogue
                             // I/O, 8 no A TMEM stores, 32 no B loads, 64 no drains, 128 no converter work
 };
@@ -283,7 +309,9 @@ struct Smem {
 // 16-byte chunk c of row r in a TMA tile with 64-B rows, 64-byte swizzle (bits [4,5] ^= bits [7,8])
 __device__ __forceinline__ uint32_t swz64(int r, int c) { return (uint32_t)r * 64u + (uint32_t)((c ^ (r >> 1)) & 3) * 16u; }
 
-template <bool FUSED>   // FUSED: the DIRICHLET epilogue only (a separate instantiation keeps registers down)
+// FUSED: the DIRICHLET epilogue only (a separate instantiation keeps registers down).  H16: FP16-split
+// products (RATIO / STORE / PARTIAL of the reconstruction, A = theta~ in (0, 1])
+template <bool FUSED, bool H16>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmIn,
                    const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmDv,
@@ -291,17 +319,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const int BN = p.bn;
-    const uint32_t b_bytes = (uint32_t)BN * TC_KB * 4;     // one of hi / lo
-    const uint32_t stage_bytes = (uint32_t)stage_bytes_of(BN);
+    constexpr int KB = H16 ? TC_KB16 : TC_KB;               // k-elements per stage
+    constexpr uint32_t A_BYTES = (uint32_t)TC_BM * KB * 4;
+    const uint32_t b_bytes = (uint32_t)BN * TC_KB * 4;     // one of hi / lo (BN x 16 tf32 or BN x 32 halves)
+    const uint32_t stage_bytes = (uint32_t)stage_bytes_of(BN, H16);
     unsigned char *ring = smem_raw + p.ring_off;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mtiles = (p.M + TC_BM - 1) / TC_BM;
     const int splits = p.splits > 1 ? p.splits : 1;
     const int n_total = n_mtiles * p.n_tiles * splits;
-    const int kstart = p.k_begin & ~(TC_KB - 1);          // k-blocks on the global 16-element grid of Bsplit
-    const int kb0 = kstart / TC_KB;
-    const int n_kb = (p.k_end - kstart + TC_KB - 1) / TC_KB;
+    const int kstart = p.k_begin & ~(KB - 1);             // k-blocks on the global KB-element grid of Bsplit
+    const int kb0 = kstart / KB;
+    const int n_kb = (p.k_end - kstart + KB - 1) / KB;
     const int chunk_kb = p.chunk_kb;
     // work unit -> (row tile, column tile) and its k-blocks [kb_lo, kb_hi) (all of them unless split)
     auto unit_of = [&](int tile, int &mt, int &nt, int &ks, int &kb_lo, int &kb_hi) {
@@ -361,6 +391,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     continue;
                 }
                 const unsigned char *ab = ring + (size_t)st * stage_bytes;
+                if constexpr (H16) {
+                    // x' = 2^15 theta~ < 2^15: hi = rn_f16(x'), lo = rn_f16(x' - hi) (the difference is exact in
+                    // FP32), packed in pairs (element 2c in the low half of TMEM column c)
+                    float x[TC_KB16];
+#pragma unroll
+                    for (int c4 = 0; c4 < TC_KB16 / 4; ++c4) {
+                        const float4 v = (p.dbg & 1) ? make_float4(1.f, 1.f, 1.f, 1.f)
+                                                     : *reinterpret_cast<const float4 *>(ab + (uint32_t)t * 128u +
+                                                                                         (uint32_t)((c4 ^ (t & 7)) << 4));
+                        x[4 * c4 + 0] = v.x;
+                        x[4 * c4 + 1] = v.y;
+                        x[4 * c4 + 2] = v.z;
+                        x[4 * c4 + 3] = v.w;
+                    }
+                    const int k0 = kstart + kb * TC_KB16;
+                    if (k0 < p.k_begin || k0 + TC_KB16 > p.k_end) {
+#pragma unroll
+                        for (int i = 0; i < TC_KB16; ++i)
+                            if (k0 + i < p.k_begin || k0 + i >= p.k_end) x[i] = 0.f;
+                    }
+                    uint32_t hi[16], lo[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float a0 = x[2 * i] * 32768.f, a1 = x[2 * i + 1] * 32768.f;
+                        const __half2 h = __floats2half2_rn(a0, a1);
+                        const float2 hf = __half22float2(h);
+                        const __half2 l = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
+                        hi[i] = *reinterpret_cast<const uint32_t *>(&h);
+                        lo[i] = *reinterpret_cast<const uint32_t *>(&l);
+                    }
+                    if (!(p.dbg & 8)) {
+                        tmem_st16(a_base + st * A_STAGE_COLS, hi);
+                        tmem_st16(a_base + st * A_STAGE_COLS + 16, lo);
+                        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                    }
+                } else {
                 float x[TC_KB];
 #pragma unroll
                 for (int c4 = 0; c4 < TC_KB / 4; ++c4) {
@@ -389,6 +455,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     tmem_st16(a_base + st * A_STAGE_COLS + TC_KB, lo);
                     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
                 }
+                }
                 tc_fence_before();
                 mbar_arrive(&S.full[st]);
             }
@@ -415,35 +482,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             };
             auto pf_issue = [&]() {
                 if (pf_tile < n_total && !(p.dbg & 1))
-                    tma_prefetch_2d(&tmA, kstart + pf_kb * TC_KB, pf_mt * TC_BM);
+                    tma_prefetch_2d(&tmA, kstart + pf_kb * KB, pf_mt * TC_BM);
                 if (pf_tile < n_total) pf_advance();
             };
             for (int i = 0; i < A_PREFETCH; ++i) pf_issue();
             for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
                 int mt, nt, ks_, kb_lo, kb_hi;
                 unit_of(tile, mt, nt, ks_, kb_lo, kb_hi);
-                const float *bt = p.Bsplit + (size_t)nt * p.nkb_total * (2 * (size_t)BN * TC_KB);
+                const float *bt = p.Bsplit + (size_t)nt * p.nkb_total * (2 * (size_t)BN * TC_KB);   // same floats per block
                 for (int kb = kb_lo; kb < kb_hi; ++kb, rp.next(nst)) {
                     const uint32_t st = rp.st;
                     mbar_wait_sleep(&S.empty[st], rp.ph ^ 1);
                     unsigned char *sa = ring + (size_t)st * stage_bytes;
-                    const uint32_t bytes = ((p.dbg & 32) ? 0u : 2 * b_bytes) + ((p.dbg & 1) ? 0u : (uint32_t)A_TILE_BYTES);
+                    const uint32_t bytes = ((p.dbg & 32) ? 0u : 2 * b_bytes) + ((p.dbg & 1) ? 0u : A_BYTES);
                     if (bytes == 0) {
                         mbar_arrive(&S.loaded[st]);
                         continue;
                     }
                     mbar_arrive_expect_tx(&S.loaded[st], bytes);
                     if (!(p.dbg & 32))
-                        bulk_g2s(sa + A_TILE_BYTES, bt + (size_t)(kb0 + kb) * (2 * (size_t)BN * TC_KB), 2 * b_bytes,
+                        bulk_g2s(sa + A_BYTES, bt + (size_t)(kb0 + kb) * (2 * (size_t)BN * TC_KB), 2 * b_bytes,
                                  &S.loaded[st]);
-                    if (!(p.dbg & 1)) tma_load_2d(sa, &tmA, kstart + kb * TC_KB, mt * TC_BM, &S.loaded[st]);
+                    if (!(p.dbg & 1)) tma_load_2d(sa, &tmA, kstart + kb * KB, mt * TC_BM, &S.loaded[st]);
                     pf_issue();
                 }
             }
         }
     } else if (warp == W_MMA) {
         // ------------------------------------------------------------ MMA issuer
-        const uint32_t idesc = idesc_tf32(BN);
+        const uint32_t idesc = H16 ? idesc_f16(BN) : idesc_tf32(BN);
         RingPos rp;
         const uint32_t nst = (uint32_t)p.stages;
         uint32_t ch_it = 0;
@@ -463,20 +530,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t a_hi = tmem + (uint32_t)a_col0(BN) + st * A_STAGE_COLS;
-                        const uint32_t a_lo = a_hi + TC_KB;
-                        const uint32_t b_hi = smem_u32(ring + (size_t)st * stage_bytes + A_TILE_BYTES);
+                        const uint32_t a_lo = a_hi + A_STAGE_COLS / 2;
+                        const uint32_t b_hi = smem_u32(ring + (size_t)st * stage_bytes + A_BYTES);
                         const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
-                        for (int kk = 0; kk < TC_KB / 8; ++kk) {
-                            // K = 8 per MMA: 8 TMEM columns of A; 2 core matrices along K = 2 * LBO bytes of B
+                        for (int kk = 0; kk < 2; ++kk) {
+                            // K = 8 (tf32) / 16 (f16) per MMA: 8 TMEM columns of A; 2 core matrices (16 B rows)
+                            // along K = 2 * LBO bytes of B
                             const uint32_t bo = (uint32_t)kk * 2 * ((uint32_t)BN * 16);
                             const uint64_t dbh = umma_desc(b_hi + bo, (uint32_t)BN * 16, 128);
                             const uint64_t dbl = umma_desc(b_lo + bo, (uint32_t)BN * 16, 128);
                             const uint32_t first = (kb == cb && kk == 0) ? 0u : 1u;
                             if (p.dbg & 2) continue;
-                            tc_mma_tf32_ts(d, a_lo + 8 * kk, dbh, idesc, first);   // small terms first
-                            tc_mma_tf32_ts(d, a_hi + 8 * kk, dbl, idesc, 1u);
-                            tc_mma_tf32_ts(d, a_hi + 8 * kk, dbh, idesc, 1u);
+                            if constexpr (H16) {
+                                tc_mma_f16_ts(d, a_lo + 8 * kk, dbh, idesc, first);   // small terms first
+                                tc_mma_f16_ts(d, a_hi + 8 * kk, dbl, idesc, 1u);
+                                tc_mma_f16_ts(d, a_hi + 8 * kk, dbh, idesc, 1u);
+                            } else {
+                                tc_mma_tf32_ts(d, a_lo + 8 * kk, dbh, idesc, first);   // small terms first
+                                tc_mma_tf32_ts(d, a_hi + 8 * kk, dbl, idesc, 1u);
+                                tc_mma_tf32_ts(d, a_hi + 8 * kk, dbh, idesc, 1u);
+                            }
                         }
                         tc_commit(&S.empty[st]);
                     }
@@ -638,6 +712,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 mbar_arrive(&S.pempty[slot]);
             }
             // the tile's full sum is in registers; the MMAs of the next tile are already running
+            if constexpr (H16) {   // undo the power-of-two operand scales (exact)
+#pragma unroll
+                for (int j = 0; j < EPI_CH; ++j) {
+                    const int c0 = 32 * (cg + EPI_PER_Q * j);
+                    if (c0 >= BN) continue;
+                    const float4 *cs = reinterpret_cast<const float4 *>(p.colscale + n0 + c0);
+#pragma unroll
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        if (c0 + 4 * i4 >= BN) break;
+                        const float4 c = __ldg(cs + i4);
+                        acc[j][4 * i4] *= c.x;
+                        acc[j][4 * i4 + 1] *= c.y;
+                        acc[j][4 * i4 + 2] *= c.z;
+                        acc[j][4 * i4 + 3] *= c.w;
+                    }
+                }
+            }
             const int row = r0 + lane;
             const bool row_ok = row < p.M;
             double part = 0.0;
@@ -763,7 +854,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-int stages_for(int bn, int ring_off = RING_OFF) {
+int stages_for(int bn, int ring_off = RING_OFF, bool h16 = false) {
     // as many stages as shared memory and the TMEM A columns allow: with few row tiles the per-stage load
     // latency bounds a CTA (round 2, config 1: ~0.9k cycles per k-block at 8 stages whatever the width)
     static int cap = -1;
@@ -771,7 +862,7 @@ int stages_for(int bn, int ring_off = RING_OFF) {
         const char *e = getenv("NFHMM_TC_STAGES");   // A/B experiments
         cap = (e && atoi(e) >= 2 && atoi(e) <= MAX_STAGES) ? atoi(e) : MAX_STAGES;
     }
-    int s = (SMEM_MAX - ring_off) / stage_bytes_of(bn);
+    int s = (SMEM_MAX - ring_off) / stage_bytes_of(bn, h16);
     if (s > tmem_a_stages(bn)) s = tmem_a_stages(bn);
     return s > cap ? cap : s;
 }
@@ -798,20 +889,22 @@ cudaError_t make_map(CUtensorMap *m, const float *base, int64_t cols, int64_t ro
 
 // A [M][lda] (cols = lda); epilogue in / out [M][ldc]
 cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, float *eout, cudaStream_t st,
-                      const float *dvT = nullptr) {
+                      const float *dvT = nullptr, bool h16 = false) {
     const int g_num_sms = device_sms();
     if (p.bn < 16 || p.bn > TC_MAX_BN || p.bn % 16 || p.stages < 2) return cudaErrorInvalidValue;
     if (p.ring_off == 0) p.ring_off = RING_OFF;
-    const size_t smem = (size_t)p.ring_off + (size_t)p.stages * stage_bytes_of(p.bn);
+    const size_t smem = (size_t)p.ring_off + (size_t)p.stages * stage_bytes_of(p.bn, h16);
     if (smem > SMEM_MAX) return cudaErrorInvalidValue;
     const bool fused = p.mode == TC_DIRICHLET;
-    auto kern = fused ? tc_gemm_kernel<true> : tc_gemm_kernel<false>;
+    if (h16 && (fused || p.mode == TC_SEPARATE || p.mode == TC_BACKPROJ || !p.colscale)) return cudaErrorInvalidValue;
+    auto kern = fused ? tc_gemm_kernel<true, false> : h16 ? tc_gemm_kernel<false, true> : tc_gemm_kernel<false, false>;
     {
         cudaError_t e = ensure_dyn_smem((const void *)kern, SMEM_MAX);
         if (e != cudaSuccess) return e;
     }
     CUtensorMap mA, mIn, mOut, mDv;
-    cudaError_t e = make_map(&mA, A, lda, p.M, lda, TC_KB, TC_BM, CU_TENSOR_MAP_SWIZZLE_64B);
+    cudaError_t e = h16 ? make_map(&mA, A, lda, p.M, lda, TC_KB16, TC_BM, CU_TENSOR_MAP_SWIZZLE_128B)
+                        : make_map(&mA, A, lda, p.M, lda, TC_KB, TC_BM, CU_TENSOR_MAP_SWIZZLE_64B);
     if (e != cudaSuccess) return e;
     mIn = mA;
     mOut = mA;
@@ -836,7 +929,7 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
         if (ec && atoi(ec) > 0) chunk = atoi(ec);
     }
     p.dbg = dbg;
-    p.chunk_kb = chunk;
+    p.chunk_kb = h16 ? (chunk + 1) / 2 : chunk;   // the same 256 k-elements per accumulation slot
     kern<<<grid, TC_THREADS, smem, st>>>(mA, mIn, mOut, mDv, p);
     return cudaGetLastError();
 }
@@ -909,11 +1002,11 @@ __global__ void __launch_bounds__(256) tc_split_reduce_kernel(int mode, int spli
 }
 
 cudaError_t launch_split(TcParams p, const float *A, int lda, const float *ein, float *eout, int ldc, double *data_part,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool h16 = false) {
     const int mode = p.mode;
     p.mode = TC_PARTIAL;
     p.tma_epi = 0;
-    cudaError_t e = launch_tc(p, A, lda, nullptr, nullptr, st);
+    cudaError_t e = launch_tc(p, A, lda, nullptr, nullptr, st, nullptr, h16);
     if (e != cudaSuccess) return e;
     const int n_sub = (ldc + 15) / 16;
     const long long threads = (long long)p.M * n_sub;
@@ -974,6 +1067,51 @@ void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t
         }
 }
 
+size_t tc_presplit16_floats(int64_t n_rows, int64_t k_len, int bn) {
+    const int64_t nt = (n_rows + bn - 1) / bn, nkb = (k_len + TC_KB16 - 1) / TC_KB16;
+    return (size_t)nt * nkb * bn * TC_KB16;   // 2 x bn x 32 halves per chunk
+}
+
+// FP16 image of B[n][k] for the H16 reconstruction: row n scaled by 2^s_n so that its maximum lies in
+// [2^14, 2^15), then hi = rn_f16(x'), lo = rn_f16(x' - hi); chunk (nt, kb) = [hi: c8, r, 8][lo: c8, r, 8]
+// (c8 < 4: 8-element core-matrix rows of 16 bytes).  colscale[n] = 2^-(15 + s_n) undoes the B scale and
+// the converters' 2^15 scale of A; it is written for nt_n * bn columns (1 past n_rows).
+void tc_presplit16_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
+                        float *dst, float *colscale, int64_t k_pad) {
+    if (k_pad < k_len) k_pad = k_len;
+    const int64_t nt_n = (n_rows + bn - 1) / bn, nkb = (k_pad + TC_KB16 - 1) / TC_KB16;
+    auto get = [&](int64_t n, int64_t k) {
+        return (n < n_rows && k < k_len) ? (transposed ? src[(size_t)k * ld_src + n] : src[(size_t)n * ld_src + k]) : 0.f;
+    };
+    std::vector<float> sc((size_t)nt_n * bn, 1.f);
+    for (int64_t n = 0; n < nt_n * bn; ++n) {
+        float mx = 0.f;
+        for (int64_t k = 0; k < k_len && n < n_rows; ++k) mx = fmaxf(mx, get(n, k));
+        int e = 0;
+        if (mx > 0.f) {
+            frexpf(mx, &e);   // mx = f 2^e, f in [0.5, 1): scaled max 2^(15-e) mx in [2^14, 2^15)
+            e = 15 - e;
+        }
+        sc[n] = ldexpf(1.f, e);
+        colscale[n] = ldexpf(1.f, -(e + 15));
+    }
+    __half *h = reinterpret_cast<__half *>(dst);
+    for (int64_t nt = 0; nt < nt_n; ++nt)
+        for (int64_t kb = 0; kb < nkb; ++kb) {
+            __half *chunk = h + ((size_t)nt * nkb + kb) * 2 * bn * TC_KB16;
+            for (int r = 0; r < bn; ++r)
+                for (int kk = 0; kk < TC_KB16; ++kk) {
+                    const int64_t n = nt * bn + r, k = kb * TC_KB16 + kk;
+                    const float x = get(n, k) * sc[n];
+                    const __half hi = __float2half_rn(x);
+                    const __half lo = __float2half_rn(x - __half2float(hi));
+                    const size_t off = (size_t)(kk / 8) * (bn * 8) + (size_t)r * 8 + (kk % 8);
+                    chunk[off] = hi;
+                    chunk[(size_t)bn * TC_KB16 + off] = lo;
+                }
+        }
+}
+
 cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st) {
     TcParams p{};
     p.mode = a.R ? TC_RATIO : (a.out_src ? TC_SEPARATE : TC_STORE);
@@ -997,8 +1135,11 @@ cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st) {
     p.s = a.s;
     p.flags = a.flags;
     p.max_ctas = a.max_ctas;
+    const bool h16 = a.colscale != nullptr && p.mode != TC_SEPARATE;
+    p.colscale = a.colscale;
+    p.stages = stages_for(bn, RING_OFF, h16);
     if (p.mode == TC_RATIO && a.Vhat) return cudaErrorInvalidValue;   // RATIO always goes through TMA
-    return launch_tc(p, a.A, a.lda, a.V, a.R, st);
+    return launch_tc(p, a.A, a.lda, a.V, a.R, st, nullptr, h16);
 }
 
 cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st) {
@@ -1014,6 +1155,7 @@ cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaS
     p.Bsplit = a.Bsplit;
     p.nkb_total = a.nkb_total;
     p.ldc = a.ldb;
+    p.max_ctas = a.max_ctas;
     return launch_tc(p, a.A, a.lda, a.theta, a.n_out, st);
 }
 
@@ -1057,11 +1199,16 @@ cudaError_t launch_recon_tc_split(int bn, const ReconArgs &a, float *part, cudaS
     p.ldc = a.ldv;
     p.F = a.F;
     p.flags = a.flags;
-    p.splits = tc_split_count(a.k_end - (a.k_begin & ~(TC_KB - 1)));
+    p.max_ctas = a.max_ctas;
+    const bool h16 = a.colscale != nullptr;
+    p.colscale = a.colscale;
+    p.stages = stages_for(bn, RING_OFF, h16);
+    // ceil(k / 256) accumulation chunks either way (16 k-blocks of 16 or 8 of 32)
+    p.splits = tc_split_count(a.k_end - (a.k_begin & ~((h16 ? TC_KB16 : TC_KB) - 1)));
     p.part = part;
     p.ldp = p.n_tiles * bn;
     if (!a.R || a.Vhat || p.ldp < a.ldv) return cudaErrorInvalidValue;
-    return launch_split(p, a.A, a.lda, a.V, a.R, a.ldv, a.data_part, st);
+    return launch_split(p, a.A, a.lda, a.V, a.R, a.ldv, a.data_part, st, h16);
 }
 
 int tc_fused_blocks_per_chunk(int K) { return (2 * K - 2 + 32) / K; }

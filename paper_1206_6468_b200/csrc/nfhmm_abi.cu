@@ -32,6 +32,8 @@ struct nfhmm {
     float *bwd = nullptr, *ec = nullptr, *fwd = nullptr;   // FB messages b, u (q(D) = u .* b / sum), emissions
     float *vt = nullptr, *scale = nullptr, *vsrc = nullptr;
     float *bs_a = nullptr, *bs_b = nullptr;   // tensor-core path: pre-split beta for (a) and betaT for (b)
+    float *bs_a16 = nullptr, *csa = nullptr;  // 3xFP16 reconstruction: FP16 image of beta and its column scales
+    bool h16 = false;
     double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
     double *fconst = nullptr;   // per-frame alpha_0, psi(alpha_0), bound constant (set_observations)
     double *elbo_part = nullptr;   // [M][ELBO_MAX_BLOCKS] bound partial sums
@@ -44,6 +46,10 @@ struct nfhmm {
     // forward-backward overlapped with the reconstruction GEMM: the GEMM's persistent grid leaves
     // `overlap_sms` SMs to the latency-bound recursion, which runs on a side stream (fork / join events)
     int overlap_sms = 0, num_sms = 0;
+    // the next sweep's back-projection (b) joins the reconstruction in the forward-backward's shadow: (b) of
+    // sweep i+1 needs only R (from (a) of sweep i) and theta~, so the side-stream recursion overlaps (a) and
+    // (b); n_ready = n for the coming sweep already sits in the alpha buffer (never after a call's last sweep)
+    bool defer = false, n_ready = false;
     cudaStream_t fbst = nullptr;
     cudaEvent_t fev[2] = {nullptr, nullptr};
     int ldf = 0, nt_tc_b = 0;
@@ -199,6 +205,10 @@ size_t carve(nfhmm_t *h, char *base) {
     p = take((size_t)h->M * h->S * h->T * h->F * 4); h->vsrc = (float *)p;
     p = take(tc_presplit_floats(h->F, h->Kt, h->bn_tc_a) * 4); h->bs_a = (float *)p;
     p = take(tc_presplit_floats(h->Kt, h->Fa, h->bn_tc_b) * 4); h->bs_b = (float *)p;
+    if (h->h16) {
+        p = take(tc_presplit16_floats(h->F, h->Kt, h->bn_tc_a) * 4);  h->bs_a16 = (float *)p;
+        p = take((size_t)h->nt_tc_a * h->bn_tc_a * 4);               h->csa = (float *)p;
+    }
     if (h->fused) {
         const size_t sn = (size_t)h->S * h->N, ldf = (size_t)h->ldf;
         p = take(sn * ldf * 4);                  h->dvT = (float *)p;
@@ -236,6 +246,11 @@ int run_recon(nfhmm_t *h, int cls, ReconArgs a) {
         a.B = h->beta;      // [F_pad][Kt_pad], K-major rows
         a.Bsplit = h->bs_a;
         a.nkb_total = (h->Kt + 15) / 16;
+        if (h->h16 && !a.out_src) {   // A = theta~: the 3xFP16 products (DESIGN "3xFP16 reconstruction")
+            a.Bsplit = h->bs_a16;
+            a.nkb_total = (h->Kt + 31) / 32;
+            a.colscale = h->csa;
+        }
         a.ldb = h->Kb;
         a.n_tiles = h->nt_tc_a;
         if (h->split && a.R && !a.Vhat) {
@@ -280,8 +295,9 @@ DirichletArgs dirichlet_args(nfhmm_t *h, bool write_alpha);
 
 // (b) n = theta .* (R beta): the Eq. 6 data term  sum_l V_lt z_{t,l,k}; fused engine: (b) with the
 // element step of (c)+(d) in its epilogue (theta updated in place, alpha stored on the last sweep)
-int step_backproj(nfhmm_t *h, bool last = true) {
+int step_backproj(nfhmm_t *h, bool last = true, int max_ctas = 0) {
     BackprojArgs b{};
+    b.max_ctas = max_ctas;
     b.M = (int)h->frames;
     b.Kpad = h->Fa;
     b.A = h->R;
@@ -402,7 +418,8 @@ int sweep(nfhmm_t *h, bool last) {
         if (!r) r = step_backproj(h, last);
         if (!r) r = step_eq8(h);
     } else {
-        r = step_backproj(h);
+        if (!h->n_ready) r = step_backproj(h);
+        h->n_ready = false;
         if (!r) r = step_dirichlet(h, last);
     }
     if (r) return r;
@@ -424,6 +441,11 @@ int sweep(nfhmm_t *h, bool last) {
         r = step_fb(h);
         h->st = main_st;
         if (r) return r;
+        if (h->defer && !last && !h->fused) {   // (b) of sweep i+1, still beside the recursion
+            r = step_backproj(h, true, h->num_sms - h->overlap_sms);
+            if (r) return r;
+            h->n_ready = true;
+        }
         CU(h, cudaEventRecord(h->fev[1], h->fbst));
         CU(h, cudaStreamWaitEvent(h->st, h->fev[1], 0));
     } else {
@@ -474,6 +496,7 @@ int capture_sweep(nfhmm_t *h, bool last) {
     cudaStream_t user = h->st;
     const int64_t l0 = h->launches;
     const int done = h->iters_done;
+    const bool ready = h->n_ready;
     h->st = h->gst;
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamBeginCapture(h->gst, cudaStreamCaptureModeThreadLocal);
@@ -481,6 +504,7 @@ int capture_sweep(nfhmm_t *h, bool last) {
     cudaError_t e2 = cudaStreamEndCapture(h->gst, &g);
     h->st = user;
     h->iters_done = done;
+    h->n_ready = ready;
     const int64_t k = h->launches - l0;
     h->launches = l0;
     if (r) return r;
@@ -594,8 +618,13 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         // (with the multi-chain forward-backward, round 2: 0 / 20 / 24 / 32 / 40 SMs -> 72.8 / 78.8 / 82.6 /
         // 81.8 / 79.9 M frame-iterations/s; the one-chain kernel keeps 32)
         h->overlap_sms = (h->math == NFHMM_MATH_TC && frames > 65536 && h->fb_nchunk == 0) ? ((h->fb_multi == 2 && fb_mma_supported(h->N, h->M, 0)) ? 16 : (h->fb_multi && fb_multi_supported(h->N, h->M, 0)) ? 24 : 32) : 0;
+        // few chains (parallel-in-time forward-backward, single mixtures): the three phases of the
+        // recursion run beside (a) and (b) as well (their persistent grids keep 148 - 32 CTAs)
+        if (h->math == NFHMM_MATH_TC && h->fb_nchunk > 0) h->overlap_sms = 32;
         if (eo) h->overlap_sms = h->math == NFHMM_MATH_TC ? atoi(eo) : 0;
-        if (h->overlap_sms < 0 || h->overlap_sms > 64) h->overlap_sms = 0;
+        if (h->overlap_sms < 0 || h->overlap_sms > 96) h->overlap_sms = 0;
+        const char *ed2 = getenv("NFHMM_DEFER");   // 0: the next sweep's (b) waits for the recursion
+        h->defer = h->overlap_sms > 0 && !h->fused && !(ed2 && atoi(ed2) == 0);
     }
     {   // split-K for few row tiles: measured per k-block step ~0.6 us whatever the tile width, so
         // single-mixture contractions (8-16 row tiles, 50-75 k-blocks per CTA) are latency-bound; units of
@@ -611,6 +640,10 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         if (h->split) h->bn_tc_a = tc_pick_bn_split(F, frames, tc_split_count(Kt));
     }
     h->nt_tc_a = (int)((F + h->bn_tc_a - 1) / h->bn_tc_a);
+    {   // 3xFP16 reconstruction (tensor-core engine): NFHMM_RECON=tf32 selects the 3xTF32 products
+        const char *e = getenv("NFHMM_RECON");
+        h->h16 = h->math == NFHMM_MATH_TC && !(e && strcmp(e, "tf32") == 0);
+    }
     // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)
     h->c_prior_T = (double)T * (lgamma((double)Kt + o.gamma * S * K) - (double)S * K * lgamma(1.0 + o.gamma));
     // no CUDA call here: dims/layout/workspace queries work without a device; the first call that
@@ -650,7 +683,7 @@ int nfhmm_set_workspace(nfhmm_t *h, void *dptr, size_t bytes) {
     drop_graphs(h);   // the captured sweeps hold workspace pointers
     // zero everything once: all padding (bins >= F, elements >= Kt) stays zero for the handle's life
     CU(h, cudaMemsetAsync(h->ws, 0, need, h->st));
-    h->have_model = h->have_obs = h->R_valid = false;
+    h->have_model = h->have_obs = h->R_valid = h->n_ready = false;
     h->iters_done = 0;
     return NFHMM_OK;
 }
@@ -702,6 +735,14 @@ int nfhmm_set_model(nfhmm_t *h, const float *dict, const float *trans, const flo
         std::vector<float> bsa(tc_presplit_floats(h->F, h->Kt, h->bn_tc_a));
         std::vector<float> bsb(tc_presplit_floats(h->Kt, h->Fa, h->bn_tc_b));
         tc_presplit_host(hd.data(), h->F, /*transposed=*/true, h->F, h->Kt, h->bn_tc_a, bsa.data());    // B[n=l][k]
+        if (h->h16) {
+            std::vector<float> b16(tc_presplit16_floats(h->F, h->Kt, h->bn_tc_a));
+            std::vector<float> cs((size_t)h->nt_tc_a * h->bn_tc_a);
+            tc_presplit16_host(hd.data(), h->F, /*transposed=*/true, h->F, h->Kt, h->bn_tc_a, b16.data(), cs.data());
+            CU(h, cudaMemcpyAsync(h->bs_a16, b16.data(), b16.size() * 4, cudaMemcpyHostToDevice, h->st));
+            CU(h, cudaMemcpyAsync(h->csa, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, h->st));
+            CU(h, cudaStreamSynchronize(h->st));
+        }
         // B[n=k][l]: bins l < F, chunks laid out for the padded contraction Fa the kernel walks
         tc_presplit_host(hd.data(), h->F, /*transposed=*/false, h->Kt, h->F, h->bn_tc_b, bsb.data(), h->Fa);
         CU(h, cudaMemcpyAsync(h->bs_a, bsa.data(), bsa.size() * 4, cudaMemcpyHostToDevice, h->st));
@@ -712,7 +753,7 @@ int nfhmm_set_model(nfhmm_t *h, const float *dict, const float *trans, const flo
     CU(h, cudaMemcpyAsync(h->prior, hp.data(), np * 4, cudaMemcpyHostToDevice, h->st));
     CU(h, cudaStreamSynchronize(h->st));   // host vectors go out of scope
     h->have_model = true;
-    h->R_valid = false;
+    h->R_valid = h->n_ready = false;
     return NFHMM_OK;
 }
 
@@ -735,6 +776,7 @@ int nfhmm_reset(nfhmm_t *h) {
     CU(h, cudaMemsetAsync(h->flags + 1, 0, 2 * sizeof(unsigned), h->st));   // sweep counter, ELBO block count
     CU(h, cudaMemsetAsync(h->elbo_ctr, 0, (size_t)h->M * sizeof(unsigned), h->st));
     h->R_valid = false;
+    h->n_ready = false;
     r = recon_ratio(h);
     if (r) return r;
     h->R_valid = true;
@@ -764,7 +806,8 @@ int nfhmm_vb_iterate_async(nfhmm_t *h, int32_t n_iters) {
     int i = 0;
     // eager sweeps: profiling (per-launch events), short calls, and the first sweep of the handle
     const bool use_graphs = h->graphs && !h->prof && h->R_valid;
-    for (; i < n_iters && (!use_graphs || h->eager_sweeps == 0 || n_iters - i < 2); ++i) {
+    // (with the deferred back-projection the graphs start from n_ready: the call's first sweep runs eagerly)
+    for (; i < n_iters && (!use_graphs || h->eager_sweeps == 0 || n_iters - i < 2 || (h->defer && !h->n_ready)); ++i) {
         r = sweep(h, i == n_iters - 1);
         if (r) return r;
         h->eager_sweeps++;

@@ -38,8 +38,10 @@ struct ReconArgs {
     float *out_src;           // SEPARATE: V_src base for this source
     int T, S, s;              // SEPARATE: address ((m*S + s)*T + t)*F + l
     unsigned *flags;
-    const float *Bsplit;      // tensor-core path: pre-split, pre-tiled beta (tc_presplit_host)
+    const float *Bsplit;      // tensor-core path: pre-split, pre-tiled beta (tc_presplit_host / tc_presplit16_host)
     int nkb_total;
+    const float *colscale;    // non-NULL: FP16-split products (Bsplit from tc_presplit16_host, its column scales);
+                              // RATIO / STORE with A = theta~ only
     int max_ctas;             // tensor-core path: cap on the persistent grid (0 = one CTA per SM)
 };
 
@@ -54,6 +56,7 @@ struct BackprojArgs {
     float *n_out;             // [M][ldb]  n = theta .* (R beta)   (data term of Eq. 6)
     const float *Bsplit;      // tensor-core path: pre-split, pre-tiled betaT
     int nkb_total;
+    int max_ctas;             // tensor-core path: cap on the persistent grid (0 = one CTA per SM)
 };
 
 // Launchers (return cudaError_t of the launch).
@@ -70,6 +73,10 @@ int tc_pick_bn(int64_t n, int mult = 16, int64_t rows = 0, int sms = 148);
 size_t tc_presplit_floats(int64_t n_rows, int64_t k_len, int bn);
 void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
                       float *dst, int64_t k_pad = 0);
+// FP16 image for the 3xFP16 reconstruction (rows scaled by powers of two; colscale[nt_n * bn] undoes them)
+size_t tc_presplit16_floats(int64_t n_rows, int64_t k_len, int bn);
+void tc_presplit16_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
+                        float *dst, float *colscale, int64_t k_pad = 0);
 cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st);
 cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st);
 // Split-K reconstruction for few row tiles (single mixtures): tc_split_count(k) units of one TMEM accumulation chunk per

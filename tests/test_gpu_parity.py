@@ -298,3 +298,51 @@ def test_long_single_chain_parallel_scan_fits(chunk, monkeypatch):
         monkeypatch.setenv("NFHMM_FB_CHUNK", chunk)
     cfg, model, V = make_inputs(0, S=1, N=64, K=3, F=33, T=20000, M=1, counts=300)
     check_parity(cfg, model, V, 3)
+
+
+@pytest.mark.parametrize("c,over", [(0, {}), (1, dict(T=300)), (3, dict(T=200, M=3)), (4, dict(T=40, M=2))])
+def test_recon_tf32_variant_matches_3xfp16(c, over, monkeypatch):
+    """The default reconstruction runs 3xFP16 products (theta~ scaled by 2^15, dictionary rows by powers of two;
+    DESIGN "3xFP16 reconstruction"); NFHMM_RECON=tf32 selects the 3xTF32 products.  Both keep ~22 significant
+    bits per product, so they agree with each other and with the oracle."""
+    cfg, model, V = make_inputs(c, **over)
+    h16 = run_gpu(cfg, model, V, 5)
+    monkeypatch.setenv("NFHMM_RECON", "tf32")
+    tf = run_gpu(cfg, model, V, 5)
+    for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
+        assert rel_l2(h16[key], tf[key]) <= 3e-6, key
+    assert np.all(np.abs(h16["free_energy"] - tf["free_energy"]) <= 1e-7 * np.abs(tf["free_energy"]))
+    o1 = run_oracle(cfg, model, V[0], 1, separate=False)
+    g1 = run_gpu(cfg, model, V[:1], 1, separate=False)
+    compare(f"recon-h16:{cfg.name}/m0/sweep1", "V_hat", g1["V_hat"][0], o1["V_hat"], TOL1)
+    compare(f"recon-h16:{cfg.name}/m0/sweep1", "d_hat", g1["d_hat"][0], o1["d_hat"], TOL1)
+    o = run_oracle(cfg, model, V[0], 5)
+    assert rel_l2(h16["V_star"][0], o["V_star"]) <= TOL_VSTAR
+    assert np.all(np.abs(h16["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
+
+
+def test_recon_3xfp16_extreme_dynamic_range():
+    """Range stress for the 3xFP16 reconstruction: very sparse dictionaries (Dirichlet(0.05): entries down
+    to ~1e-30 beside ~1), frame masses from 1 to 10^7 counts (theta~ down to ~1e-8) and silent frames.
+    Products below the FP16 range of a row carry at most 2^-38 of that row's largest term (DESIGN), so
+    sweep-1 parity holds at the north-star tolerance."""
+    cfg, model, V = make_inputs(0, S=2, N=4, K=3, F=65, T=150, counts=1000)
+    rng = np.random.default_rng(1206)
+    beta = rng.dirichlet(np.full(cfg.F, 0.05), size=cfg.S * cfg.N * cfg.K).astype(np.float32)
+    beta = np.maximum(beta, np.float32(1e-30))
+    beta /= beta.sum(1, keepdims=True)
+    model.beta[...] = beta.reshape(model.beta.shape)
+    mass = 10.0 ** rng.uniform(0, 7, size=cfg.T)
+    V0 = np.zeros((1, cfg.T, cfg.F), np.float32)
+    W = rng.dirichlet(np.ones(cfg.S * cfg.N * cfg.K), size=cfg.T) @ beta
+    for t in range(cfg.T):
+        V0[0, t] = rng.multinomial(int(mass[t]), W[t] / W[t].sum())
+    V0[0, 5:8] = 0.0
+    o1 = run_oracle(cfg, model, V0[0], 1, separate=False)
+    g1 = run_gpu(cfg, model, V0, 1, separate=False)
+    for key, ref in (("V_hat", o1["V_hat"]), ("d_hat", o1["d_hat"]), ("alpha_hat", o1["alpha"])):
+        compare(f"recon-h16-range/m0/sweep1", key, g1[key][0], ref, TOL1)
+    o = run_oracle(cfg, model, V0[0], 8)
+    g = run_gpu(cfg, model, V0, 8)
+    assert rel_l2(g["V_star"][0], o["V_star"]) <= TOL_VSTAR
+    assert np.all(np.abs(g["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
