@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--mixtures", type=int, default=None, help="override total mixtures (default: config)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--math", choices=["tc", "simt"], default="tc",
-                    help="contraction engine: tcgen05 3xTF32 (default) or FP32 FFMA")
+                    help="contraction engine: tcgen05 split products (default: 3xFP16; NFHMM_RECON / NFHMM_BACKPROJ="
+                         "tf32 select 3xTF32) or FP32 FFMA")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-bound-off", action="store_true", help="skip the timing with the free energy off")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -396,6 +397,7 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     prof = h.profile_read()
+    products = h.products()   # how (a) / (b) form their products: 3xfp16 / 3xtf32 / ffma
     h.profile_enable(False)
     ms_per_step = elapsed / args.steps
     frame_iters = cfg.M * cfg.T * iters                     # whole job, all ranks
@@ -501,23 +503,27 @@ def run_ours(args):
         if k in ("recon", "backproj"):
             flops = 2.0 * frames_local * cfg.F * cfg.Kt       # algorithmic FLOPs per launch (true F, Kt)
             achieved = flops / t_launch / 1e12
-            if args.math == "tc":
-                # FP32 contraction as 3xTF32 on tcgen05: TF32 dense = measured bf16 x 1/2 (nominal 1.1 / 2.25
-                # PFLOP/s), three MMAs per product -> FP32-equivalent peak = TF32 / 3.  The GEMMs run inside
-                # a long step (hundreds of ms back to back, power-capped clocks), so the sustained bf16
-                # figure is the denominator (the recipe's rule); the burst-based fraction is reported too.
+            kind = products["recon" if k == "recon" else "backproj"]
+            if kind in ("3xtf32", "3xfp16"):
+                # FP32-accurate contraction as three split products on tcgen05.  3xTF32: TF32 dense = measured
+                # bf16 x 1/2 (nominal 1.1 / 2.25 PFLOP/s); 3xFP16: FP16 dense = the bf16 rate.  Three MMAs per
+                # product -> FP32-equivalent peak = that / 3.  The GEMMs run inside a long step (hundreds of
+                # ms back to back, power-capped clocks), so the sustained bf16 figure is the denominator (the
+                # recipe's rule); the burst-based fraction is reported too.
+                rate = 0.5 if kind == "3xtf32" else 1.0
                 bf16_s = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1645.8)))
                 bf16_b = float(peaks.get("bf16_tflops", 1645.8))
-                peak = bf16_s * 0.5 / 3.0
-                # also against the nominal dense peak (2.25 PFLOP/s bf16 -> 375 TFLOP/s 3xTF32)
+                peak = bf16_s * rate / 3.0
+                # also against the nominal dense peak (2.25 PFLOP/s bf16 -> 375 / 750 TFLOP/s)
                 # at the maximum and at the measured SM clock of the timed steps
-                nominal = 2250.0 * 0.5 / 3.0
+                nominal = 2250.0 * rate / 3.0
                 clk_mhz = (clk or {}).get("sm_mhz") or sm_max
-                return {"kernel": k, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                        "frac": achieved / peak, "frac_vs_burst": achieved / (bf16_b * 0.5 / 3.0),
+                dt = "TF32" if kind == "3xtf32" else "FP16"
+                return {"kernel": k, "bound": "tensor", "products": kind, "achieved": achieved, "peak": peak,
+                        "unit": "TFLOP/s", "frac": achieved / peak, "frac_vs_burst": achieved / (bf16_b * rate / 3.0),
                         "frac_vs_nominal_max_clock": achieved / nominal,
                         "frac_vs_nominal_at_clock": achieved / (nominal * clk_mhz / sm_max),
-                        "peak_note": f"3xTF32 FP32-equivalent: measured sustained bf16 {bf16_s} TF/s x 1/2 (TF32) / 3",
+                        "peak_note": f"3x{dt} FP32-equivalent: measured sustained bf16 {bf16_s} TF/s x {rate:g} ({dt}) / 3",
                         "fp32_ffma_peak": fp32_peak}
             return {"kernel": k, "bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                     "frac": achieved / fp32_peak, "peak_note": f"FP32 FFMA 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz"}
@@ -533,7 +539,7 @@ def run_ours(args):
 
     dom = max(("recon", "backproj", "dirichlet", "fb"), key=lambda k: prof[k][0])
     roof = roofline_of(dom)
-    roof_all = {k: {kk: v for kk, v in (roofline_of(k) or {}).items() if kk in ("bound", "achieved", "frac", "unit")}
+    roof_all = {k: {kk: v for kk, v in (roofline_of(k) or {}).items() if kk in ("bound", "achieved", "frac", "unit", "products")}
                 for k in ("recon", "backproj", "dirichlet", "fb")}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")

@@ -150,6 +150,17 @@ int nfhmm_kernel_launches(const nfhmm_t *h, int64_t *count);
 int nfhmm_layout(const nfhmm_t *h, int64_t *F_pad, int64_t *Kt_pad, int32_t *bn_recon,
                  int32_t *bn_backproj);
 
+/* How the two contractions of the sweep form their products (informational; DESIGN "3xFP16 products"):
+ *   NFHMM_PRODUCTS_FFMA   FP32 FFMA tiles (SIMT engine);
+ *   NFHMM_PRODUCTS_3XTF32 tcgen05 kind::tf32, x = hi + lo with hi = rn_tf32(x), three MMAs per product;
+ *   NFHMM_PRODUCTS_3XFP16 tcgen05 kind::f16, the operands scaled by exact powers of two and split into
+ *                         FP16 hi + lo (the same 11-bit significands as TF32), three MMAs per product.
+ * Either pointer may be NULL.  Returns NFHMM_EINVAL for h == NULL. */
+#define NFHMM_PRODUCTS_FFMA 0
+#define NFHMM_PRODUCTS_3XTF32 1
+#define NFHMM_PRODUCTS_3XFP16 2
+int nfhmm_products(const nfhmm_t *h, int32_t *recon, int32_t *backproj);
+
 /* Per-kernel-class device timing: when enabled, every launch on the handle's stream is bracketed by
  * CUDA events (no host synchronisation).  Classes: */
 #define NFHMM_K_RECON 0      /* (a) reconstruction GEMM + ratio epilogue (z-step, Eq. 7)          */

@@ -297,9 +297,24 @@ struct TcParams {
     float *part;
     int ldp;
     const float *colscale;  // H16: per output column 2^-(15 + s_l) (the B row scale and the A scale undone)
+    // H16 R scaling (DESIGN "3xFP16 products"): the reconstruction writes R' = c_l R (c_l = 2^30 colscale_l, a
+    // power of two ~ max_k beta_l(k)) and the largest R' of every row (float bits, atomicMax) to rowmax; the
+    // H16 back-projection scales row t of R' by 2^(14 - E_t) (E_t = exponent of rowmax[t]) and undoes it
+    unsigned *rowmax;
     int dbg;                // performance experiments only (NFHMM_TC_DEBUG): 1 no A loads, 2 no MMAs, 4 no epilogue
-                            // I/O, 8 no A TMEM stores, 32 no B loads, 64 no drains, 128 no converter work
+                            // I/O, 8 no A TMEM stores, 32 no B loads, 64 no drains, 128 no converter work,
+                            // 256 no L2 prefetch of the epilogue operand
 };
+
+// H16 back-projection: A scale 2^(14 - E) of row `row` (E = exponent of its largest R'; 1 for empty rows)
+__device__ __forceinline__ float row_a_scale(const TcParams &p, int row) {
+    if (row >= p.M) return 1.f;
+    const unsigned u = __ldg(p.rowmax + row);
+    if (u == 0u) return 1.f;
+    int e = (int)((u >> 23) & 0xFF) - 127;
+    e = min(max(e, -100), 100);
+    return __uint_as_float((uint32_t)(127 + 14 - e) << 23);
+}
 
 struct Smem {
     uint64_t full[MAX_STAGES], empty[MAX_STAGES], loaded[MAX_STAGES], pfull[2], pempty[2], ebar[EPI_WARPS];
@@ -377,6 +392,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ------------------------------------------------------------ converters (A operand -> TMEM)
         const int t = threadIdx.x;
         const uint32_t a_base = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)a_col0(BN);
+        float asc = 32768.f;   // H16: this row's A scale (set at the first k-block of each tile)
         RingPos rp;
         const uint32_t nst = (uint32_t)p.stages;
         for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
@@ -392,8 +408,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
                 const unsigned char *ab = ring + (size_t)st * stage_bytes;
                 if constexpr (H16) {
-                    // x' = 2^15 theta~ < 2^15: hi = rn_f16(x'), lo = rn_f16(x' - hi) (the difference is exact in
-                    // FP32), packed in pairs (element 2c in the low half of TMEM column c)
+                    // x' = 2^15 theta~ < 2^15 (recon) or 2^(14 - E_t) R'[t] (back-projection): hi = rn_f16(x'),
+                    // lo = rn_f16(x' - hi) (the difference is exact in FP32), packed in pairs (element 2c in the
+                    // low half of TMEM column c)
+                    if (kb == kb_lo) asc = p.mode == TC_BACKPROJ ? row_a_scale(p, mt_ * TC_BM + t) : 32768.f;
                     float x[TC_KB16];
 #pragma unroll
                     for (int c4 = 0; c4 < TC_KB16 / 4; ++c4) {
@@ -414,7 +432,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     uint32_t hi[16], lo[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
-                        const float a0 = x[2 * i] * 32768.f, a1 = x[2 * i + 1] * 32768.f;
+                        const float a0 = x[2 * i] * asc, a1 = x[2 * i + 1] * asc;
                         const __half2 h = __floats2half2_rn(a0, a1);
                         const float2 hf = __half22float2(h);
                         const __half2 l = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
@@ -687,7 +705,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int m0 = mt * TC_BM, n0 = nt * BN;
             const int r0 = m0 + 32 * q;            // first row of this warp's 32-row slice
             // chunk 0's operand lands while the tile accumulates; chunk 1's is fetched after chunk 0 left
-            if (tma_epi && lane == 0) fetch(0, n0, r0);
+            // (one buffer per warp), so it is pulled into L2 now: its fetch then waits on L2, not on HBM
+            if (tma_epi && lane == 0) {
+                fetch(0, n0, r0);
+#pragma unroll
+                for (int j = 1; j < EPI_CH && !(p.dbg & 256); ++j)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int c0 = 32 * (cg + EPI_PER_Q * j) + 16 * hh;
+                        if (c0 + 16 <= BN) tma_prefetch_2d(&tmIn, n0 + c0, r0);
+                    }
+            }
             __syncwarp();
             float e0f = 1.f;   // DIRICHLET: e^{-psi(alpha_0)} of this thread's frame
             if (fused && r0 + lane < p.M) e0f = (float)p.fconst[4 * (size_t)(r0 + lane) + 3];
@@ -712,7 +740,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 mbar_arrive(&S.pempty[slot]);
             }
             // the tile's full sum is in registers; the MMAs of the next tile are already running
-            if constexpr (H16) {   // undo the power-of-two operand scales (exact)
+            if (H16 && p.mode != TC_RATIO && p.mode != TC_PARTIAL) {   // undo the power-of-two operand scales (exact)
+                // (RATIO / PARTIAL keep the raw sums: R' = V / (2^-30 acc) and V_hat = colscale acc per element)
+                const float rf = p.mode == TC_BACKPROJ ? 1.f / row_a_scale(p, r0 + lane) * 32768.f : 1.f;
 #pragma unroll
                 for (int j = 0; j < EPI_CH; ++j) {
                     const int c0 = 32 * (cg + EPI_PER_Q * j);
@@ -722,16 +752,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     for (int i4 = 0; i4 < 8; ++i4) {
                         if (c0 + 4 * i4 >= BN) break;
                         const float4 c = __ldg(cs + i4);
-                        acc[j][4 * i4] *= c.x;
-                        acc[j][4 * i4 + 1] *= c.y;
-                        acc[j][4 * i4 + 2] *= c.z;
-                        acc[j][4 * i4 + 3] *= c.w;
+                        acc[j][4 * i4] *= c.x * rf;
+                        acc[j][4 * i4 + 1] *= c.y * rf;
+                        acc[j][4 * i4 + 2] *= c.z * rf;
+                        acc[j][4 * i4 + 3] *= c.w * rf;
                     }
                 }
             }
             const int row = r0 + lane;
             const bool row_ok = row < p.M;
             double part = 0.0;
+            float rmax = 0.f;      // RATIO: largest R' of this thread's columns (H16 back-projection scale)
             uint64_t hg2 = 0ull;   // DIRICHLET: packed running sum of g~ over this thread's columns
             if (tma_epi) {
 #pragma unroll
@@ -758,15 +789,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             const float4 x = *px;
                             const float xv[4] = {x.x, x.y, x.z, x.w};
                             float y[4];
+                            float4 cs4 = make_float4(1.f, 1.f, 1.f, 1.f);
+                            if (H16 && p.mode == TC_RATIO) cs4 = __ldg(reinterpret_cast<const float4 *>(p.colscale + n0 + c0) + i4);
+                            const float csv[4] = {cs4.x, cs4.y, cs4.z, cs4.w};
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
-                                const float vh = acc[j][16 * hh + 4 * i4 + e];
+                                const float a_ = acc[j][16 * hh + 4 * i4 + e];
+                                // H16: V_hat = colscale a_ (exact); R' = c_l R = V / (2^-30 a_)
+                                const float vh = (H16 && p.mode == TC_RATIO) ? a_ * csv[e] : a_;
                                 if (p.mode == TC_BACKPROJ) {
                                     y[e] = xv[e] * vh;                       // n = theta .* (R beta)
                                 } else {
                                     // R = V / V_hat: correctly rounded reciprocal times V (<= 1.5 ulp
                                     // of the quotient); log2 on the SFU, scaled by ln 2 per sub-tile
-                                    float rc = __frcp_rn(vh);
+                                    float rc = __frcp_rn((H16 && p.mode == TC_RATIO) ? a_ * 9.31322574615478515625e-10f : vh);
                                     y[e] = 0.f;
                                     if (xv[e] > 0.f) {
                                         if (vh > 0.f) {
@@ -776,6 +812,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                             bad |= FLAG_ZERO_SUPPORT;
                                         }
                                     }
+                                    rmax = fmaxf(rmax, y[e]);
                                 }
                             }
                             *px = make_float4(y[0], y[1], y[2], y[3]);
@@ -794,6 +831,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     }
                 }
                 if (!row_ok) part = 0.0;
+                if (p.rowmax && p.mode == TC_RATIO && row_ok && rmax > 0.f) atomicMax(p.rowmax + row, __float_as_uint(rmax));
             } else if (!FUSED) {
 #pragma unroll
                 for (int j = 0; j < EPI_CH; ++j) {
@@ -896,7 +934,8 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
     const size_t smem = (size_t)p.ring_off + (size_t)p.stages * stage_bytes_of(p.bn, h16);
     if (smem > SMEM_MAX) return cudaErrorInvalidValue;
     const bool fused = p.mode == TC_DIRICHLET;
-    if (h16 && (fused || p.mode == TC_SEPARATE || p.mode == TC_BACKPROJ || !p.colscale)) return cudaErrorInvalidValue;
+    if (h16 && (fused || p.mode == TC_SEPARATE || !p.colscale)) return cudaErrorInvalidValue;
+    if (h16 && p.mode == TC_BACKPROJ && !p.rowmax) return cudaErrorInvalidValue;
     auto kern = fused ? tc_gemm_kernel<true, false> : h16 ? tc_gemm_kernel<false, true> : tc_gemm_kernel<false, false>;
     {
         cudaError_t e = ensure_dyn_smem((const void *)kern, SMEM_MAX);
@@ -941,7 +980,8 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
 __global__ void __launch_bounds__(256) tc_split_reduce_kernel(int mode, int splits, const float *__restrict__ part,
                                                               int ldp, int M, int ldc, const float *__restrict__ ein,
                                                               float *__restrict__ eout, double *data_part, int n_sub,
-                                                              unsigned *flags) {
+                                                              unsigned *flags, const float *__restrict__ colscale,
+                                                              unsigned *rowmax) {
     const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const int row = (int)(id / n_sub), sub = (int)(id - (long long)row * n_sub);
     if (row >= M) return;
@@ -973,18 +1013,21 @@ __global__ void __launch_bounds__(256) tc_split_reduce_kernel(int mode, int spli
         }
         return;
     }
-    float lsum = 0.f;
+    float lsum = 0.f, rmax = 0.f;
     unsigned bad = 0;
 #pragma unroll
     for (int i4 = 0; i4 < 4; ++i4) {
         if (4 * i4 >= w) break;
         const float4 v4 = reinterpret_cast<const float4 *>(x)[i4];
         const float xv[4] = {v4.x, v4.y, v4.z, v4.w};
+        const float4 cs4 = colscale ? __ldg(reinterpret_cast<const float4 *>(colscale + c0) + i4) : make_float4(1.f, 1.f, 1.f, 1.f);
+        const float csv[4] = {cs4.x, cs4.y, cs4.z, cs4.w};
         float r[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const float vh = acc[4 * i4 + e];
-            const float rc = __frcp_rn(vh);
+            // H16 sums are raw: V_hat = colscale acc, R' = c_l R = V / (2^-30 acc) (as the tile epilogue)
+            const float vh = colscale ? acc[4 * i4 + e] * csv[e] : acc[4 * i4 + e];
+            const float rc = __frcp_rn(colscale ? acc[4 * i4 + e] * 9.31322574615478515625e-10f : vh);
             r[e] = 0.f;
             if (xv[e] > 0.f) {
                 if (vh > 0.f) {
@@ -994,9 +1037,11 @@ __global__ void __launch_bounds__(256) tc_split_reduce_kernel(int mode, int spli
                     bad |= FLAG_ZERO_SUPPORT;
                 }
             }
+            rmax = fmaxf(rmax, r[e]);
         }
         reinterpret_cast<float4 *>(y)[i4] = make_float4(r[0], r[1], r[2], r[3]);
     }
+    if (rowmax && rmax > 0.f) atomicMax(rowmax + row, __float_as_uint(rmax));
     if (data_part) data_part[(size_t)row * n_sub + sub] = rint(0.69314718055994530942 * 1048576.0 * (double)lsum);
     if (bad) atomicOr(flags, bad);
 }
@@ -1011,7 +1056,8 @@ cudaError_t launch_split(TcParams p, const float *A, int lda, const float *ein, 
     const int n_sub = (ldc + 15) / 16;
     const long long threads = (long long)p.M * n_sub;
     tc_split_reduce_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(mode, p.splits, p.part, p.ldp, p.M, ldc,
-                                                                            ein, eout, data_part, n_sub, p.flags);
+                                                                            ein, eout, data_part, n_sub, p.flags,
+                                                                            h16 ? p.colscale : nullptr, p.rowmax);
     return cudaGetLastError();
 }
 
@@ -1047,7 +1093,7 @@ size_t tc_presplit_floats(int64_t n_rows, int64_t k_len, int bn) {
 // column tile are laid out for k_pad >= k_len (the contraction length the kernel walks, nkb_total =
 // ceil(k_pad / 16)), so tile nt starts at chunk nt * nkb_total.
 void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
-                      float *dst, int64_t k_pad) {
+                      float *dst, int64_t k_pad, const float *kscale) {
     if (k_pad < k_len) k_pad = k_len;
     const int64_t nt_n = (n_rows + bn - 1) / bn, nkb = (k_pad + TC_KB - 1) / TC_KB;
     for (int64_t nt = 0; nt < nt_n; ++nt)
@@ -1058,6 +1104,7 @@ void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t
                     const int64_t n = nt * bn + r, k = kb * TC_KB + kk;
                     float x = 0.f;
                     if (n < n_rows && k < k_len) x = transposed ? src[(size_t)k * ld_src + n] : src[(size_t)n * ld_src + k];
+                    if (kscale && n < n_rows && k < k_len) x *= kscale[k];   // power of two: exact
                     const float hi = tf32_rn_bits(x);
                     const float lo = tf32_rn_bits(x - hi);
                     const size_t off = (size_t)(kk / 4) * (bn * 4) + (size_t)r * 4 + (kk % 4);
@@ -1077,11 +1124,13 @@ size_t tc_presplit16_floats(int64_t n_rows, int64_t k_len, int bn) {
 // (c8 < 4: 8-element core-matrix rows of 16 bytes).  colscale[n] = 2^-(15 + s_n) undoes the B scale and
 // the converters' 2^15 scale of A; it is written for nt_n * bn columns (1 past n_rows).
 void tc_presplit16_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
-                        float *dst, float *colscale, int64_t k_pad) {
+                        float *dst, float *colscale, int64_t k_pad, const float *kscale) {
     if (k_pad < k_len) k_pad = k_len;
     const int64_t nt_n = (n_rows + bn - 1) / bn, nkb = (k_pad + TC_KB16 - 1) / TC_KB16;
     auto get = [&](int64_t n, int64_t k) {
-        return (n < n_rows && k < k_len) ? (transposed ? src[(size_t)k * ld_src + n] : src[(size_t)n * ld_src + k]) : 0.f;
+        if (n >= n_rows || k >= k_len) return 0.f;
+        const float x = transposed ? src[(size_t)k * ld_src + n] : src[(size_t)n * ld_src + k];
+        return kscale ? x * kscale[k] : x;
     };
     std::vector<float> sc((size_t)nt_n * bn, 1.f);
     for (int64_t n = 0; n < nt_n * bn; ++n) {
@@ -1137,6 +1186,7 @@ cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st) {
     p.max_ctas = a.max_ctas;
     const bool h16 = a.colscale != nullptr && p.mode != TC_SEPARATE;
     p.colscale = a.colscale;
+    p.rowmax = p.mode == TC_RATIO ? a.rowmax : nullptr;
     p.stages = stages_for(bn, RING_OFF, h16);
     if (p.mode == TC_RATIO && a.Vhat) return cudaErrorInvalidValue;   // RATIO always goes through TMA
     return launch_tc(p, a.A, a.lda, a.V, a.R, st, nullptr, h16);
@@ -1156,7 +1206,11 @@ cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaS
     p.nkb_total = a.nkb_total;
     p.ldc = a.ldb;
     p.max_ctas = a.max_ctas;
-    return launch_tc(p, a.A, a.lda, a.theta, a.n_out, st);
+    const bool h16 = a.colscale != nullptr;   // 3xFP16 products on R' (rows scaled by 2^(14 - E_t))
+    p.colscale = a.colscale;
+    p.rowmax = h16 ? const_cast<unsigned *>(a.rowmax) : nullptr;
+    if (h16) p.stages = stages_for(bn, RING_OFF, true);
+    return launch_tc(p, a.A, a.lda, a.theta, a.n_out, st, nullptr, h16);
 }
 
 int tc_split_count(int64_t k_len) {
@@ -1202,6 +1256,7 @@ cudaError_t launch_recon_tc_split(int bn, const ReconArgs &a, float *part, cudaS
     p.max_ctas = a.max_ctas;
     const bool h16 = a.colscale != nullptr;
     p.colscale = a.colscale;
+    p.rowmax = a.rowmax;
     p.stages = stages_for(bn, RING_OFF, h16);
     // ceil(k / 256) accumulation chunks either way (16 k-blocks of 16 or 8 of 32)
     p.splits = tc_split_count(a.k_end - (a.k_begin & ~((h16 ? TC_KB16 : TC_KB) - 1)));

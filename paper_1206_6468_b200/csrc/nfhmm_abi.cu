@@ -34,6 +34,10 @@ struct nfhmm {
     float *bs_a = nullptr, *bs_b = nullptr;   // tensor-core path: pre-split beta for (a) and betaT for (b)
     float *bs_a16 = nullptr, *csa = nullptr;  // 3xFP16 reconstruction: FP16 image of beta and its column scales
     bool h16 = false;
+    // 3xFP16 back-projection (needs h16: the reconstruction then writes R' = c_l R and the per-row maxima)
+    float *bs_b16 = nullptr, *csb = nullptr;
+    unsigned *rowmax = nullptr;
+    bool h16b = false;
     double *eoff = nullptr, *logZ = nullptr, *data_part = nullptr, *hdir = nullptr, *fe = nullptr;
     double *fconst = nullptr;   // per-frame alpha_0, psi(alpha_0), bound constant (set_observations)
     double *elbo_part = nullptr;   // [M][ELBO_MAX_BLOCKS] bound partial sums
@@ -50,6 +54,7 @@ struct nfhmm {
     // sweep i+1 needs only R (from (a) of sweep i) and theta~, so the side-stream recursion overlaps (a) and
     // (b); n_ready = n for the coming sweep already sits in the alpha buffer (never after a call's last sweep)
     bool defer = false, n_ready = false;
+    bool fb_first = false;   // launch the recursion before the GEMM (few chains: the recursion is the longer branch)
     cudaStream_t fbst = nullptr;
     cudaEvent_t fev[2] = {nullptr, nullptr};
     int ldf = 0, nt_tc_b = 0;
@@ -208,6 +213,11 @@ size_t carve(nfhmm_t *h, char *base) {
     if (h->h16) {
         p = take(tc_presplit16_floats(h->F, h->Kt, h->bn_tc_a) * 4);  h->bs_a16 = (float *)p;
         p = take((size_t)h->nt_tc_a * h->bn_tc_a * 4);               h->csa = (float *)p;
+        p = take(fr * 4);                                            h->rowmax = (unsigned *)p;
+    }
+    if (h->h16b) {
+        p = take(tc_presplit16_floats(h->Kt, h->Fa, h->bn_tc_b) * 4); h->bs_b16 = (float *)p;
+        p = take((size_t)h->nt_tc_b * h->bn_tc_b * 4);               h->csb = (float *)p;
     }
     if (h->fused) {
         const size_t sn = (size_t)h->S * h->N, ldf = (size_t)h->ldf;
@@ -246,10 +256,12 @@ int run_recon(nfhmm_t *h, int cls, ReconArgs a) {
         a.B = h->beta;      // [F_pad][Kt_pad], K-major rows
         a.Bsplit = h->bs_a;
         a.nkb_total = (h->Kt + 15) / 16;
-        if (h->h16 && !a.out_src) {   // A = theta~: the 3xFP16 products (DESIGN "3xFP16 reconstruction")
+        if (h->h16 && !a.out_src) {   // A = theta~: the 3xFP16 products (DESIGN "3xFP16 products")
             a.Bsplit = h->bs_a16;
             a.nkb_total = (h->Kt + 31) / 32;
             a.colscale = h->csa;
+            if (a.R && h->h16b) a.rowmax = h->rowmax;   // per-row maxima of R' (3xFP16 back-projection;
+                                                          // zeroed by recon_ratio's caller)
         }
         a.ldb = h->Kb;
         a.n_tiles = h->nt_tc_a;
@@ -272,7 +284,10 @@ int data_tiles(const nfhmm_t *h) {
     return h->nt_a;
 }
 
-int recon_ratio(nfhmm_t *h, int max_ctas = 0) {
+// zero: clear the per-row maxima of R' first (the overlapped sweep clears them before its fork, so that no
+// memset kernel sits between the fork and the capped GEMM grid: the recursion's CTAs would take the SMs first)
+int recon_ratio(nfhmm_t *h, int max_ctas = 0, bool zero = true) {
+    if (zero && h->h16b) CU(h, cudaMemsetAsync(h->rowmax, 0, (size_t)h->frames * 4, h->st));
     ReconArgs a{};
     a.max_ctas = max_ctas;
     a.M = (int)h->frames;
@@ -324,6 +339,12 @@ int step_backproj(nfhmm_t *h, bool last = true, int max_ctas = 0) {
             d.alpha_out = last ? h->alpha : nullptr;
             LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj_dirichlet_tc(h->bn_tc_b, h->Kt, b, d, h->st));
             return NFHMM_OK;
+        }
+        if (h->h16b) {   // A = R' (rows scaled by 2^(14 - E_t)), B = beta^T / c_l in FP16
+            b.Bsplit = h->bs_b16;
+            b.nkb_total = (h->Fa + 31) / 32;
+            b.colscale = h->csb;
+            b.rowmax = h->rowmax;
         }
         LAUNCH(h, NFHMM_K_BACKPROJ, launch_backproj_tc(h->bn_tc_b, h->Kt, b, h->st));
     } else {
@@ -412,7 +433,7 @@ int sweep(nfhmm_t *h, bool last) {
         if (r) return r;
         h->R_valid = true;
     }
-    int r;
+    int r = NFHMM_OK;
     if (h->fused) {
         r = step_dv(h);
         if (!r) r = step_backproj(h, last);
@@ -432,15 +453,26 @@ int sweep(nfhmm_t *h, bool last) {
             CU(h, cudaEventCreateWithFlags(&h->fev[0], cudaEventDisableTiming));
             CU(h, cudaEventCreateWithFlags(&h->fev[1], cudaEventDisableTiming));
         }
+        if (h->h16b) CU(h, cudaMemsetAsync(h->rowmax, 0, (size_t)h->frames * 4, h->st));
         CU(h, cudaEventRecord(h->fev[0], h->st));
         CU(h, cudaStreamWaitEvent(h->fbst, h->fev[0], 0));
-        r = recon_ratio(h, h->num_sms - h->overlap_sms);
-        if (r) return r;
+        // launch order decides who takes the SMs first: the GEMM for many chains (its capped grid, the
+        // recursion in the rest), the recursion for few chains (there the recursion is the longer branch)
         cudaStream_t main_st = h->st;
-        h->st = h->fbst;
-        r = step_fb(h);
-        h->st = main_st;
+        if (h->fb_first) {
+            h->st = h->fbst;
+            r = step_fb(h);
+            h->st = main_st;
+            if (r) return r;
+        }
+        r = recon_ratio(h, h->num_sms - h->overlap_sms, false);
         if (r) return r;
+        if (!h->fb_first) {
+            h->st = h->fbst;
+            r = step_fb(h);
+            h->st = main_st;
+            if (r) return r;
+        }
         if (h->defer && !last && !h->fused) {   // (b) of sweep i+1, still beside the recursion
             r = step_backproj(h, true, h->num_sms - h->overlap_sms);
             if (r) return r;
@@ -625,6 +657,11 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         if (h->overlap_sms < 0 || h->overlap_sms > 96) h->overlap_sms = 0;
         const char *ed2 = getenv("NFHMM_DEFER");   // 0: the next sweep's (b) waits for the recursion
         h->defer = h->overlap_sms > 0 && !h->fused && !(ed2 && atoi(ed2) == 0);
+        // with the deferred (b) the multi-chain recursion hides behind (a) + (b): 16 SMs suffice (measured at
+        // config 3: 12 / 16 / 24 / 32 SMs -> 80.7 / 87.9 / 85.7 / 83.2 M; 24 without the deferral: 87.3 M)
+        if (!eo && h->defer && h->fb_nchunk == 0 && h->overlap_sms == 24) h->overlap_sms = 16;
+        const char *ef = getenv("NFHMM_FB_FIRST");
+        h->fb_first = ef ? atoi(ef) != 0 : h->fb_nchunk > 0;
     }
     {   // split-K for few row tiles: measured per k-block step ~0.6 us whatever the tile width, so
         // single-mixture contractions (8-16 row tiles, 50-75 k-blocks per CTA) are latency-bound; units of
@@ -643,6 +680,8 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
     {   // 3xFP16 reconstruction (tensor-core engine): NFHMM_RECON=tf32 selects the 3xTF32 products
         const char *e = getenv("NFHMM_RECON");
         h->h16 = h->math == NFHMM_MATH_TC && !(e && strcmp(e, "tf32") == 0);
+        const char *eb = getenv("NFHMM_BACKPROJ");   // tf32: the 3xTF32 back-projection (on R')
+        h->h16b = h->h16 && !h->fused && !(eb && strcmp(eb, "tf32") == 0);
     }
     // c_prior = lnGamma(Kt + gamma S K) - S K lnGamma(1 + gamma)  (Eq. 1 normaliser, DESIGN R8)
     h->c_prior_T = (double)T * (lgamma((double)Kt + o.gamma * S * K) - (double)S * K * lgamma(1.0 + o.gamma));
@@ -735,16 +774,29 @@ int nfhmm_set_model(nfhmm_t *h, const float *dict, const float *trans, const flo
         std::vector<float> bsa(tc_presplit_floats(h->F, h->Kt, h->bn_tc_a));
         std::vector<float> bsb(tc_presplit_floats(h->Kt, h->Fa, h->bn_tc_b));
         tc_presplit_host(hd.data(), h->F, /*transposed=*/true, h->F, h->Kt, h->bn_tc_a, bsa.data());    // B[n=l][k]
+        std::vector<float> kinv;   // H16: 1 / c_l per bin (R' = c_l R, so the back-projection contracts beta / c_l)
         if (h->h16) {
             std::vector<float> b16(tc_presplit16_floats(h->F, h->Kt, h->bn_tc_a));
             std::vector<float> cs((size_t)h->nt_tc_a * h->bn_tc_a);
             tc_presplit16_host(hd.data(), h->F, /*transposed=*/true, h->F, h->Kt, h->bn_tc_a, b16.data(), cs.data());
+            kinv.resize((size_t)h->F);
+            for (int64_t l = 0; l < h->F; ++l) kinv[l] = ldexpf(1.f, -30) / cs[l];   // exact (powers of two)
             CU(h, cudaMemcpyAsync(h->bs_a16, b16.data(), b16.size() * 4, cudaMemcpyHostToDevice, h->st));
             CU(h, cudaMemcpyAsync(h->csa, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, h->st));
             CU(h, cudaStreamSynchronize(h->st));
         }
+        if (h->h16b) {
+            std::vector<float> b16(tc_presplit16_floats(h->Kt, h->Fa, h->bn_tc_b));
+            std::vector<float> cs((size_t)h->nt_tc_b * h->bn_tc_b);
+            tc_presplit16_host(hd.data(), h->F, /*transposed=*/false, h->Kt, h->F, h->bn_tc_b, b16.data(), cs.data(), h->Fa,
+                               kinv.data());
+            CU(h, cudaMemcpyAsync(h->bs_b16, b16.data(), b16.size() * 4, cudaMemcpyHostToDevice, h->st));
+            CU(h, cudaMemcpyAsync(h->csb, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, h->st));
+            CU(h, cudaStreamSynchronize(h->st));
+        }
         // B[n=k][l]: bins l < F, chunks laid out for the padded contraction Fa the kernel walks
-        tc_presplit_host(hd.data(), h->F, /*transposed=*/false, h->Kt, h->F, h->bn_tc_b, bsb.data(), h->Fa);
+        tc_presplit_host(hd.data(), h->F, /*transposed=*/false, h->Kt, h->F, h->bn_tc_b, bsb.data(), h->Fa,
+                         h->h16 ? kinv.data() : nullptr);
         CU(h, cudaMemcpyAsync(h->bs_a, bsa.data(), bsa.size() * 4, cudaMemcpyHostToDevice, h->st));
         CU(h, cudaMemcpyAsync(h->bs_b, bsb.data(), bsb.size() * 4, cudaMemcpyHostToDevice, h->st));
         CU(h, cudaStreamSynchronize(h->st));
@@ -1025,6 +1077,14 @@ const char *nfhmm_last_error(const nfhmm_t *h) { return h ? h->err.c_str() : "";
 int nfhmm_kernel_launches(const nfhmm_t *h, int64_t *count) {
     if (!h || !count) return NFHMM_EINVAL;
     *count = h->launches;
+    return NFHMM_OK;
+}
+
+int nfhmm_products(const nfhmm_t *h, int32_t *recon, int32_t *backproj) {
+    if (!h) return NFHMM_EINVAL;
+    const bool tc = h->math == NFHMM_MATH_TC;
+    if (recon) *recon = !tc ? NFHMM_PRODUCTS_FFMA : h->h16 ? NFHMM_PRODUCTS_3XFP16 : NFHMM_PRODUCTS_3XTF32;
+    if (backproj) *backproj = !tc ? NFHMM_PRODUCTS_FFMA : h->h16b ? NFHMM_PRODUCTS_3XFP16 : NFHMM_PRODUCTS_3XTF32;
     return NFHMM_OK;
 }
 

@@ -41,7 +41,8 @@ struct ReconArgs {
     const float *Bsplit;      // tensor-core path: pre-split, pre-tiled beta (tc_presplit_host / tc_presplit16_host)
     int nkb_total;
     const float *colscale;    // non-NULL: FP16-split products (Bsplit from tc_presplit16_host, its column scales);
-                              // RATIO / STORE with A = theta~ only
+                              // RATIO / STORE with A = theta~ only; RATIO then writes R' = c_l R (c_l = 2^30 colscale_l)
+    unsigned *rowmax;         // H16 RATIO: per-row largest R' (float bits, atomicMax; zeroed by the caller)
     int max_ctas;             // tensor-core path: cap on the persistent grid (0 = one CTA per SM)
 };
 
@@ -57,6 +58,8 @@ struct BackprojArgs {
     const float *Bsplit;      // tensor-core path: pre-split, pre-tiled betaT
     int nkb_total;
     int max_ctas;             // tensor-core path: cap on the persistent grid (0 = one CTA per SM)
+    const float *colscale;    // non-NULL: 3xFP16 products (Bsplit from tc_presplit16_host of beta^T / c_l); A = R'
+    const unsigned *rowmax;   // with colscale: per-row largest R' (from the H16 reconstruction)
 };
 
 // Launchers (return cudaError_t of the launch).
@@ -72,11 +75,12 @@ int tc_pick_bn(int64_t n, int mult = 16, int64_t rows = 0, int sms = 148);
 // into tf32 hi/lo and re-tiled into the shared-memory image of each pipeline stage (host side, once).
 size_t tc_presplit_floats(int64_t n_rows, int64_t k_len, int bn);
 void tc_presplit_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
-                      float *dst, int64_t k_pad = 0);
+                      float *dst, int64_t k_pad = 0, const float *kscale = nullptr);
 // FP16 image for the 3xFP16 reconstruction (rows scaled by powers of two; colscale[nt_n * bn] undoes them)
 size_t tc_presplit16_floats(int64_t n_rows, int64_t k_len, int bn);
+// kscale (optional): element (n, k) is multiplied by kscale[k] first (the back-projection's 1 / c_l)
 void tc_presplit16_host(const float *src, int64_t ld_src, bool transposed, int64_t n_rows, int64_t k_len, int bn,
-                        float *dst, float *colscale, int64_t k_pad = 0);
+                        float *dst, float *colscale, int64_t k_pad = 0, const float *kscale = nullptr);
 cudaError_t launch_recon_tc(int bn, const ReconArgs &a, cudaStream_t st);
 cudaError_t launch_backproj_tc(int bn, int n_valid, const BackprojArgs &a, cudaStream_t st);
 // Split-K reconstruction for few row tiles (single mixtures): tc_split_count(k) units of one TMEM accumulation chunk per

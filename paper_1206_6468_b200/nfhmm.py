@@ -62,6 +62,7 @@ SIGNATURES = {
     "nfhmm_bench_kernel": (ctypes.c_int, [_P, ctypes.c_int, _I32, ctypes.POINTER(_D)]),
     "nfhmm_layout": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32),
                                     ctypes.POINTER(_I32)]),
+    "nfhmm_products": (ctypes.c_int, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
     # spectrogram front end / resynthesis
     "nfhmm_stft": (ctypes.c_int, [_P, _I64, _I64, _I32, _I32, ctypes.c_float, _P, _P, _I32, _P]),
     "nfhmm_istft": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I32, _I32, ctypes.c_float, _P, _I64, _I32, _P]),
@@ -196,6 +197,16 @@ def nfhmm_layout(h):
     return dict(F_pad=fp.value, Kt_pad=kp.value, bn_recon=br.value, bn_backproj=bb.value)
 
 
+PRODUCTS = {0: "ffma", 1: "3xtf32", 2: "3xfp16"}
+
+
+def nfhmm_products(h):
+    """Product splitting of the (a) reconstruction and (b) back-projection contractions (include/nfhmm.h)."""
+    r, b = ctypes.c_int32(), ctypes.c_int32()
+    _check(h, _lib.nfhmm_products(h, ctypes.byref(r), ctypes.byref(b)))
+    return dict(recon=PRODUCTS[r.value], backproj=PRODUCTS[b.value])
+
+
 KERNEL_CLASSES = ("recon", "backproj", "dirichlet", "fb", "elbo", "separate", "other")
 
 
@@ -283,6 +294,9 @@ class NFHMM:
 
     def layout(self):
         return nfhmm_layout(self.h)
+
+    def products(self):
+        return nfhmm_products(self.h)
 
     def profile_enable(self, on=True):
         nfhmm_profile_enable(self.h, on)

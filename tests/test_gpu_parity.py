@@ -211,7 +211,9 @@ def test_fused_dirichlet_epilogue_matches_separate_kernel(c, over, monkeypatch):
     fus = run_gpu(cfg, model, V, 5)
     for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
         assert rel_l2(fus[key], sep[key]) <= 2e-6, key
-    assert np.all(np.abs(fus["free_energy"] - sep["free_energy"]) <= 1e-7 * np.abs(sep["free_energy"]))
+    # the fused engine's back-projection is 3xTF32, the default's 3xFP16: the bound's data term moves by
+    # ~1e-7 relative (round 2 measured L vs the oracle after one sweep: 2.1e-7 for 3xTF32, 8e-8 for 3xFP16)
+    assert np.all(np.abs(fus["free_energy"] - sep["free_energy"]) <= 1e-6 * np.abs(sep["free_energy"]))
     o = run_oracle(cfg, model, V[0], 5)
     assert rel_l2(fus["V_star"][0], o["V_star"]) <= TOL_VSTAR
     assert np.all(np.abs(fus["free_energy"][0] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
@@ -307,11 +309,17 @@ def test_recon_tf32_variant_matches_3xfp16(c, over, monkeypatch):
     bits per product, so they agree with each other and with the oracle."""
     cfg, model, V = make_inputs(c, **over)
     h16 = run_gpu(cfg, model, V, 5)
-    monkeypatch.setenv("NFHMM_RECON", "tf32")
+    monkeypatch.setenv("NFHMM_BACKPROJ", "tf32")     # 3xFP16 reconstruction, 3xTF32 back-projection on R'
+    mixed = run_gpu(cfg, model, V, 5)
+    monkeypatch.setenv("NFHMM_RECON", "tf32")        # both 3xTF32 (plain R)
     tf = run_gpu(cfg, model, V, 5)
-    for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
-        assert rel_l2(h16[key], tf[key]) <= 3e-6, key
-    assert np.all(np.abs(h16["free_energy"] - tf["free_energy"]) <= 1e-7 * np.abs(tf["free_energy"]))
+    for other in (mixed, tf):
+        for key in ("d_hat", "alpha_hat", "V_hat", "V_star"):
+            assert rel_l2(h16[key], other[key]) <= 3e-6, key
+        # (the data term sum V log V_hat moves by ~1e-7 relative with V_hat's ~1e-6 rounding differences)
+        assert np.all(np.abs(h16["free_energy"] - other["free_energy"]) <= 1e-6 * np.abs(other["free_energy"]))
+    monkeypatch.delenv("NFHMM_RECON")
+    monkeypatch.delenv("NFHMM_BACKPROJ")
     o1 = run_oracle(cfg, model, V[0], 1, separate=False)
     g1 = run_gpu(cfg, model, V[:1], 1, separate=False)
     compare(f"recon-h16:{cfg.name}/m0/sweep1", "V_hat", g1["V_hat"][0], o1["V_hat"], TOL1)
@@ -322,8 +330,9 @@ def test_recon_tf32_variant_matches_3xfp16(c, over, monkeypatch):
 
 
 def test_recon_3xfp16_extreme_dynamic_range():
-    """Range stress for the 3xFP16 reconstruction: very sparse dictionaries (Dirichlet(0.05): entries down
-    to ~1e-30 beside ~1), frame masses from 1 to 10^7 counts (theta~ down to ~1e-8) and silent frames.
+    """Range stress for the 3xFP16 contractions: very sparse dictionaries (Dirichlet(0.05): entries down
+    to ~1e-30 beside ~1), frame masses from 1 to 10^7 counts (theta~ down to ~1e-8), silent frames and
+    counts in a bin no dictionary covers.
     Products below the FP16 range of a row carry at most 2^-38 of that row's largest term (DESIGN), so
     sweep-1 parity holds at the north-star tolerance."""
     cfg, model, V = make_inputs(0, S=2, N=4, K=3, F=65, T=150, counts=1000)
@@ -338,6 +347,10 @@ def test_recon_3xfp16_extreme_dynamic_range():
     for t in range(cfg.T):
         V0[0, t] = rng.multinomial(int(mass[t]), W[t] / W[t].sum())
     V0[0, 5:8] = 0.0
+    # mispredicted bins: counts where every dictionary is ~0 (R = V / V_hat huge: the back-projection's
+    # per-row A scale is set by these entries, the rest of the row sits far below its maximum)
+    l_bad = int(np.argmin(beta.max(0)))
+    V0[0, 20:30, l_bad] += np.float32(3.0)
     o1 = run_oracle(cfg, model, V0[0], 1, separate=False)
     g1 = run_gpu(cfg, model, V0, 1, separate=False)
     for key, ref in (("V_hat", o1["V_hat"]), ("d_hat", o1["d_hat"]), ("alpha_hat", o1["alpha"])):
