@@ -301,6 +301,7 @@ struct TcParams {
     // power of two ~ max_k beta_l(k)) and the largest R' of every row (float bits, atomicMax) to rowmax; the
     // H16 back-projection scales row t of R' by 2^(14 - E_t) (E_t = exponent of rowmax[t]) and undoes it
     unsigned *rowmax;
+    int a_prefetch;         // stages ahead at which the producer pulls A tiles into L2 (A_PREFETCH)
     int dbg;                // performance experiments only (NFHMM_TC_DEBUG): 1 no A loads, 2 no MMAs, 4 no epilogue
                             // I/O, 8 no A TMEM stores, 32 no B loads, 64 no drains, 128 no converter work,
                             // 256 no L2 prefetch of the epilogue operand
@@ -320,6 +321,20 @@ struct Smem {
     uint64_t full[MAX_STAGES], empty[MAX_STAGES], loaded[MAX_STAGES], pfull[2], pempty[2], ebar[EPI_WARPS];
     uint32_t tmem_base;
 };
+
+// One element of the RATIO epilogue, branch-free: R = V / V_hat as V times the SFU reciprocal of `den`
+// (V_hat, or V_hat / c_l for the H16 R'; rcp.approx: <= 1 ulp, so R is within 2 ulp), and V log2 V_hat (SFU)
+// added to the sub-tile's sum; V > 0 where V_hat = 0 raises the zero-support flag (R = 0 there).  Used by the
+// tile epilogue and by the split-K reduction alike, so split and unsplit results stay bitwise equal.
+__device__ __forceinline__ float ratio_elem(float v, float vh, float den, float &lsum, unsigned &bad) {
+    float rc;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(den));
+    const bool pos = v > 0.f, sup = vh > 0.f;
+    bad |= (pos && !sup) ? (unsigned)FLAG_ZERO_SUPPORT : 0u;
+    const bool use = pos && sup;
+    lsum = fmaf(use ? v : 0.f, __log2f(sup ? vh : 1.f), lsum);
+    return use ? v * rc : 0.f;
+}
 
 // 16-byte chunk c of row r in a TMA tile with 64-B rows, 64-byte swizzle (bits [4,5] ^= bits [7,8])
 __device__ __forceinline__ uint32_t swz64(int r, int c) { return (uint32_t)r * 64u + (uint32_t)((c ^ (r >> 1)) & 3) * 16u; }
@@ -430,12 +445,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             if (k0 + i < p.k_begin || k0 + i >= p.k_end) x[i] = 0.f;
                     }
                     uint32_t hi[16], lo[16];
+                    const uint64_t asc2 = f2c(asc);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const float a0 = x[2 * i] * asc, a1 = x[2 * i + 1] * asc;
+                    for (int i = 0; i < 16; ++i) {   // packed pairs: FMUL2, F2FP, 2 cvt, FADD2, F2FP per pair
+                        const uint64_t a2 = f2mul(f2pack(x[2 * i], x[2 * i + 1]), asc2);
+                        float a0, a1;
+                        f2unpack(a2, a0, a1);
                         const __half2 h = __floats2half2_rn(a0, a1);
                         const float2 hf = __half22float2(h);
-                        const __half2 l = __floats2half2_rn(a0 - hf.x, a1 - hf.y);
+                        float l0, l1;
+                        f2unpack(f2sub(a2, f2pack(hf.x, hf.y)), l0, l1);
+                        const __half2 l = __floats2half2_rn(l0, l1);
                         hi[i] = *reinterpret_cast<const uint32_t *>(&h);
                         lo[i] = *reinterpret_cast<const uint32_t *>(&l);
                     }
@@ -503,7 +523,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     tma_prefetch_2d(&tmA, kstart + pf_kb * KB, pf_mt * TC_BM);
                 if (pf_tile < n_total) pf_advance();
             };
-            for (int i = 0; i < A_PREFETCH; ++i) pf_issue();
+            for (int i = 0; i < p.a_prefetch; ++i) pf_issue();
             for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
                 int mt, nt, ks_, kb_lo, kb_hi;
                 unit_of(tile, mt, nt, ks_, kb_lo, kb_hi);
@@ -800,18 +820,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                 if (p.mode == TC_BACKPROJ) {
                                     y[e] = xv[e] * vh;                       // n = theta .* (R beta)
                                 } else {
-                                    // R = V / V_hat: correctly rounded reciprocal times V (<= 1.5 ulp
-                                    // of the quotient); log2 on the SFU, scaled by ln 2 per sub-tile
-                                    float rc = __frcp_rn((H16 && p.mode == TC_RATIO) ? a_ * 9.31322574615478515625e-10f : vh);
-                                    y[e] = 0.f;
-                                    if (xv[e] > 0.f) {
-                                        if (vh > 0.f) {
-                                            y[e] = xv[e] * rc;
-                                            lsum = fmaf(xv[e], __log2f(vh), lsum);
-                                        } else {
-                                            bad |= FLAG_ZERO_SUPPORT;
-                                        }
-                                    }
+                                    y[e] = ratio_elem(xv[e], vh, (H16 && p.mode == TC_RATIO) ? a_ * 9.31322574615478515625e-10f : vh,
+                                                      lsum, bad);
                                     rmax = fmaxf(rmax, y[e]);
                                 }
                             }
@@ -968,6 +978,12 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
         if (ec && atoi(ec) > 0) chunk = atoi(ec);
     }
     p.dbg = dbg;
+    static int apf = -1;
+    if (apf < 0) {
+        const char *e = getenv("NFHMM_TC_PREFETCH");   // A/B experiments
+        apf = (e && atoi(e) >= 0) ? atoi(e) : A_PREFETCH;
+    }
+    p.a_prefetch = apf;
     p.chunk_kb = h16 ? (chunk + 1) / 2 : chunk;   // the same 256 k-elements per accumulation slot
     kern<<<grid, TC_THREADS, smem, st>>>(mA, mIn, mOut, mDv, p);
     return cudaGetLastError();
@@ -1027,16 +1043,7 @@ __global__ void __launch_bounds__(256) tc_split_reduce_kernel(int mode, int spli
         for (int e = 0; e < 4; ++e) {
             // H16 sums are raw: V_hat = colscale acc, R' = c_l R = V / (2^-30 acc) (as the tile epilogue)
             const float vh = colscale ? acc[4 * i4 + e] * csv[e] : acc[4 * i4 + e];
-            const float rc = __frcp_rn(colscale ? acc[4 * i4 + e] * 9.31322574615478515625e-10f : vh);
-            r[e] = 0.f;
-            if (xv[e] > 0.f) {
-                if (vh > 0.f) {
-                    r[e] = xv[e] * rc;
-                    lsum = fmaf(xv[e], __log2f(vh), lsum);
-                } else {
-                    bad |= FLAG_ZERO_SUPPORT;
-                }
-            }
+            r[e] = ratio_elem(xv[e], vh, colscale ? acc[4 * i4 + e] * 9.31322574615478515625e-10f : vh, lsum, bad);
             rmax = fmaxf(rmax, r[e]);
         }
         reinterpret_cast<float4 *>(y)[i4] = make_float4(r[0], r[1], r[2], r[3]);
