@@ -42,6 +42,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "dirichlet_math.cuh"
@@ -158,6 +159,18 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int
                  "r"(c1), "r"(smem_u32(src))
                  : "memory");
 }
+// the same copy into the shared memory of every CTA in ctaMask (same CTA-relative offsets), each CTA's
+// mbarrier at bar's offset receiving the complete_tx
+__device__ __forceinline__ void bulk_g2s_mc(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
@@ -167,6 +180,14 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 
 __device__ __forceinline__ void tc_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+// arrive on the mbarrier at bar's offset in every CTA of ctaMask when this thread's MMAs complete
+__device__ __forceinline__ void tc_commit_mc(uint64_t *bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                     smem_u32(bar)),
+                 "h"(mask)
                  : "memory");
 }
 
@@ -301,6 +322,7 @@ struct TcParams {
     // power of two ~ max_k beta_l(k)) and the largest R' of every row (float bits, atomicMax) to rowmax; the
     // H16 back-projection scales row t of R' by 2^(14 - E_t) (E_t = exponent of rowmax[t]) and undoes it
     unsigned *rowmax;
+    int pair;               // 1: cluster of two CTAs sharing every B image by multicast (see the kernel)
     int a_prefetch;         // stages ahead at which the producer pulls A tiles into L2 (A_PREFETCH)
     int dbg;                // performance experiments only (NFHMM_TC_DEBUG): 1 no A loads, 2 no MMAs, 4 no epilogue
                             // I/O, 8 no A TMEM stores, 32 no B loads, 64 no drains, 128 no converter work,
@@ -341,7 +363,7 @@ __device__ __forceinline__ uint32_t swz64(int r, int c) { return (uint32_t)r * 6
 
 // FUSED: the DIRICHLET epilogue only (a separate instantiation keeps registers down).  H16: FP16-split
 // products (RATIO / STORE / PARTIAL of the reconstruction, A = theta~ in (0, 1])
-template <bool FUSED, bool H16>
+template <bool FUSED, bool H16, bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmIn,
                    const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmDv,
@@ -358,13 +380,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_mtiles = (p.M + TC_BM - 1) / TC_BM;
     const int splits = p.splits > 1 ? p.splits : 1;
-    const int n_total = n_mtiles * p.n_tiles * splits;
+    // PAIR (cluster of two CTAs, p.pair): the pair walks units (row-tile pair, column tile) together, rank r
+    // taking row tile 2 u_m + r; each CTA fetches half of every B image and multicasts it to both, so the
+    // dictionary crosses L2 -> SM once per two row tiles.  A row tile past the end computes on TMA zero
+    // fill and stores nothing (the tensor maps clip), so both CTAs see the same B sequence.
+    constexpr bool pair = PAIR;   // a separate instantiation: the unpaired kernels keep their code
+    uint32_t crank = 0;
+    if constexpr (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+    // first unit and stride of this CTA's walk, read at each use (as special registers: a variable held
+    // across the kernel measurably added spills to the 96-register roles)
+#define TC_U0 (PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x)
+#define TC_USTRIDE (PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x)
+    const int n_total = pair ? ((n_mtiles + 1) >> 1) * p.n_tiles : n_mtiles * p.n_tiles * splits;
     const int kstart = p.k_begin & ~(KB - 1);             // k-blocks on the global KB-element grid of Bsplit
     const int kb0 = kstart / KB;
     const int n_kb = (p.k_end - kstart + KB - 1) / KB;
     const int chunk_kb = p.chunk_kb;
     // work unit -> (row tile, column tile) and its k-blocks [kb_lo, kb_hi) (all of them unless split)
     auto unit_of = [&](int tile, int &mt, int &nt, int &ks, int &kb_lo, int &kb_hi) {
+        if (pair) {
+            const int um = tile / p.n_tiles;
+            nt = tile - um * p.n_tiles;
+            mt = 2 * um + (int)crank;
+            ks = 0;
+            kb_lo = 0;
+            kb_hi = n_kb;
+            return;
+        }
         ks = tile % splits;
         const int t2 = tile / splits;
         mt = t2 / p.n_tiles;
@@ -376,7 +418,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.stages; ++i) {
             mbar_init(&S.full[i], 128);      // the converters
-            mbar_init(&S.empty[i], 1);       // tcgen05.commit of the stage's MMAs
+            mbar_init(&S.empty[i], pair ? 2 : 1);   // tcgen05.commit of the stage's MMAs (PAIR: both CTAs')
             mbar_init(&S.loaded[i], 1);      // the producer's expect_tx (A + B bytes)
         }
         for (int i = 0; i < 2; ++i) {
@@ -400,6 +442,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (pair) cluster_sync();   // the peer's multicast copies and commits target these barriers
     tc_fence_after();
     const uint32_t tmem = S.tmem_base;
 
@@ -410,7 +453,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         float asc = 32768.f;   // H16: this row's A scale (set at the first k-block of each tile)
         RingPos rp;
         const uint32_t nst = (uint32_t)p.stages;
-        for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
+        for (int tile = TC_U0; tile < n_total; tile += TC_USTRIDE) {
             int mt_, nt_, ks_, kb_lo, kb_hi;
             unit_of(tile, mt_, nt_, ks_, kb_lo, kb_hi);
             for (int kb = kb_lo; kb < kb_hi; ++kb, rp.next(nst)) {
@@ -505,7 +548,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {
             RingPos rp;
             const uint32_t nst = (uint32_t)p.stages;
-            int pf_tile = blockIdx.x, pf_kb = 0, pf_mt = 0, pf_hi = 0;
+            int pf_tile = TC_U0, pf_kb = 0, pf_mt = 0, pf_hi = 0;
             {
                 int a_, b_, c_;
                 unit_of(pf_tile, pf_mt, a_, b_, pf_kb, pf_hi);
@@ -513,7 +556,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             auto pf_advance = [&]() {
                 if (++pf_kb == pf_hi) {
-                    pf_tile += gridDim.x;
+                    pf_tile += TC_USTRIDE;
                     int a_, b_;
                     if (pf_tile < n_total) unit_of(pf_tile, pf_mt, a_, b_, pf_kb, pf_hi);
                 }
@@ -524,7 +567,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 if (pf_tile < n_total) pf_advance();
             };
             for (int i = 0; i < p.a_prefetch; ++i) pf_issue();
-            for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
+            for (int tile = TC_U0; tile < n_total; tile += TC_USTRIDE) {
                 int mt, nt, ks_, kb_lo, kb_hi;
                 unit_of(tile, mt, nt, ks_, kb_lo, kb_hi);
                 const float *bt = p.Bsplit + (size_t)nt * p.nkb_total * (2 * (size_t)BN * TC_KB);   // same floats per block
@@ -538,9 +581,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         continue;
                     }
                     mbar_arrive_expect_tx(&S.loaded[st], bytes);
-                    if (!(p.dbg & 32))
-                        bulk_g2s(sa + A_BYTES, bt + (size_t)(kb0 + kb) * (2 * (size_t)BN * TC_KB), 2 * b_bytes,
-                                 &S.loaded[st]);
+                    if (!(p.dbg & 32)) {
+                        const float *bsrc = bt + (size_t)(kb0 + kb) * (2 * (size_t)BN * TC_KB);
+                        if (pair)   // this CTA's half ([hi] or [lo]) into both CTAs' stage
+                            bulk_g2s_mc(sa + A_BYTES + crank * b_bytes, bsrc + crank * (b_bytes / 4), b_bytes,
+                                        &S.loaded[st], 0x3);
+                        else
+                            bulk_g2s(sa + A_BYTES, bsrc, 2 * b_bytes, &S.loaded[st]);
+                    }
                     if (!(p.dbg & 1)) tma_load_2d(sa, &tmA, kstart + kb * KB, mt * TC_BM, &S.loaded[st]);
                     pf_issue();
                 }
@@ -552,7 +600,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         RingPos rp;
         const uint32_t nst = (uint32_t)p.stages;
         uint32_t ch_it = 0;
-        for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
+        for (int tile = TC_U0; tile < n_total; tile += TC_USTRIDE) {
             int mt_, nt_, ks_, kb_lo, kb_hi;
             unit_of(tile, mt_, nt_, ks_, kb_lo, kb_hi);
             for (int cb = kb_lo; cb < kb_hi; cb += chunk_kb, ++ch_it) {
@@ -590,7 +638,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                 tc_mma_tf32_ts(d, a_hi + 8 * kk, dbh, idesc, 1u);
                             }
                         }
-                        tc_commit(&S.empty[st]);
+                        if (pair) tc_commit_mc(&S.empty[st], 0x3);   // the peer's B half lives here too
+                        else tc_commit(&S.empty[st]);
                     }
                     __syncwarp();
                 }
@@ -719,7 +768,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int w = c0 + 32 <= BN ? 32 : 16;
             if (!((endm >> (w - 1)) & 1) && rok && rel <= nb_last) (rel == 0 ? dst0 : dstn)[(size_t)(bq + rel) * ldf + row] = sp;
         };
-        for (int tile = blockIdx.x; tile < n_total; tile += gridDim.x) {
+        for (int tile = TC_U0; tile < n_total; tile += TC_USTRIDE) {
             int mt, nt, ks, kb_lo, kb_hi;
             unit_of(tile, mt, nt, ks, kb_lo, kb_hi);
             const int m0 = mt * TC_BM, n0 = nt * BN;
@@ -894,6 +943,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (pair) cluster_sync();   // no multicast copy or commit may still target this CTA's shared memory
     if (warp == W_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
@@ -946,7 +996,21 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
     const bool fused = p.mode == TC_DIRICHLET;
     if (h16 && (fused || p.mode == TC_SEPARATE || !p.colscale)) return cudaErrorInvalidValue;
     if (h16 && p.mode == TC_BACKPROJ && !p.rowmax) return cudaErrorInvalidValue;
-    auto kern = fused ? tc_gemm_kernel<true, false> : h16 ? tc_gemm_kernel<false, true> : tc_gemm_kernel<false, false>;
+    const int n_mt = (p.M + TC_BM - 1) / TC_BM;
+    const int sms = (p.max_ctas > 0 && p.max_ctas < g_num_sms) ? p.max_ctas : g_num_sms;
+    // PAIR for the sweep's many-row-tile contractions (RATIO / BACKPROJ through TMA, unsplit, >= 2 row tiles
+    // per CTA); NFHMM_TC_PAIR=0 turns it off (A/B experiments)
+    const char *pev = getenv("NFHMM_TC_PAIR");   // read per launch (tests switch it within one process)
+    const int pair_env = pev ? atoi(pev) : -1;
+    // (measured at config 3: the back-projection, 17 k-blocks per tile, 88.7 -> 85.2 ms per step; the
+    // reconstruction, 25 k-blocks, unchanged; config 4 (33 / 250 k-blocks per tile) slower with it)
+    const int nkb_tile = (p.k_end - (p.k_begin & ~((h16 ? TC_KB16 : TC_KB) - 1)) + (h16 ? TC_KB16 : TC_KB) - 1) /
+                         (h16 ? TC_KB16 : TC_KB);
+    p.pair = (pair_env > 0 || (pair_env < 0 && nkb_tile <= 24)) && p.tma_epi && p.splits <= 1 && p.mode != TC_DIRICHLET &&
+             n_mt >= 2 * sms ? 1 : 0;
+    auto kern = fused ? tc_gemm_kernel<true, false, false>
+                : h16 ? (p.pair ? tc_gemm_kernel<false, true, true> : tc_gemm_kernel<false, true, false>)
+                      : (p.pair ? tc_gemm_kernel<false, false, true> : tc_gemm_kernel<false, false, false>);
     {
         cudaError_t e = ensure_dyn_smem((const void *)kern, SMEM_MAX);
         if (e != cudaSuccess) return e;
@@ -967,9 +1031,8 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
         if (e == cudaSuccess) e = make_map(&mOut, eout, p.ldc, p.M, p.ldc, 16, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (e != cudaSuccess) return e;
     }
-    const int n_total = ((p.M + TC_BM - 1) / TC_BM) * p.n_tiles * (p.splits > 1 ? p.splits : 1);
-    const int sms = (p.max_ctas > 0 && p.max_ctas < g_num_sms) ? p.max_ctas : g_num_sms;
-    const int grid = n_total < sms ? n_total : sms;
+    const int n_total = p.pair ? ((n_mt + 1) / 2) * p.n_tiles : n_mt * p.n_tiles * (p.splits > 1 ? p.splits : 1);
+    int grid = p.pair ? std::min(2 * n_total, sms & ~1) : (n_total < sms ? n_total : sms);
     static int dbg = -1, chunk = CHUNK_KB;
     if (dbg < 0) {
         const char *ev = getenv("NFHMM_TC_DEBUG");
@@ -985,6 +1048,21 @@ cudaError_t launch_tc(TcParams p, const float *A, int lda, const float *ein, flo
     }
     p.a_prefetch = apf;
     p.chunk_kb = h16 ? (chunk + 1) / 2 : chunk;   // the same 256 k-elements per accumulation slot
+    if (p.pair) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(TC_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, mA, mIn, mOut, mDv, p);
+    }
     kern<<<grid, TC_THREADS, smem, st>>>(mA, mIn, mOut, mDv, p);
     return cudaGetLastError();
 }

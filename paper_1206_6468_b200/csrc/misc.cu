@@ -65,11 +65,18 @@ __global__ void __launch_bounds__(256) elbo_kernel(ElboArgs p) {
     }
 }
 
-__global__ void init_state_kernel(int frames, int ld, int Kt, float a0, float th0, float *alpha, float *theta) {
+__device__ double digamma_fp64(double x);
+
+// DESIGN R5: alpha = a0 = 1 + gamma/N, theta~ = exp(psi(a0) - psi(Kt a0)) (uniform; FP64 digamma below)
+__global__ void init_state_kernel(int frames, int ld, int Kt, double a0, float *alpha, float *theta) {
+    __shared__ float th0_s;
+    if (threadIdx.x == 0) th0_s = (float)exp(digamma_fp64(a0) - digamma_fp64(a0 * (double)Kt));
+    __syncthreads();
+    const float th0 = th0_s, a0f = (float)a0;
     const size_t n = (size_t)frames * ld;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const int k = (int)(i % ld);
-        alpha[i] = k < Kt ? a0 : 0.f;
+        alpha[i] = k < Kt ? a0f : 0.f;
         theta[i] = k < Kt ? th0 : 0.f;
     }
 }
@@ -196,9 +203,9 @@ cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st) {
 }
 
 // alpha, theta of DESIGN R5; u = b = 1 so that the marginals u .* b / sum are the uniform d = 1/N
-cudaError_t launch_init_state(int frames, int ld, int Kt, float alpha0, float theta0, float *alpha, float *theta,
-                              float *u_fwd, float *b_bwd, long long d_count, cudaStream_t st) {
-    init_state_kernel<<<grid_for((size_t)frames * ld, 256), 256, 0, st>>>(frames, ld, Kt, alpha0, theta0, alpha, theta);
+cudaError_t launch_init_state(int frames, int ld, int Kt, double alpha0, float *alpha, float *theta, float *u_fwd,
+                              float *b_bwd, long long d_count, cudaStream_t st) {
+    init_state_kernel<<<grid_for((size_t)frames * ld, 256), 256, 0, st>>>(frames, ld, Kt, alpha0, alpha, theta);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     fill_kernel<<<grid_for((size_t)d_count, 256), 256, 0, st>>>(u_fwd, d_count, 1.f);

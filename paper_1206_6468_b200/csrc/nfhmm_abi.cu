@@ -813,17 +813,10 @@ int nfhmm_reset(nfhmm_t *h) {
     int r = enter(h);
     if (r) return r;
     if (!h->have_model || !h->have_obs) return fail(h, NFHMM_ESTATE, "set_model and set_observations must precede reset");
-    // DESIGN R5: alpha = 1 + gamma/N, d = 1/N; theta = exp(psi(alpha) - psi(Kt alpha)) (uniform)
+    // DESIGN R5: alpha = 1 + gamma/N, d = 1/N, theta~ uniform (init_state_kernel)
     const double a0 = 1.0 + h->gamma / h->N;
-    auto dg = [](double x) {
-        double res = 0.0;
-        while (x < 10.0) { res -= 1.0 / x; x += 1.0; }
-        const double f = 1.0 / (x * x);
-        return res + log(x) - 0.5 / x - f * (1.0 / 12 - f * (1.0 / 120 - f / 252));
-    };
-    const float th0 = (float)exp(dg(a0) - dg(a0 * h->Kt));
-    LAUNCH(h, NFHMM_K_OTHER, launch_init_state((int)h->frames, h->Kb, h->Kt, (float)a0, th0, h->alpha, h->theta, h->fwd,
-                                h->bwd, (long long)h->M * h->S * h->T * h->N, h->st));
+    LAUNCH(h, NFHMM_K_OTHER, launch_init_state((int)h->frames, h->Kb, h->Kt, a0, h->alpha, h->theta, h->fwd, h->bwd,
+                                (long long)h->M * h->S * h->T * h->N, h->st));
     CU(h, cudaMemsetAsync(h->fe, 0, (size_t)h->M * h->max_iters * 8, h->st));
     CU(h, cudaMemsetAsync(h->flags + 1, 0, 2 * sizeof(unsigned), h->st));   // sweep counter, ELBO block count
     CU(h, cudaMemsetAsync(h->elbo_ctr, 0, (size_t)h->M * sizeof(unsigned), h->st));

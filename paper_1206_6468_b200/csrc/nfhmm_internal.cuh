@@ -178,8 +178,8 @@ constexpr int ELBO_MAX_BLOCKS = 16;   // blocks per mixture (frames split so a s
 cudaError_t launch_elbo(const ElboArgs &a, cudaStream_t st);
 
 // Initial state (DESIGN R5): alpha = 1 + gamma/N, theta = exp(psi(a) - psi(Kt a)), d = 1/N.
-cudaError_t launch_init_state(int frames, int ld, int Kt, float alpha0, float theta0, float *alpha,
-                              float *theta, float *u_fwd, float *b_bwd, long long d_count, cudaStream_t st);
+cudaError_t launch_init_state(int frames, int ld, int Kt, double alpha0, float *alpha, float *theta, float *u_fwd,
+                              float *b_bwd, long long d_count, cudaStream_t st);
 // d[r][:] = u[r][:] .* b[r][:] / sum(u[r][:] .* b[r][:]) over rows of N (q(D) marginals from the FB messages)
 cudaError_t launch_marginals(const float *u, const float *b, float *d, long long rows, int N, cudaStream_t st);
 // betaT [rows][ldT] -> beta [ldT][ldb] transpose (rows = Kt, cols = F)

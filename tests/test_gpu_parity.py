@@ -264,6 +264,27 @@ def test_fb_overlap_is_bitwise_neutral(graphs, monkeypatch):
         assert np.array_equal(ov[key], seq[key]), key
 
 
+def test_cta_pair_multicast_is_bitwise_neutral(monkeypatch):
+    """Many row tiles: the contractions run as clusters of two CTAs that share every dictionary image by
+    TMA multicast (each fetches half).  297 row tiles (odd: the last pair's second CTA computes on zero
+    fill past the end and stores nothing) -- bitwise equal to the unpaired kernel, and the last mixture
+    (whose frames end in the unpaired tail) matches the oracle after one sweep and after four."""
+    cfg, model, V = make_inputs(3, M=19, T=2000)          # 38,000 frames = 297 row tiles of 128
+    paired = run_gpu(cfg, model, V, 4)
+    one = run_gpu(cfg, model, V, 1, separate=False)
+    monkeypatch.setenv("NFHMM_TC_PAIR", "0")
+    single = run_gpu(cfg, model, V, 4)
+    for key in ("d_hat", "alpha_hat", "V_hat", "V_star", "free_energy"):
+        assert np.array_equal(paired[key], single[key]), key
+    m = V.shape[0] - 1
+    o1 = run_oracle(cfg, model, V[m], 1, separate=False)
+    for key, okey in (("d_hat", "d_hat"), ("V_hat", "V_hat"), ("alpha_hat", "alpha")):
+        compare(f"pair:{cfg.name}:M19/m{m}/sweep1", key, one[key][m], o1[okey], TOL1)
+    o = run_oracle(cfg, model, V[m], 4)
+    assert rel_l2(paired["V_star"][m], o["V_star"]) <= TOL_VSTAR
+    assert np.all(np.abs(paired["free_energy"][m] - o["free_energy"]) <= TOL_L * np.abs(o["free_energy"]))
+
+
 @pytest.mark.parametrize("c,over", [(3, dict(T=40, M=21)), (0, dict(T=60, M=20)), (2, dict(T=30, M=13)),
                                     (3, dict(T=35, M=37, N=24))])
 def test_multi_chain_forward_backward(c, over, monkeypatch):
