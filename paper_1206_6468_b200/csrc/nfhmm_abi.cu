@@ -400,6 +400,10 @@ int step_eq8(nfhmm_t *h) {
 
 // (e) forward-backward per source
 int step_fb(nfhmm_t *h) {
+    // NFHMM_SKIP_FB=1: timing experiment only (what the sweep costs without the recursion; the posteriors
+    // are then wrong) -- used to measure how much of the forward-backward the overlap hides
+    static const int skip_fb = getenv("NFHMM_SKIP_FB") ? atoi(getenv("NFHMM_SKIP_FB")) : 0;
+    if (skip_fb) return NFHMM_OK;
     FBArgs f{};
     f.M = (int)h->M;
     f.S = h->S;
