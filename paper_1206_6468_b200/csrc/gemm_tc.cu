@@ -1,6 +1,9 @@
 // gemm_tc.cu -- the (a) reconstruction and (b) back-projection contractions on the 5th-generation tensor
-// cores (tcgen05, sm_100a) with 3xTF32 splitting, so the products keep FP32 accuracy (BASELINE north_star:
-// "SIMT FFMA tiles or 3xTF32 split tcgen05 with TMA-staged dictionary tiles in shared memory").
+// cores (tcgen05, sm_100a) with split products, so they keep FP32 accuracy (BASELINE north_star: "SIMT FFMA
+// tiles or 3xTF32 split tcgen05 with TMA-staged dictionary tiles in shared memory").  The default is the
+// H16 instantiation (3xFP16: kind::f16 at twice the TF32 rate, operands scaled by powers of two, DESIGN
+// "3xFP16 products"); the description below is of the 3xTF32 kernel, which H16 follows with 32-element
+// stages.  PAIR instantiations run as clusters of two CTAs that share every B image by TMA multicast.
 //
 // C[M x N] = A[M x K] * B[N x K]^T:
 //   (a) recon:    A = theta [frames][Kt_pad],  B = beta  (N = bins,     K = elements) -> V_hat   (Eq. 7)
