@@ -435,55 +435,88 @@ def run_ours(args):
         torch.cuda.empty_cache()
 
     # ---- e2e: public API with host buffers, copies inside the timed region -------------------
-    # Every step copies its V from pinned host memory, runs the sweeps and the separation, and reads
-    # the separated spectrograms back into pinned host memory.  Steps alternate between two handles on
-    # two streams (the public API's batch pipeline: nfhmm_separate_async + nfhmm_sync), so one step's
-    # host<->device copies run while the other step computes; the timed region spans all steps' copies.
+    # Every step copies its V from pinned host memory, runs the sweeps and the separation through the public
+    # API, and reads the separated spectrograms back into pinned host memory.  The host->device copy of a
+    # step (into one of two device input buffers) and the device->host copy of its V* (from one of two device
+    # output buffers) run on two copy streams beside the other steps' computes, ordered by events (a buffer
+    # is refilled only after the step that used it).  Large batches (> 65,536 frames: the GPU is full) run
+    # the steps back to back on one handle -- two handles on two streams let the steps' kernels interleave
+    # with the tuned SM partition and measured 5 % slower at config 3; small ones alternate between two
+    # handles on two streams, whose computes then overlap (single mixtures leave most SMs idle).
+    # The timed region spans every step's copies.
     e2e = None
     if not args.no_e2e:
         Vh = torch.from_numpy(V).pin_memory()
         out_h = [torch.empty((M, cfg.S, cfg.T, cfg.F), dtype=torch.float32).pin_memory() for _ in range(2)]
-        streams = [torch.cuda.Stream(dev) for _ in range(2)]
-        hs = [NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, device=dev, max_iters=max(iters, 1), stream=st,
-                    math=args.math) for st in streams]
-        for hh in hs:
-            hh.set_model(model.beta, model.trans, model.prior)
+        Vd = [torch.empty(Vh.shape, dtype=torch.float32, device=f"cuda:{dev}") for _ in range(2)]
+        out_d = [torch.empty(out_h[0].shape, dtype=torch.float32, device=f"cuda:{dev}") for _ in range(2)]
+        nh = 1 if M * cfg.T > 65536 else 2
+        csts = [torch.cuda.Stream(dev) for _ in range(nh)]      # the handles' compute streams
+        h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        hes = [NFHMM(cfg.F, cfg.T, cfg.S, cfg.N, cfg.K, n_mix=M, device=dev, max_iters=max(iters, 1), stream=c,
+                     math=args.math) for c in csts]
+        for he in hes:
+            he.set_model(model.beta, model.trans, model.prior)
+        ev_comp, ev_out = [None, None], [None, None]
 
         def e2e_step(i):
-            hh = hs[i % 2]
-            hh.set_observations(Vh)
-            hh.vb_iterate_async(iters)
-            hh.separate_into(out_h[i % 2], sync=False)
+            k = i % 2
+            he, cst = hes[i % nh], csts[i % nh]
+            with torch.cuda.stream(h2d):                  # V of step i into Vd[k] (free once step i-2 computed)
+                if ev_comp[k] is not None:
+                    h2d.wait_event(ev_comp[k])
+                Vd[k].copy_(Vh, non_blocking=True)
+                e_in = torch.cuda.Event()
+                e_in.record(h2d)
+            cst.wait_event(e_in)
+            if ev_out[k] is not None:                     # out_d[k] read back (step i-2)
+                cst.wait_event(ev_out[k])
+            he.set_observations(Vd[k])
+            he.vb_iterate_async(iters)
+            he.separate_into(out_d[k], sync=False)
+            e_c = torch.cuda.Event()
+            e_c.record(cst)
+            ev_comp[k] = e_c
+            with torch.cuda.stream(d2h):                  # V* of step i back to the host
+                d2h.wait_event(e_c)
+                out_h[k].copy_(out_d[k], non_blocking=True)
+                e_o = torch.cuda.Event()
+                e_o.record(d2h)
+            ev_out[k] = e_o
 
-        for i in range(2):   # warm both handles (graph capture, first-touch)
+        for i in range(2):   # warm up (graph capture, first-touch)
             e2e_step(i)
-        for hh in hs:
-            hh.sync()
         torch.cuda.synchronize()
+        for he in hes:
+            he.sync()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         j0 = torch.cuda.Event()
         e0.record(stream)
         j0.record(stream)
-        for st in streams:
+        for st in (*csts, h2d, d2h):
             st.wait_event(j0)
         for i in range(args.steps):
             e2e_step(i)
-        for st in streams:
+        for st in (*csts, h2d, d2h):
             stream.wait_stream(st)
         e1.record(stream)
         torch.cuda.synchronize()
-        for hh in hs:
-            hh.sync()   # sticky device flags of every step
+        for he in hes:
+            he.sync()   # sticky device flags of every step
         el = e0.elapsed_time(e1)
         if world > 1:
             el = pdist.max_over_ranks(el, device=f"cuda:{dev}")
         e2e = {"value": frame_iters / (el / args.steps / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": int(Vh.numel() * 4) * world, "d2h_bytes_per_step": int(out_h[0].numel() * 4) * world,
-               "ms_per_step": el / args.steps, "pipeline": "2 handles on 2 streams: copies of one step overlap the other's compute"}
-        for hh in hs:
-            hh.close()
+               "ms_per_step": el / args.steps,
+               "pipeline": (f"{nh} handle(s) on {nh} compute stream(s); each step's H2D and D2H on two copy streams "
+                            "beside the other steps' computes")}
+        for he in hes:
+            he.close()
+        del Vd, out_d
+        torch.cuda.empty_cache()
 
     # ---- roofline of the dominant kernel ------------------------------------------------------
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
