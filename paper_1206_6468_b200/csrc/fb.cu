@@ -1262,7 +1262,9 @@ int fb_pick_chunks(int64_t chains, int64_t T, int N, int *chunk_len) {
     // Parallel in time only while the sequential recursion would leave most of the GPU idle (at most
     // 32 chains -- e.g. single-mixture configurations), for N <= 64 (phase-2 smem) and long enough sequences.  Chunk length ~ sqrt(T): phase 1
     // costs ~L matrix products per chunk, phase 2 ~T/L vector-matrix products per chain.
-    if (chains > 32 || N > 64 || T < 96) return 0;
+    int max_chains = 32;
+    if (const char *e = getenv("NFHMM_FB_PARALLEL_MAX")) max_chains = atoi(e);   // experiments (chain bound)
+    if (chains > max_chains || N > 64 || T < 96) return 0;
     // chunk length ~ sqrt(2.3 T) in multiples of 16 (round 2 sweep, frame-iterations/s: config 1 (T = 1000)
     // L = 24 / 32 / 48 / 64 / 96 -> 7.3 / 7.6 / 8.2 / 7.9 / 7.4 M; config 2 (T = 2000) 32 / 48 / 64 / 96 ->
     // 9.5 / 10.2 / 10.3 / 10.2 M): the transfer and re-run phases cost ~L steps, the scan ~T / L chunks

@@ -645,15 +645,21 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         const char *em = getenv("NFHMM_FB_MULTI");
         // (the tensor-core kernel, NFHMM_FB_MULTI=2, measured 68 vs 90 ms per step alone but needs >= 16 SMs
         // beside the reconstruction GEMM and measured no faster there: 77.9 vs 80.1 M frame-iterations/s)
-        h->fb_multi = em ? atoi(em) : 1;
+        // (up to 64 chains the one-chain kernel, whose step is shorter, wins: at 32 mixtures of config 3 --
+        // the per-GPU share on 8 GPUs -- 68.6 -> 94.3 M frame-iterations/s; at 64 mixtures the multi-chain
+        // kernel, 103.6 vs 97.5 M)
+        h->fb_multi = em ? atoi(em) : (h->M * h->S > 64 ? 1 : 0);
         if (h->fb_multi < 0 || h->fb_multi > 2) h->fb_multi = 1;
-        // Large batches (> 65,536 frames, sequential forward-backward): the reconstruction GEMM leaves 32
-        // SMs to the forward-backward running beside it (measured at config 3: 16 / 24 / 32 / 40 / 48 / 64
+        // Sequential forward-backward: the reconstruction GEMM leaves 32 SMs to the forward-backward running
+        // beside it (measured at config 3: 16 / 24 / 32 / 40 / 48 / 64
         // reserved SMs -> -5 / -6 / +1.9 / +1.6 / -0.2 / -4.7 %).  NFHMM_OVERLAP=n overrides (0 = off).
         const char *eo = getenv("NFHMM_OVERLAP");
         // (with the multi-chain forward-backward, round 2: 0 / 20 / 24 / 32 / 40 SMs -> 72.8 / 78.8 / 82.6 /
         // 81.8 / 79.9 M frame-iterations/s; the one-chain kernel keeps 32)
-        h->overlap_sms = (h->math == NFHMM_MATH_TC && frames > 65536 && h->fb_nchunk == 0) ? ((h->fb_multi == 2 && fb_mma_supported(h->N, h->M, 0)) ? 16 : (h->fb_multi && fb_multi_supported(h->N, h->M, 0)) ? 24 : 32) : 0;
+        // (any batch size with the sequential recursion, round 2: at 32 mixtures -- the per-GPU share of
+        // config 3 on 8 GPUs, 64,000 frames -- the step is the recursion's latency and the overlap measured
+        // 49.5 -> 68.6 M frame-iterations/s; 8 to 24 SMs within 1 %)
+        h->overlap_sms = (h->math == NFHMM_MATH_TC && h->fb_nchunk == 0) ? ((h->fb_multi == 2 && fb_mma_supported(h->N, h->M, 0)) ? 16 : (h->fb_multi && fb_multi_supported(h->N, h->M, 0)) ? 24 : 32) : 0;
         // few chains (parallel-in-time forward-backward, single mixtures): the three phases of the
         // recursion run beside (a) and (b) as well (their persistent grids keep 148 - 32 CTAs)
         if (h->math == NFHMM_MATH_TC && h->fb_nchunk > 0) h->overlap_sms = 32;
@@ -875,6 +881,9 @@ int nfhmm_vb_iterate_async(nfhmm_t *h, int32_t n_iters) {
             h->launches += h->g_kernels;
             h->iters_done++;
         }
+        // the replays end with the call's last sweep, which defers nothing: the next call's first sweep
+        // must form n itself (capture_sweep restores the host flag it had before capturing)
+        h->n_ready = false;
         CU(h, cudaEventRecord(h->gev[1], h->gst));
         CU(h, cudaStreamWaitEvent(h->st, h->gev[1], 0));
     }

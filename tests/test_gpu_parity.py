@@ -104,8 +104,12 @@ def test_empty_frames_and_sharding_invariance():
     np.testing.assert_allclose(batched["V_star"][1].sum(0), V[1], rtol=1e-5, atol=1e-3)
 
 
-def test_resume_equals_single_call_and_device_io():
-    cfg, model, V = make_inputs(0)
+@pytest.mark.parametrize("c,over", [(0, {}), (1, dict(T=300)), (3, dict(M=6, T=120))])
+def test_resume_equals_single_call_and_device_io(c, over):
+    """Sweeps split over several calls equal one call, bitwise, and device I/O equals host I/O.  Covers the
+    CUDA-graph replays with the recursion beside the contractions and the deferred back-projection (config 0
+    and the batch: sequential recursion; config 1: parallel in time), whose state crosses call boundaries."""
+    cfg, model, V = make_inputs(c, **over)
     a = run_gpu(cfg, model, V, 7)
     b = run_gpu(cfg, model, V, 7, split=[3, 1, 3])
     c = run_gpu(cfg, model, V, 7, device_io=True)
@@ -292,6 +296,7 @@ def test_multi_chain_forward_backward(c, over, monkeypatch):
     remainder states spread over the lanes; M not a multiple of C leaves a partly empty group) agrees
     with the one-chain-per-warp kernel and with the oracle."""
     cfg, model, V = make_inputs(c, **over)
+    monkeypatch.setenv("NFHMM_FB_MULTI", "1")   # (the default for <= 64 chains is the one-chain kernel)
     multi = run_gpu(cfg, model, V, 4)
     if cfg.N % 8 == 0 and V.shape[0] >= 16:   # tensor-core variant (16 chains per warp, mma.sync 3xTF32)
         monkeypatch.setenv("NFHMM_FB_MULTI", "2")
