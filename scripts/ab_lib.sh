@@ -1,7 +1,9 @@
 #!/bin/bash
-# per-rank workloads of the 1/2/4/8-GPU config-3 runs on one GPU (defaults), then the GPU suite
+# config 0 / 2 with the overlap now on for every sequential recursion
 mkdir -p gpurun_out/ab
-b() { timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-bound-off --no-cpu-baseline "$@" 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']/1e6,3), round(d['ms_per_step'],3), d['clocks']['sm_mhz'], {k:round(v['ms_per_step'],1) for k,v in d['kernels'].items()})"; }
-for M in 32 64 128 256; do echo "M$M default: $(b --mixtures $M)" >> gpurun_out/ab/bench.log; done
-echo "cfg1 default: $(b --config 1)" >> gpurun_out/ab/bench.log
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/ab/pytest.log 2>&1; echo rc=$? >> gpurun_out/ab/pytest.log
+b() { timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-bound-off --no-cpu-baseline "$@" 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']/1e6,3), round(d['ms_per_step'],3), d['clocks']['sm_mhz'], {k:round(v['ms_per_step'],2) for k,v in d['kernels'].items()})"; }
+for rep in 1 2; do
+echo "cfg0 default: $(b --config 0)" >> gpurun_out/ab/bench.log
+echo "cfg0 overlap0: $(NFHMM_OVERLAP=0 b --config 0)" >> gpurun_out/ab/bench.log
+done
+echo "cfg2 default: $(b --config 2)" >> gpurun_out/ab/bench.log
