@@ -150,6 +150,20 @@ int nfhmm_kernel_launches(const nfhmm_t *h, int64_t *count);
 int nfhmm_layout(const nfhmm_t *h, int64_t *F_pad, int64_t *Kt_pad, int32_t *bn_recon,
                  int32_t *bn_backproj);
 
+/* Bounds checker (in place of compute-sanitizer, which this pool does not run).  When the
+ * environment variable NFHMM_GUARD=<bytes> (0 .. 2^30) is set at nfhmm_create, the workspace carries a
+ * guard zone before its first piece and after every piece: from the piece's exact end (its byte count,
+ * not its 256-byte rounding) to the next piece, at least <bytes> long.  nfhmm_set_workspace fills the
+ * zones with the byte 0xA5; nfhmm_workspace_size includes them.  nfhmm_guard_check synchronises the
+ * handle's streams and copies every zone to the host: *checked_bytes = the zone bytes inspected (0 when
+ * NFHMM_GUARD was unset), *bad_bytes = those no longer 0xA5, i.e. written by a kernel or copy outside
+ * the extent of a workspace piece.  Returns NFHMM_ECUDA if *bad_bytes > 0 (nfhmm_last_error names the
+ * first piece whose zone was hit, in carve order; -1 = before the first piece), NFHMM_ESTATE before a
+ * workspace exists, NFHMM_EINVAL for NULL arguments.  Debug/test instrument: reads of a zone are not
+ * detected here, but they see 0xA5 instead of 0, which the parity tests (bitwise against an unguarded
+ * handle) expose. */
+int nfhmm_guard_check(nfhmm_t *h, int64_t *checked_bytes, int64_t *bad_bytes);
+
 /* How the two contractions of the sweep form their products (informational; DESIGN "3xFP16 products"):
  *   NFHMM_PRODUCTS_FFMA   FP32 FFMA tiles (SIMT engine);
  *   NFHMM_PRODUCTS_3XTF32 tcgen05 kind::tf32, x = hi + lo with hi = rn_tf32(x), three MMAs per product;

@@ -77,6 +77,12 @@ struct nfhmm {
     int64_t g_kernels = 0;      // kernels per captured sweep
     int eager_sweeps = 0;       // sweeps run eagerly by this handle (capture only after one)
     unsigned *flags = nullptr;
+    // guard zones (NFHMM_GUARD=<bytes>, a bounds checker in place of compute-sanitizer): every workspace
+    // piece is followed (and the first preceded) by a zone filled with kGuardByte at set_workspace, from
+    // the piece's exact end; nfhmm_guard_check counts the zone bytes a kernel overwrote
+    size_t guard = 0;
+    struct Zone { size_t off, len; int piece; };
+    std::vector<Zone> zones;
 
     bool have_model = false, have_obs = false, R_valid = false;
     int iters_done = 0;
@@ -163,14 +169,22 @@ bool is_device_ptr(const void *p) {
 
 size_t al(size_t b) { return (b + 255) & ~size_t(255); }
 
+const int kGuardByte = 0xA5;
+
 // Carve (or just size) the workspace.  Order is fixed; sizes in bytes.
 size_t carve(nfhmm_t *h, char *base) {
     const size_t fr = (size_t)h->frames, Fa = h->Fa, Kb = h->Kb;
     const size_t chainTN = (size_t)h->M * h->S * h->T * h->N, chainT = (size_t)h->M * h->S * h->T;
-    size_t o = 0;
+    const size_t g = al(h->guard);
+    size_t o = g;
+    int piece = 0;
+    h->zones.clear();
+    if (g) h->zones.push_back({0, g, -1});
     auto take = [&](size_t bytes) {
         char *p = base ? base + o : nullptr;
-        o += al(bytes);
+        if (g) h->zones.push_back({o + bytes, al(bytes) - bytes + g, piece});
+        o += al(bytes) + g;
+        ++piece;
         return p;
     };
     char *p;
@@ -588,11 +602,15 @@ int nfhmm_create(int64_t F, int64_t T, int32_t S, int32_t N, int32_t K, const nf
         o.max_iters < 1 || (o.math != NFHMM_MATH_TC && o.math != NFHMM_MATH_SIMT))
         return NFHMM_EINVAL;
     if (N > 128) return NFHMM_EINVAL;  // forward-backward keeps <= 4 states per lane
+    const char *eg = getenv("NFHMM_GUARD");
+    const long long guard = eg ? atoll(eg) : 0;
+    if (guard < 0 || guard > (1LL << 30)) return NFHMM_EINVAL;
     const int64_t Kt = (int64_t)S * N * K;
     const int64_t frames = o.n_mix * T;
     if (Kt > (1 << 24) || F > (1 << 24) || frames > (int64_t)1 << 30) return NFHMM_EINVAL;
     nfhmm_t *h = new (std::nothrow) nfhmm;
     if (!h) return NFHMM_ENOMEM;
+    h->guard = (size_t)guard;
     h->F = F;
     h->T = T;
     h->S = S;
@@ -732,6 +750,8 @@ int nfhmm_set_workspace(nfhmm_t *h, void *dptr, size_t bytes) {
     drop_graphs(h);   // the captured sweeps hold workspace pointers
     // zero everything once: all padding (bins >= F, elements >= Kt) stays zero for the handle's life
     CU(h, cudaMemsetAsync(h->ws, 0, need, h->st));
+    for (const auto &z : h->zones)
+        CU(h, cudaMemsetAsync((char *)h->ws + z.off, kGuardByte, z.len, h->st));
     h->have_model = h->have_obs = h->R_valid = h->n_ready = false;
     h->iters_done = 0;
     return NFHMM_OK;
@@ -1091,6 +1111,31 @@ int nfhmm_products(const nfhmm_t *h, int32_t *recon, int32_t *backproj) {
     const bool tc = h->math == NFHMM_MATH_TC;
     if (recon) *recon = !tc ? NFHMM_PRODUCTS_FFMA : h->h16 ? NFHMM_PRODUCTS_3XFP16 : NFHMM_PRODUCTS_3XTF32;
     if (backproj) *backproj = !tc ? NFHMM_PRODUCTS_FFMA : h->h16b ? NFHMM_PRODUCTS_3XFP16 : NFHMM_PRODUCTS_3XTF32;
+    return NFHMM_OK;
+}
+
+int nfhmm_guard_check(nfhmm_t *h, int64_t *checked_bytes, int64_t *bad_bytes) {
+    int r = enter(h);
+    if (r) return r;
+    if (!checked_bytes || !bad_bytes) return fail(h, NFHMM_EINVAL, "null output pointer");
+    *checked_bytes = *bad_bytes = 0;
+    if (!h->ws) return fail(h, NFHMM_ESTATE, "no workspace");
+    CU(h, cudaStreamSynchronize(h->st));
+    if (h->fbst) CU(h, cudaStreamSynchronize(h->fbst));
+    if (h->gst) CU(h, cudaStreamSynchronize(h->gst));
+    std::vector<unsigned char> buf;
+    int first = -2;
+    for (const auto &z : h->zones) {
+        buf.resize(z.len);
+        CU(h, cudaMemcpy(buf.data(), (const char *)h->ws + z.off, z.len, cudaMemcpyDeviceToHost));
+        int64_t bad = 0;
+        for (unsigned char c : buf) bad += c != (unsigned char)kGuardByte;
+        if (bad && first == -2) first = z.piece;
+        *checked_bytes += (int64_t)z.len;
+        *bad_bytes += bad;
+    }
+    if (*bad_bytes) return fail(h, NFHMM_ECUDA, "%lld guard bytes overwritten (first after workspace piece %d)",
+                                (long long)*bad_bytes, first);
     return NFHMM_OK;
 }
 

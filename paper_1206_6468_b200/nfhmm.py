@@ -63,6 +63,7 @@ SIGNATURES = {
     "nfhmm_layout": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_I32),
                                     ctypes.POINTER(_I32)]),
     "nfhmm_products": (ctypes.c_int, [_P, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+    "nfhmm_guard_check": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     # spectrogram front end / resynthesis
     "nfhmm_stft": (ctypes.c_int, [_P, _I64, _I64, _I32, _I32, ctypes.c_float, _P, _P, _I32, _P]),
     "nfhmm_istft": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I32, _I32, ctypes.c_float, _P, _I64, _I32, _P]),
@@ -210,6 +211,16 @@ def nfhmm_products(h):
 KERNEL_CLASSES = ("recon", "backproj", "dirichlet", "fb", "elbo", "separate", "other")
 
 
+def nfhmm_guard_check(h):
+    """(checked_bytes, bad_bytes) of the workspace guard zones (NFHMM_GUARD, include/nfhmm.h); returns
+    rather than raises when zones were overwritten so the caller can report the counts."""
+    c, b = ctypes.c_int64(), ctypes.c_int64()
+    st = _lib.nfhmm_guard_check(h, ctypes.byref(c), ctypes.byref(b))
+    if st not in (0, NFHMM_ECUDA) or (st == NFHMM_ECUDA and b.value == 0):
+        _check(h, st)
+    return c.value, b.value, (_lib.nfhmm_last_error(h).decode() if st else "")
+
+
 def nfhmm_profile_enable(h, on=True):
     _check(h, _lib.nfhmm_profile_enable(h, 1 if on else 0))
 
@@ -297,6 +308,9 @@ class NFHMM:
 
     def products(self):
         return nfhmm_products(self.h)
+
+    def guard_check(self):
+        return nfhmm_guard_check(self.h)
 
     def profile_enable(self, on=True):
         nfhmm_profile_enable(self.h, on)

@@ -27,7 +27,7 @@ def make_inputs(c, **override):
 
 
 def run_gpu(cfg, model, V, iters, gamma=1.0, separate=True, max_iters=1024, device_io=False, split=None,
-            math="tc"):
+            math="tc", guard=False):
     """Run the CUDA path: set_model, set_observations, vb_iterate(iters) (optionally split into several
     calls), posteriors (+ separate).  Returns dict of host numpy arrays."""
     import torch
@@ -48,6 +48,8 @@ def run_gpu(cfg, model, V, iters, gamma=1.0, separate=True, max_iters=1024, devi
         vst, vs = h.separate(V_src=True)
         out["V_star"], out["V_src"] = vst, vs
     out["launches"] = h.kernel_launches()
+    if guard:   # NFHMM_GUARD zones of the workspace (include/nfhmm.h nfhmm_guard_check)
+        out["guard"] = h.guard_check()
     h.close()
     return out
 

@@ -121,3 +121,22 @@ def test_trainer_null_handle_calls_are_safe():
     assert lib.nhmm_train_em(None, 1) == n.NFHMM_EINVAL
     assert lib.nhmm_train_set_data(None, None) == n.NFHMM_EINVAL
     assert lib.nhmm_train_last_error(None) == b""
+
+
+def test_guard_zones_enlarge_the_workspace(monkeypatch):
+    """NFHMM_GUARD (include/nfhmm.h nfhmm_guard_check): a zone before the first piece and after each of
+    the >= 25 pieces, each >= the guard size; invalid sizes are rejected at create."""
+    from paper_1206_6468_b200 import nfhmm as n
+    monkeypatch.delenv("NFHMM_GUARD", raising=False)
+    h = n.nfhmm_create(33, 10, 2, 4, 3)
+    base = n.nfhmm_workspace_size(h)
+    n.nfhmm_destroy(h)
+    monkeypatch.setenv("NFHMM_GUARD", "1000")        # rounded up to 1024
+    h = n.nfhmm_create(33, 10, 2, 4, 3)
+    guarded = n.nfhmm_workspace_size(h)
+    n.nfhmm_destroy(h)
+    extra = guarded - base
+    assert extra % 1024 == 0 and extra // 1024 >= 26
+    monkeypatch.setenv("NFHMM_GUARD", "-1")
+    with pytest.raises(n.NFHMMError):
+        n.nfhmm_create(33, 10, 2, 4, 3)
