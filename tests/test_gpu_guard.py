@@ -113,3 +113,36 @@ def test_device_outputs_written_only_inside_their_extent():
     assert np.array_equal(outs["vst"][1].cpu().numpy(), vst_h)
     assert np.array_equal(outs["vs"][1].cpu().numpy(), vs_h)
     h.close()
+
+
+@pytest.mark.parametrize("win,hop,n", [(1024, 256, 16000 + 77), (64, 48, 1000), (8, 8, 8)])
+def test_stft_istft_device_outputs_inside_their_extent(win, hop, n):
+    """nfhmm_stft / nfhmm_istft into caller-owned device buffers (views into NaN-filled buffers, ragged
+    signal lengths): nothing outside the views changes, and the views equal the host-buffer outputs."""
+    import torch
+    from paper_1206_6468_b200 import nfhmm as nf
+    lib = nf.library()
+    rng = np.random.default_rng(1206)
+    x = rng.standard_normal((3, n)).astype(np.float32)
+    T, F = 1 + (n - win) // hop, win // 2 + 1
+    ref = nf.stft(x, win=win, hop=hop, gain=3.0)
+    xd = torch.from_numpy(x).cuda()
+    Xb, Xv = _sentinel((3, T, F, 2), torch.float32)
+    Vb, Vv = _sentinel((3, T, F), torch.float32)
+    st = lib.nfhmm_stft(xd.data_ptr(), 3, n, win, hop, 3.0, Xv.data_ptr(), Vv.data_ptr(), 0,
+                        nf._stream_ptr(None, 0))
+    assert st == 0
+    torch.cuda.synchronize()
+    for buf, view in ((Xb, Xv), (Vb, Vv)):
+        assert torch.isnan(buf[:4096]).all() and torch.isnan(buf[4096 + view.numel():]).all()
+    assert np.array_equal(Xv.cpu().numpy().view(np.complex64)[..., 0], ref["X"])
+    assert np.array_equal(Vv.cpu().numpy(), ref["V"])
+    M = np.stack([ref["V"] * 0.25, ref["V"] * 0.75], axis=1).astype(np.float32)      # [3][2][T][F]
+    y_ref = nf.istft(ref["X"], M, n, win=win, hop=hop, gain=3.0)
+    yb, yv = _sentinel((3, 2, n), torch.float32)
+    st = lib.nfhmm_istft(Xv.data_ptr(), torch.from_numpy(M).cuda().data_ptr(), 3, 2, T, win, hop, 3.0,
+                         yv.data_ptr(), n, 0, nf._stream_ptr(None, 0))
+    assert st == 0
+    torch.cuda.synchronize()
+    assert torch.isnan(yb[:4096]).all() and torch.isnan(yb[4096 + yv.numel():]).all()
+    assert np.array_equal(yv.cpu().numpy(), y_ref)
