@@ -894,6 +894,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
                 if (!row_ok) part = 0.0;
                 if (p.rowmax && p.mode == TC_RATIO && row_ok && rmax > 0.f) atomicMax(p.rowmax + row, __float_as_uint(rmax));
+            } else if (!FUSED && !H16 && !(p.dbg & 4) && (p.mode == TC_STORE || p.mode == TC_SEPARATE)) {
+                // V_hat / V_hat^(s) rows are F floats (F odd in general: no TMA map), so each 32 x 32 chunk is
+                // staged in the warp's epilogue tile (XOR swizzle: conflict-free both ways) and stored row by
+                // row, 32 lanes on 32 consecutive columns of one row (coalesced), instead of thread = row
+                float *tile = reinterpret_cast<float *>(etile);
+                size_t myoff = 0;
+                float sc = 1.f;
+                if (row_ok) {
+                    if (p.mode == TC_SEPARATE) {
+                        const int m = row / p.T, tt = row - m * p.T;
+                        myoff = ((size_t)(m * p.S + p.s) * p.T + tt) * p.F;
+                        sc = p.row_scale[row];
+                    } else {
+                        myoff = (size_t)row * p.F;
+                    }
+                }
+                float *const out = p.mode == TC_SEPARATE ? p.out_src : p.Vhat;
+                const int nrows = min(32, p.M - r0);
+#pragma unroll
+                for (int j = 0; j < EPI_CH; ++j) {
+                    const int c0 = 32 * (cg + EPI_PER_Q * j);
+                    const int colb = n0 + c0;
+                    if (c0 >= BN) continue;
+                    const int w = min(32, BN - c0);
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) tile[lane * 32 + (i ^ lane)] = acc[j][i] * sc;
+                    __syncwarp();
+                    const bool col_ok = lane < w && colb + lane < p.F;
+                    for (int r = 0; r < nrows; ++r) {
+                        const size_t off = __shfl_sync(0xffffffffu, (unsigned long long)myoff, r);
+                        if (col_ok) out[off + colb + lane] = tile[r * 32 + (lane ^ r)];
+                    }
+                }
             } else if (!FUSED) {
 #pragma unroll
                 for (int j = 0; j < EPI_CH; ++j) {
