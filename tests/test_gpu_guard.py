@@ -146,3 +146,37 @@ def test_stft_istft_device_outputs_inside_their_extent(win, hop, n):
     torch.cuda.synchronize()
     assert torch.isnan(yb[:4096]).all() and torch.isnan(yb[4096 + yv.numel():]).all()
     assert np.array_equal(yv.cpu().numpy(), y_ref)
+
+
+@pytest.mark.parametrize("c,over", [(0, {}), (4, dict(T=40, N=70, K=4, F=65)), (0, dict(T=1))])
+def test_trainer_device_outputs_inside_their_extent(c, over):
+    """nhmm_train_get into caller-owned device buffers (views into NaN-filled buffers): nothing outside
+    the views changes, and the views equal the host-buffer outputs (N-HMM EM training, NEXT-3)."""
+    import ctypes
+    import torch
+    from paper_1206_6468_b200 import nfhmm as nf
+    from paper_1206_6468_b200 import synth
+    cfg = synth.config(c, **over)
+    seed = synth.seed_of(c)
+    model = synth.make_model(cfg, seed)
+    V = synth.make_training_data(cfg, model, seed)
+    b0, a0, p0 = synth.make_em_init(cfg, seed)
+    S, T, N, K, F = V.shape[0], V.shape[1], cfg.N, cfg.K, cfg.F
+    tr = nf.NHMMTrainer(F, T, N, K, n_src=S, max_iters=4)
+    tr.set_data(V)
+    tr.set_params(b0, a0, p0)
+    tr.em(3)
+    host = tr.get()
+    outs = [_sentinel((S, N, K, F), torch.float32), _sentinel((S, N, N), torch.float32),
+            _sentinel((S, N), torch.float32), _sentinel((S, T, N, K), torch.float32),
+            _sentinel((S, 4), torch.float64)]
+    it = ctypes.c_int32()
+    st = nf.library().nhmm_train_get(tr.h, *[v.data_ptr() for _, v in outs], ctypes.byref(it))
+    assert st == 0 and it.value == 3
+    torch.cuda.synchronize()
+    for buf, view in outs:
+        assert torch.isnan(buf[:4096]).all() and torch.isnan(buf[4096 + view.numel():]).all()
+    for (_, view), key in zip(outs, ("dict", "trans", "prior", "weights")):
+        assert np.array_equal(view.cpu().numpy(), host[key]), key
+    assert np.array_equal(outs[4][1].cpu().numpy()[:, :3], host["loglik"])
+    tr.close()
