@@ -180,3 +180,16 @@ def test_trainer_device_outputs_inside_their_extent(c, over):
         assert np.array_equal(view.cpu().numpy(), host[key]), key
     assert np.array_equal(outs[4][1].cpu().numpy()[:, :3], host["loglik"])
     tr.close()
+
+
+@pytest.mark.parametrize("c,over,iters", [(3, dict(M=34, T=2000), 3), (1, dict(), 6), (3, dict(M=19, T=500), 4)])
+def test_repeated_runs_are_bitwise_identical(c, over, iters):
+    """Race detection without racecheck: the launch paths with concurrency between CTAs or streams (the
+    recursion beside the capped contractions on a side stream, CUDA graphs, CTA pairs sharing multicast
+    images and commit barriers, atomicMax row maxima, split-K partials, the parallel-in-time scan) run
+    four times on fresh handles; a data race would show up as run-to-run differences in some output."""
+    cfg, model, V = make_inputs(c, **over)
+    runs = [run_gpu(cfg, model, V, iters) for _ in range(4)]
+    for r in runs[1:]:
+        for key in KEYS:
+            assert np.array_equal(runs[0][key], r[key]), key
