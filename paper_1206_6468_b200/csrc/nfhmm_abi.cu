@@ -56,6 +56,9 @@ struct nfhmm {
     bool defer = false, n_ready = false;
     bool fb_first = false;   // launch the recursion before the GEMM (few chains: the recursion is the longer branch)
     cudaStream_t fbst = nullptr;
+    cudaStream_t pst = nullptr;    // NFHMM_PRIO=1 (experiment): the contractions of the overlapped sweep on a high-priority stream
+    cudaEvent_t pev = nullptr;
+    int prio = -1;
     cudaEvent_t fev[2] = {nullptr, nullptr};
     int ldf = 0, nt_tc_b = 0;
     // split-K reconstruction for few row tiles (single mixtures): units of one accumulation chunk + reduce
@@ -471,6 +474,16 @@ int sweep(nfhmm_t *h, bool last) {
             CU(h, cudaEventCreateWithFlags(&h->fev[0], cudaEventDisableTiming));
             CU(h, cudaEventCreateWithFlags(&h->fev[1], cudaEventDisableTiming));
         }
+        if (h->prio < 0) {
+            const char *ep = getenv("NFHMM_PRIO");
+            h->prio = (ep && atoi(ep) != 0 && !h->graphs) ? 1 : 0;
+            if (h->prio) {
+                int lo = 0, hi = 0;
+                CU(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                CU(h, cudaStreamCreateWithPriority(&h->pst, cudaStreamNonBlocking, hi));
+                CU(h, cudaEventCreateWithFlags(&h->pev, cudaEventDisableTiming));
+            }
+        }
         if (h->h16b) CU(h, cudaMemsetAsync(h->rowmax, 0, (size_t)h->frames * 4, h->st));
         CU(h, cudaEventRecord(h->fev[0], h->st));
         CU(h, cudaStreamWaitEvent(h->fbst, h->fev[0], 0));
@@ -483,7 +496,12 @@ int sweep(nfhmm_t *h, bool last) {
             h->st = main_st;
             if (r) return r;
         }
+        if (h->prio) {   // pending recursion CTAs must not take the SMs (a) frees ahead of (b)'s CTAs
+            CU(h, cudaStreamWaitEvent(h->pst, h->fev[0], 0));
+            h->st = h->pst;
+        }
         r = recon_ratio(h, h->num_sms - h->overlap_sms, false);
+        h->st = main_st;
         if (r) return r;
         if (!h->fb_first) {
             h->st = h->fbst;
@@ -492,9 +510,15 @@ int sweep(nfhmm_t *h, bool last) {
             if (r) return r;
         }
         if (h->defer && !last && !h->fused) {   // (b) of sweep i+1, still beside the recursion
+            if (h->prio) h->st = h->pst;
             r = step_backproj(h, true, h->num_sms - h->overlap_sms);
+            h->st = main_st;
             if (r) return r;
             h->n_ready = true;
+        }
+        if (h->prio) {
+            CU(h, cudaEventRecord(h->pev, h->pst));
+            CU(h, cudaStreamWaitEvent(h->st, h->pev, 0));
         }
         CU(h, cudaEventRecord(h->fev[1], h->fbst));
         CU(h, cudaStreamWaitEvent(h->st, h->fev[1], 0));
@@ -1080,6 +1104,8 @@ int nfhmm_destroy(nfhmm_t *h) {
     for (cudaEvent_t e : h->fev)
         if (e) cudaEventDestroy(e);
     if (h->fbst) cudaStreamDestroy(h->fbst);
+    if (h->pst) cudaStreamDestroy(h->pst);
+    if (h->pev) cudaEventDestroy(h->pev);
     if (h->ws_owned && h->ws) cudaFree(h->ws);
     delete h;
     return NFHMM_OK;
@@ -1122,6 +1148,7 @@ int nfhmm_guard_check(nfhmm_t *h, int64_t *checked_bytes, int64_t *bad_bytes) {
     if (!h->ws) return fail(h, NFHMM_ESTATE, "no workspace");
     CU(h, cudaStreamSynchronize(h->st));
     if (h->fbst) CU(h, cudaStreamSynchronize(h->fbst));
+    if (h->pst) CU(h, cudaStreamSynchronize(h->pst));
     if (h->gst) CU(h, cudaStreamSynchronize(h->gst));
     std::vector<unsigned char> buf;
     int first = -2;
